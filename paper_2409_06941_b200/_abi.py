@@ -1,0 +1,386 @@
+"""ctypes mirror of include/freeride.h.
+
+One binding serves every library that exports the header: the product
+(`_lib/libfreeride.so`) and, in tests only, the reference's own sources behind
+the oracle shim (`oracle/_ref/libbubblesim_ref.so`).  Status codes are mapped
+back onto the reference's exception types (types.hpp:22-42, task.hpp:62,
+pipeline.cpp:155) so callers see the reference's error behaviour.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+TASK_ID_MAX = 64
+
+FR_OK = 0
+FR_ERR_VALIDATION = 1
+FR_ERR_SCHEMA = 2
+FR_ERR_INVARIANT = 3
+FR_ERR_ILLEGAL_TRANSITION = 4
+FR_ERR_CAPACITY = 5
+FR_ERR_ARGUMENT = 6
+FR_ERR_NOT_FOUND = 7
+FR_ERR_UNSUPPORTED = 8
+FR_ERR_CUDA_BASE = 100
+
+tick = C.c_int64
+
+
+class FreeRideError(RuntimeError):
+    code = -1
+
+
+class ValidationError(FreeRideError):
+    """bubblesim::ValidationError (types.hpp:22): `.field` names the config field."""
+    code = FR_ERR_VALIDATION
+
+    def __init__(self, field, message):
+        super().__init__(message)
+        self.field = field
+
+
+class SchemaError(FreeRideError):
+    """bubblesim::SchemaError (types.hpp:34): `.path` names the document path."""
+    code = FR_ERR_SCHEMA
+
+    def __init__(self, path, message):
+        super().__init__(message)
+        self.path = path
+
+
+class IllegalTransition(FreeRideError):
+    """bubblesim::IllegalTransition (task.hpp:62)."""
+    code = FR_ERR_ILLEGAL_TRANSITION
+
+
+class InvariantError(FreeRideError):
+    """std::logic_error raised by the reference (e.g. pipeline.cpp:155)."""
+    code = FR_ERR_INVARIANT
+
+
+class CapacityError(FreeRideError):
+    code = FR_ERR_CAPACITY
+
+
+class CudaError(FreeRideError):
+    code = FR_ERR_CUDA_BASE
+
+
+class Struct(C.Structure):
+    def as_dict(self):
+        out = {}
+        for name, _ in self._fields_:
+            v = getattr(self, name)
+            if isinstance(v, bytes):
+                v = v.decode()
+            out[name] = v
+        return out
+
+
+class PipelineConfigC(Struct):
+    _fields_ = [
+        ("num_stages", C.c_int32),
+        ("num_micro_batches", C.c_int32),
+        ("num_epochs", C.c_int32),
+        ("n_fp", C.c_int32),
+        ("fp_duration", C.POINTER(tick)),
+        ("n_bp", C.c_int32),
+        ("n_stage_memory", C.c_int32),
+        ("bp_duration", C.POINTER(tick)),
+        ("stage_memory", C.POINTER(C.c_double)),
+        ("gpu_memory_total", C.c_double),
+        ("tick_seconds", C.c_double),
+    ]
+
+
+class Issue(Struct):
+    _fields_ = [("kind", C.c_int32), ("micro_batch", C.c_int32)]
+
+
+class OpEventC(Struct):
+    _fields_ = [
+        ("stage", C.c_int32),
+        ("kind", C.c_int32),
+        ("micro_batch", C.c_int32),
+        ("epoch", C.c_int32),
+        ("start", tick),
+        ("end", tick),
+    ]
+
+
+class BubbleC(Struct):
+    _fields_ = [
+        ("stage", C.c_int32),
+        ("epoch", C.c_int32),
+        ("start", tick),
+        ("duration", tick),
+        ("available_memory", C.c_double),
+        ("btype", C.c_int32),
+        ("reserved", C.c_int32),
+        ("prev_op", C.c_int64),
+        ("next_op", C.c_int64),
+    ]
+
+
+class SideTaskSpecC(Struct):
+    _fields_ = [
+        ("id", C.c_char * TASK_ID_MAX),
+        ("interface_kind", C.c_int32),
+        ("misbehavior", C.c_int32),
+        ("has_total_steps", C.c_int32),
+        ("has_memory_limit", C.c_int32),
+        ("has_reference_throughput", C.c_int32),
+        ("reserved", C.c_int32),
+        ("per_step_duration", tick),
+        ("total_steps", C.c_int64),
+        ("init_duration", tick),
+        ("memory_demand", C.c_double),
+        ("leak_rate_gib_per_s", C.c_double),
+        ("submit_time", tick),
+        ("memory_limit", C.c_double),
+        ("reference_throughput", C.c_double),
+    ]
+
+
+class TaskRuntimeC(Struct):
+    _fields_ = [
+        ("state", C.c_int32),
+        ("has_last_paused", C.c_int32),
+        ("has_assigned_worker", C.c_int32),
+        ("assigned_worker", C.c_int32),
+        ("has_busy_until", C.c_int32),
+        ("reserved", C.c_int32),
+        ("steps_completed", C.c_int64),
+        ("memory_allocated", C.c_double),
+        ("last_paused", tick),
+        ("busy_until", tick),
+        ("memory_demand", C.c_double),
+    ]
+
+
+class IterativeDecisionC(Struct):
+    _fields_ = [("run", C.c_int32), ("reserved", C.c_int32), ("step_end", tick)]
+
+
+class LimitConfigC(Struct):
+    _fields_ = [
+        ("grace_period", tick),
+        ("memory_headroom", C.c_double),
+        ("reclamation_delay", tick),
+    ]
+
+
+class ProfileOptionsC(Struct):
+    _fields_ = [
+        ("n_steps", C.c_int32),
+        ("reserved", C.c_int32),
+        ("step_jitter", C.c_double),
+        ("tick_seconds", C.c_double),
+    ]
+
+
+class TaskProfileC(Struct):
+    _fields_ = [
+        ("task_id", C.c_char * TASK_ID_MAX),
+        ("has_est_per_step", C.c_int32),
+        ("profiled_steps", C.c_int32),
+        ("est_per_step_duration", C.c_double),
+        ("max_per_step_duration", C.c_double),
+        ("est_memory", C.c_double),
+    ]
+
+
+class TaskViewC(Struct):
+    _fields_ = [("state", C.c_int32), ("initializing", C.c_int32)]
+
+
+class ManagerActionC(Struct):
+    _fields_ = [("kind", C.c_int32), ("task_id", C.c_char * TASK_ID_MAX)]
+
+
+class WorkerInfoC(Struct):
+    _fields_ = [
+        ("worker_id", C.c_int32),
+        ("queue_len", C.c_int32),
+        ("has_current_task", C.c_int32),
+        ("has_current_bubble", C.c_int32),
+        ("gpu_mem", C.c_double),
+        ("current_task", C.c_char * TASK_ID_MAX),
+        ("current_bubble", BubbleC),
+    ]
+
+
+class PriceConfigC(Struct):
+    _fields_ = [("price_server_1", C.c_double), ("price_server_2", C.c_double)]
+
+
+class TaskWorkC(Struct):
+    _fields_ = [
+        ("id", C.c_char * TASK_ID_MAX),
+        ("work", C.c_double),
+        ("has_throughput", C.c_int32),
+        ("reserved", C.c_int32),
+        ("throughput_per_hour", C.c_double),
+    ]
+
+
+class CostBreakdownC(Struct):
+    _fields_ = [
+        ("c_no_side", C.c_double),
+        ("c_extra", C.c_double),
+        ("c_side_tasks", C.c_double),
+        ("s", C.c_double),
+    ]
+
+
+class StageBreakdownC(Struct):
+    _fields_ = [
+        ("stage", C.c_int32),
+        ("reserved", C.c_int32),
+        ("used_by_side_tasks", tick),
+        ("runtime_overhead", tick),
+        ("idle_oom", tick),
+        ("idle_insufficient_time", tick),
+    ]
+
+
+class TransitionRecordC(Struct):
+    _fields_ = [
+        ("t", tick),
+        ("kind", C.c_int32),
+        ("worker", C.c_int32),
+        ("task", C.c_char * TASK_ID_MAX),
+    ]
+
+
+class ActivityRecordC(Struct):
+    _fields_ = [
+        ("start", tick),
+        ("end", tick),
+        ("worker", C.c_int32),
+        ("kind", C.c_int32),
+        ("clipped", C.c_int32),
+        ("reserved", C.c_int32),
+        ("task", C.c_char * TASK_ID_MAX),
+    ]
+
+
+class KillRecordC(Struct):
+    _fields_ = [
+        ("t", tick),
+        ("worker", C.c_int32),
+        ("reason", C.c_int32),
+        ("task", C.c_char * TASK_ID_MAX),
+    ]
+
+
+class AssignRecordC(Struct):
+    _fields_ = [
+        ("t", tick),
+        ("worker", C.c_int32),
+        ("reserved", C.c_int32),
+        ("task", C.c_char * TASK_ID_MAX),
+    ]
+
+
+class DispositionRecordC(Struct):
+    _fields_ = [
+        ("disposition", C.c_int32),
+        ("has_worker", C.c_int32),
+        ("worker", C.c_int32),
+        ("reserved", C.c_int32),
+        ("steps_completed", C.c_int64),
+        ("task", C.c_char * TASK_ID_MAX),
+    ]
+
+
+class BreakdownInputC(Struct):
+    _fields_ = [
+        ("num_stages", C.c_int32),
+        ("n_profiles", C.c_int32),
+        ("profiles", C.POINTER(TaskProfileC)),
+        ("n_bubbles", C.c_int64),
+        ("bubbles", C.POINTER(BubbleC)),
+        ("n_assigns", C.c_int64),
+        ("assigns", C.POINTER(AssignRecordC)),
+        ("n_transitions", C.c_int64),
+        ("transitions", C.POINTER(TransitionRecordC)),
+        ("n_activities", C.c_int64),
+        ("activities", C.POINTER(ActivityRecordC)),
+    ]
+
+
+LOOKUP_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_char_p, C.POINTER(TaskViewC))
+
+P = C.POINTER
+i32, i64, u64, dbl, vp, cp = C.c_int32, C.c_int64, C.c_uint64, C.c_double, C.c_void_p, C.c_char_p
+
+# name -> (restype, argtypes); every library exporting freeride.h host rows
+HOST_PROTOTYPES = {
+    "fr_abi_version": (C.c_int, []),
+    "fr_last_error": (cp, []),
+    "fr_last_error_field": (cp, []),
+    "fr_pipeline_validate": (C.c_int, [P(PipelineConfigC)]),
+    "fr_stage_issue_order": (C.c_int, [i32, i32, i32, P(Issue), i64, P(i64)]),
+    "fr_build_schedule": (C.c_int, [P(PipelineConfigC), P(OpEventC), i64, P(i64), P(tick)]),
+    "fr_extract_bubbles": (C.c_int, [P(PipelineConfigC), P(OpEventC), i64, P(tick), P(BubbleC), i64, P(i64)]),
+    "fr_bubble_rate": (C.c_int, [i32, P(OpEventC), i64, P(BubbleC), i64, P(dbl)]),
+    "fr_default_stage_memory": (C.c_int, [i32, dbl, dbl, dbl, P(dbl)]),
+    "fr_side_task_validate": (C.c_int, [P(SideTaskSpecC), cp]),
+    "fr_transition_legal": (C.c_int, [i32, i32, P(i32)]),
+    "fr_transition_target": (C.c_int, [i32, i32, P(i32)]),
+    "fr_apply_transition": (C.c_int, [P(TaskRuntimeC), i32, tick]),
+    "fr_iterative_run": (C.c_int, [P(TaskRuntimeC), tick, tick, dbl, dbl, tick, P(IterativeDecisionC)]),
+    "fr_imperative_run": (C.c_int, [P(TaskRuntimeC), tick, tick, P(tick)]),
+    "fr_limit_config_validate": (C.c_int, [P(LimitConfigC)]),
+    "fr_check_memory": (C.c_int, [dbl, dbl, P(i32)]),
+    "fr_program_directed_gate": (C.c_int, [dbl, dbl, P(i32)]),
+    "fr_framework_enforce": (C.c_int, [i32, tick, tick, tick, tick, P(i32)]),
+    "fr_stream_seed": (u64, [u64, cp, cp]),
+    "fr_jittered_step_ticks": (tick, [tick, dbl, P(u64)]),
+    "fr_profile_task": (C.c_int, [P(SideTaskSpecC), P(ProfileOptionsC), u64, P(TaskProfileC)]),
+    "fr_profile_bubbles": (C.c_int, [P(PipelineConfigC), P(tick), i64, P(i64), P(dbl), P(dbl)]),
+    "fr_manager_create": (C.c_int, [i32, P(dbl), P(vp)]),
+    "fr_manager_destroy": (None, [vp]),
+    "fr_manager_worker_info": (C.c_int, [vp, i32, P(WorkerInfoC)]),
+    "fr_manager_queue_at": (C.c_int, [vp, i32, i32, C.c_char_p, i32]),
+    "fr_manager_set_current_task": (C.c_int, [vp, i32, cp]),
+    "fr_select_worker": (C.c_int, [vp, dbl, P(i32)]),
+    "fr_submit_task": (C.c_int, [vp, P(TaskProfileC), P(i32), P(i32)]),
+    "fr_on_bubble_started": (C.c_int, [vp, i32, P(BubbleC), LOOKUP_FN, vp, P(ManagerActionC), i32, P(i32)]),
+    "fr_on_bubble_ended": (C.c_int, [vp, i32, tick, LOOKUP_FN, vp, P(ManagerActionC), i32, P(i32)]),
+    "fr_time_increase": (C.c_int, [dbl, dbl, P(dbl)]),
+    "fr_cost_savings": (C.c_int, [dbl, dbl, P(TaskWorkC), i32, P(PriceConfigC), P(CostBreakdownC)]),
+    "fr_bubble_breakdown": (C.c_int, [P(BreakdownInputC), P(StageBreakdownC)]),
+}
+
+
+def bind(lib: C.CDLL, prototypes: dict) -> C.CDLL:
+    for name, (res, args) in prototypes.items():
+        fn = getattr(lib, name)  # AttributeError: symbol missing -> loud
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+def raise_for(lib: C.CDLL, rc: int):
+    if rc == FR_OK:
+        return
+    msg = (lib.fr_last_error() or b"").decode(errors="replace")
+    field = (lib.fr_last_error_field() or b"").decode(errors="replace")
+    if rc == FR_ERR_VALIDATION:
+        raise ValidationError(field, msg)
+    if rc == FR_ERR_SCHEMA:
+        raise SchemaError(field, msg)
+    if rc == FR_ERR_ILLEGAL_TRANSITION:
+        raise IllegalTransition(msg)
+    if rc == FR_ERR_INVARIANT:
+        raise InvariantError(msg)
+    if rc == FR_ERR_CAPACITY:
+        raise CapacityError(msg)
+    if rc >= FR_ERR_CUDA_BASE:
+        e = CudaError(f"CUDA error {rc - FR_ERR_CUDA_BASE}: {msg}")
+        raise e
+    e = FreeRideError(f"status {rc}: {msg}")
+    e.code = rc
+    raise e
