@@ -384,3 +384,18 @@ def raise_for(lib: C.CDLL, rc: int):
     e = FreeRideError(f"status {rc}: {msg}")
     e.code = rc
     raise e
+
+
+# ---------------------------------------------------------------- freeride_gpu.h
+GPU_PROTOTYPES = {
+    "fr_stream_create": (C.c_int, [i32, P(vp)]),
+    "fr_stream_destroy": (C.c_int, [vp]),
+    "fr_stream_synchronize": (C.c_int, [vp]),
+    "fr_device_sm_count": (C.c_int, [P(i32)]),
+    "fr_img_plan_create": (C.c_int, [i32, i32, i32, i32, P(vp)]),
+    "fr_img_plan_destroy": (C.c_int, [vp]),
+    "fr_img_plan_path": (C.c_int, [vp, P(i32)]),
+    "fr_img_resize_watermark": (C.c_int, [vp, vp, vp, vp, i32, vp]),
+    "fr_img_generate": (C.c_int, [vp, i32, i32, i32, i32, u64, i32, vp]),
+    "fr_img_generate_watermark": (C.c_int, [vp, i32, i32, u64, vp]),
+}

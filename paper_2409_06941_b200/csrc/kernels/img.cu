@@ -1,0 +1,373 @@
+// K5: bilinear resize + integer watermark alpha-blend, one bounded step of
+// the image side task.
+//
+// Arithmetic (bit-exact with oracle/sidetasks.c and cv2 INTER_LINEAR_EXACT):
+//   per axis: src = (d + 0.5) * S/D - 0.5, i0 = floor, w1 = rne(frac * 256)
+//   px  = ((row_a * (256-wy) + row_b * wy) + 2^15) >> 16, rows pre-mixed in x
+//   out = (px * (255 - alpha) + wm * alpha + 127) / 255
+// At exactly 2x every weight is 128, so px = (a + b + c + d + 2) >> 2.
+//
+// Fast path (sw = 2 dw, sh = 2 dh, dw % 16 == 0), B200-first:
+//   persistent CTAs (one per SM), S-stage smem ring per CTA; for each output
+//   row one elected thread issues TMA bulk copies (cp.async.bulk, UBLKCP) of
+//   the two contiguous source rows (evict-first) and the watermark row
+//   (evict-last: it is re-read by every image of the batch) against an
+//   mbarrier with expect_tx; all threads wait on the barrier, compute 8 output
+//   pixels each from conflict-free 16-byte smem reads, stage the row in smem,
+//   and the elected thread bulk-stores it (cp.async.bulk global<-shared).
+//   One __syncthreads per row; loads for S rows are always in flight, so HBM
+//   sees only full-line streaming requests.
+#include <cmath>
+#include <vector>
+
+#include "freeride_gpu.h"
+#include "kernels/common.cuh"
+
+namespace {
+
+constexpr int kImgThreads = 256;
+constexpr int kImgStages = 3;
+constexpr int kImgCtasPerSm = 2;
+
+__device__ __forceinline__ uint32_t lanes_lo(uint32_t w) { return w & 0x00FF00FFu; }
+__device__ __forceinline__ uint32_t lanes_hi(uint32_t w) { return (w >> 8) & 0x00FF00FFu; }
+
+__device__ __forceinline__ uint32_t blend255(uint32_t px, uint32_t wmc, uint32_t alpha) {
+  return (px * (255u - alpha) + wmc * alpha + 127u) / 255u;
+}
+
+template <int S>
+__global__ void __launch_bounds__(kImgThreads, kImgCtasPerSm)
+    img_resize2x_wm_tma(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
+                        const uint8_t* __restrict__ wm, int dw, int dh, int64_t rows) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const uint32_t src_row = 6u * static_cast<uint32_t>(dw);  // one source row, RGB
+  const uint32_t wm_row = 4u * static_cast<uint32_t>(dw);
+  const uint32_t out_row = 3u * static_cast<uint32_t>(dw);
+  const uint32_t a_src = (2u * src_row + 127u) & ~127u;
+  const uint32_t a_wm = (wm_row + 127u) & ~127u;
+  const uint32_t a_out = (out_row + 127u) & ~127u;
+  const uint32_t stage_bytes = a_src + a_wm + a_out;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
+
+  const int tid = threadIdx.x;
+  const int64_t G = gridDim.x;
+  const int64_t first = blockIdx.x;
+  const int64_t nk = first < rows ? (rows - first + G - 1) / G : 0;
+
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) frk::mbar_init(&full[s], 1);
+    frk::fence_mbar_init();
+  }
+  __syncthreads();
+
+  uint64_t pol_stream = 0, pol_keep = 0;
+  if (tid == 0) {
+    pol_stream = frk::policy_evict_first();
+    pol_keep = frk::policy_evict_last();
+  }
+  auto issue = [&](int64_t k) {
+    const int s = static_cast<int>(k % S);
+    const int64_t r = first + k * G;
+    const int64_t img = r / dh;
+    const int64_t y = r - img * dh;
+    uint8_t* st = smem + s * stage_bytes;
+    frk::mbar_arrive_expect_tx(&full[s], 2u * src_row + wm_row);
+    frk::bulk_g2s(st, src + (img * 2 * dh + 2 * y) * static_cast<int64_t>(src_row), 2u * src_row,
+                  &full[s], pol_stream);
+    frk::bulk_g2s(st + a_src, wm + y * static_cast<int64_t>(wm_row), wm_row, &full[s], pol_keep);
+  };
+  if (tid == 0)
+    for (int64_t k = 0; k < nk && k < S; ++k) issue(k);
+
+  const int groups = dw >> 3;  // 8 output pixels per thread-iteration
+  for (int64_t k = 0; k < nk; ++k) {
+    const int s = static_cast<int>(k % S);
+    frk::mbar_wait(&full[s], static_cast<uint32_t>((k / S) & 1));
+    uint8_t* st = smem + s * stage_bytes;
+    const uint8_t* ra = st;
+    const uint8_t* rb = st + src_row;
+    const uint8_t* wr = st + a_src;
+    uint8_t* orow = st + a_src + a_wm;
+
+    for (int g = tid; g < groups; g += kImgThreads) {
+      uint32_t va[12], vb[12], wv[8];
+      const uint4* pa = reinterpret_cast<const uint4*>(ra + 48 * g);
+      const uint4* pb = reinterpret_cast<const uint4*>(rb + 48 * g);
+      const uint4* pw = reinterpret_cast<const uint4*>(wr + 32 * g);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const uint4 x = pa[i], y = pb[i];
+        va[4 * i + 0] = x.x; va[4 * i + 1] = x.y; va[4 * i + 2] = x.z; va[4 * i + 3] = x.w;
+        vb[4 * i + 0] = y.x; vb[4 * i + 1] = y.y; vb[4 * i + 2] = y.z; vb[4 * i + 3] = y.w;
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const uint4 x = pw[i];
+        wv[4 * i + 0] = x.x; wv[4 * i + 1] = x.y; wv[4 * i + 2] = x.z; wv[4 * i + 3] = x.w;
+      }
+      // Vertical sums of the two source rows in 16-bit lanes: ev[i] holds
+      // bytes 4i and 4i+2, od[i] bytes 4i+1 and 4i+3 (each <= 510).
+      uint32_t ev[12], od[12];
+#pragma unroll
+      for (int i = 0; i < 12; ++i) {
+        ev[i] = lanes_lo(va[i]) + lanes_lo(vb[i]);
+        od[i] = lanes_hi(va[i]) + lanes_hi(vb[i]);
+      }
+      uint32_t rgb[8];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {  // pixel pair (2q, 2q+1) = source words 3q..3q+2
+        const uint32_t e0 = ev[3 * q], e1 = ev[3 * q + 1], e2 = ev[3 * q + 2];
+        const uint32_t o0 = od[3 * q], o1 = od[3 * q + 1], o2 = od[3 * q + 2];
+        // Horizontal pairs aligned lane-for-lane with PRMT, then (s + 2) >> 2.
+        uint32_t rg[2], bb;
+        rg[0] = __byte_perm(e0, o0, 0x5410) + __byte_perm(o0, e1, 0x5432);  // R0 | G0
+        rg[1] = __byte_perm(e1, o1, 0x7632) + __byte_perm(o2, e2, 0x7610);  // R1 | G1
+        bb = __byte_perm(e0, e2, 0x5432) + __byte_perm(o1, o2, 0x7610);     // B0 | B1
+        rg[0] = ((rg[0] + 0x00020002u) >> 2) & 0x00FF00FFu;
+        rg[1] = ((rg[1] + 0x00020002u) >> 2) & 0x00FF00FFu;
+        bb = ((bb + 0x00020002u) >> 2) & 0x00FF00FFu;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const uint32_t w = wv[2 * q + j];
+          const uint32_t a = w >> 24, na = 255u - a;
+          // R,G share the pixel's alpha: blend both 16-bit lanes in one IMAD
+          // chain, then floor(t / 255) = (t + 1 + (t >> 8)) >> 8 per lane
+          // (exact for t <= 65407, checked exhaustively in the tests).
+          const uint32_t t = rg[j] * na + (__byte_perm(w, 0u, 0x4140) * a + 0x007F007Fu);
+          const uint32_t qrg = ((t + 0x00010001u + ((t >> 8) & 0x00FF00FFu)) >> 8) & 0x00FF00FFu;
+          const uint32_t b = j ? (bb >> 16) : (bb & 0xFFFFu);
+          const uint32_t tb = b * na + ((w >> 16) & 0xFFu) * a + 127u;
+          const uint32_t qb = (tb + 1u + (tb >> 8)) >> 8;
+          rgb[2 * q + j] = __byte_perm(qrg, qb, 0x0420);  // R G B _
+        }
+      }
+      uint2* po = reinterpret_cast<uint2*>(orow + 24 * g);
+      po[0] = make_uint2(__byte_perm(rgb[0], rgb[1], 0x4210), __byte_perm(rgb[1], rgb[2], 0x5421));
+      po[1] = make_uint2(__byte_perm(rgb[2], rgb[3], 0x6542), __byte_perm(rgb[4], rgb[5], 0x4210));
+      po[2] = make_uint2(__byte_perm(rgb[5], rgb[6], 0x5421), __byte_perm(rgb[6], rgb[7], 0x6542));
+    }
+    frk::fence_proxy_async_smem();
+    // Before anyone writes the next stage's output buffer, the bulk store
+    // that last read it (issued S-1 rows ago) must have drained.
+    if (tid == 0 && k + 1 >= S) frk::bulk_wait_read<S - 2>();
+    __syncthreads();
+    if (tid == 0) {
+      frk::bulk_s2g(dst + (first + k * G) * static_cast<int64_t>(out_row), orow, out_row,
+                    pol_stream);
+      frk::bulk_commit();
+      if (k + S < nk) issue(k + S);
+    }
+  }
+  if (tid == 0) frk::bulk_wait<0>();
+}
+
+// General shapes: one thread per output pixel, coefficient tables from the
+// plan (built on the host with the oracle's double-precision rule).
+__global__ void img_resize_wm_general(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
+                                      const uint8_t* __restrict__ wm,
+                                      const int32_t* __restrict__ tab, int sw, int sh, int dw,
+                                      int dh, int64_t total) {
+  const int32_t* x0 = tab;
+  const int32_t* x1 = tab + dw;
+  const int32_t* xw = tab + 2 * dw;
+  const int32_t* y0 = tab + 3 * dw;
+  const int32_t* y1 = y0 + dh;
+  const int32_t* yw = y0 + 2 * dh;
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < total;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t img = p / (static_cast<int64_t>(dw) * dh);
+    const int64_t rem = p - img * dw * dh;
+    const int y = static_cast<int>(rem / dw), x = static_cast<int>(rem % dw);
+    const uint8_t* base = src + img * static_cast<int64_t>(sw) * sh * 3;
+    const uint8_t* ra = base + static_cast<int64_t>(y0[y]) * sw * 3;
+    const uint8_t* rb = base + static_cast<int64_t>(y1[y]) * sw * 3;
+    const int a = x0[x] * 3, b = x1[x] * 3;
+    const int32_t wx1 = xw[x], wx0 = 256 - wx1, wy1 = yw[y], wy0 = 256 - wy1;
+    const uint8_t* w = wm + (static_cast<int64_t>(y) * dw + x) * 4;
+    const uint32_t alpha = w[3];
+    uint8_t* o = dst + p * 3;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const int32_t ha = ra[a + c] * wx0 + ra[b + c] * wx1;
+      const int32_t hb = rb[a + c] * wx0 + rb[b + c] * wx1;
+      const uint32_t px = static_cast<uint32_t>((ha * wy0 + hb * wy1 + (1 << 15)) >> 16);
+      o[c] = static_cast<uint8_t>(blend255(px, w[c], alpha));
+    }
+  }
+}
+
+__global__ void img_generate_kernel(uint8_t* __restrict__ dst, int64_t total_px, int w, int h,
+                                    int ch, uint64_t seed, int first) {
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < total_px;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t hw = static_cast<int64_t>(h) * w;
+    const int64_t i = p / hw + first;
+    const int64_t rem = p % hw;
+    const int64_t y = rem / w, x = rem % w;
+    const uint64_t r = frk::splitmix64(seed ^ static_cast<uint64_t>((i * h + y) * w + x));
+    for (int c = 0; c < ch; ++c) {
+      const uint32_t g = static_cast<uint32_t>(x + 2 * y + 37 * i + 85 * c);
+      dst[p * ch + c] = static_cast<uint8_t>((g + ((r >> (8 * c)) & 0x3f)) & 0xff);
+    }
+  }
+}
+
+__global__ void img_watermark_kernel(uint32_t* __restrict__ wm, int64_t n, uint64_t seed) {
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < n;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    wm[p] = static_cast<uint32_t>(
+        frk::splitmix64(seed ^ (0x5741544552ull << 24) ^ static_cast<uint64_t>(p)));
+}
+
+// Host restatement of the oracle's coefficient rule (orc_img_coeffs).
+void axis_coeffs(int S, int D, int32_t* i0, int32_t* i1, int32_t* w1) {
+  const double scale = static_cast<double>(S) / static_cast<double>(D);
+  for (int d = 0; d < D; ++d) {
+    double f = (static_cast<double>(d) + 0.5) * scale - 0.5;
+    const double fl = std::floor(f);
+    int lo = static_cast<int>(fl);
+    f -= fl;
+    if (lo < 0) {
+      lo = 0;
+      f = 0.0;
+    }
+    if (lo >= S - 1) {
+      lo = S - 1;
+      f = 0.0;
+    }
+    i0[d] = lo;
+    i1[d] = lo + 1 < S ? lo + 1 : S - 1;
+    w1[d] = static_cast<int32_t>(std::nearbyint(f * 256.0));
+  }
+}
+
+int grid_for(int64_t work, int threads, int per_sm) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t want = (work + threads - 1) / threads;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(sms) * per_sm)));
+}
+
+}  // namespace
+
+struct fr_img_plan {
+  int sw = 0, sh = 0, dw = 0, dh = 0;
+  int path = FR_IMG_PATH_GENERAL;
+  int32_t* d_tab = nullptr;
+  int smem = 0;
+  int sms = 0;
+};
+
+extern "C" {
+
+int fr_img_plan_create(int32_t sw, int32_t sh, int32_t dw, int32_t dh, fr_img_plan** out) {
+  if (!out) return frcapi::fail(FR_ERR_ARGUMENT, "null plan out");
+  if (sw < 1 || sh < 1 || dw < 1 || dh < 1)
+    return frcapi::fail(FR_ERR_VALIDATION, "image sizes must be >= 1", "image.shape");
+  auto* plan = new fr_img_plan;
+  plan->sw = sw;
+  plan->sh = sh;
+  plan->dw = dw;
+  plan->dh = dh;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&plan->sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e != cudaSuccess) {
+    delete plan;
+    return frcapi::cuda_status(e, "cudaGetDevice");
+  }
+  const bool two_x = sw == 2 * dw && sh == 2 * dh && dw % 16 == 0;
+  if (two_x) {
+    auto al = [](int x) { return (x + 127) & ~127; };
+    plan->smem = kImgStages * (al(12 * dw) + al(4 * dw) + al(3 * dw)) + kImgStages * 8;
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (plan->smem <= optin) {
+      e = cudaFuncSetAttribute(img_resize2x_wm_tma<kImgStages>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, plan->smem);
+      if (e != cudaSuccess) {
+        delete plan;
+        return frcapi::cuda_status(e, "cudaFuncSetAttribute(img_resize2x_wm_tma)");
+      }
+      plan->path = FR_IMG_PATH_TMA_2X;
+    }
+  }
+  if (plan->path == FR_IMG_PATH_GENERAL) {
+    std::vector<int32_t> tab(3 * static_cast<size_t>(dw) + 3 * static_cast<size_t>(dh));
+    axis_coeffs(sw, dw, tab.data(), tab.data() + dw, tab.data() + 2 * dw);
+    axis_coeffs(sh, dh, tab.data() + 3 * dw, tab.data() + 3 * dw + dh, tab.data() + 3 * dw + 2 * dh);
+    e = cudaMalloc(&plan->d_tab, tab.size() * sizeof(int32_t));
+    if (e == cudaSuccess)
+      e = cudaMemcpy(plan->d_tab, tab.data(), tab.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      if (plan->d_tab) cudaFree(plan->d_tab);
+      delete plan;
+      return frcapi::cuda_status(e, "coefficient table upload");
+    }
+  }
+  *out = plan;
+  return FR_OK;
+}
+
+int fr_img_plan_destroy(fr_img_plan* plan) {
+  if (!plan) return FR_OK;
+  if (plan->d_tab) cudaFree(plan->d_tab);
+  delete plan;
+  return FR_OK;
+}
+
+int fr_img_plan_path(const fr_img_plan* plan, int32_t* path) {
+  if (!plan || !path) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  *path = plan->path;
+  return FR_OK;
+}
+
+int fr_img_resize_watermark(const fr_img_plan* plan, const uint8_t* src, uint8_t* dst,
+                            const uint8_t* wm, int32_t n, void* stream) {
+  if (!plan || (n > 0 && (!src || !dst || !wm))) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  if (n < 0) return frcapi::fail(FR_ERR_VALIDATION, "n must be >= 0", "n");
+  if (n == 0) return FR_OK;
+  auto s = static_cast<cudaStream_t>(stream);
+  if (plan->path == FR_IMG_PATH_TMA_2X) {
+    const bool aligned = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst) |
+                           reinterpret_cast<uintptr_t>(wm)) & 15u) == 0;
+    if (!aligned) return frcapi::fail(FR_ERR_UNSUPPORTED, "TMA path needs 16-byte aligned buffers");
+    const int64_t rows = static_cast<int64_t>(n) * plan->dh;
+    const int grid = static_cast<int>(std::min<int64_t>(rows, int64_t(plan->sms) * kImgCtasPerSm));
+    img_resize2x_wm_tma<kImgStages><<<grid, kImgThreads, plan->smem, s>>>(src, dst, wm, plan->dw,
+                                                                        plan->dh, rows);
+  } else {
+    const int64_t total = static_cast<int64_t>(n) * plan->dw * plan->dh;
+    img_resize_wm_general<<<grid_for(total, 256, 8), 256, 0, s>>>(
+        src, dst, wm, plan->d_tab, plan->sw, plan->sh, plan->dw, plan->dh, total);
+  }
+  FR_CUDA_LAUNCHED("img_resize_watermark");
+  return FR_OK;
+}
+
+int fr_img_generate(uint8_t* dst, int32_t n, int32_t w, int32_t h, int32_t ch, uint64_t seed,
+                    int32_t first, void* stream) {
+  if (n < 0 || w < 1 || h < 1 || ch < 1 || ch > 8)
+    return frcapi::fail(FR_ERR_VALIDATION, "bad image generator shape", "image.shape");
+  const int64_t total = static_cast<int64_t>(n) * w * h;
+  if (total == 0) return FR_OK;
+  img_generate_kernel<<<grid_for(total, 256, 8), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      dst, total, w, h, ch, seed, first);
+  FR_CUDA_LAUNCHED("img_generate");
+  return FR_OK;
+}
+
+int fr_img_generate_watermark(uint8_t* wm, int32_t w, int32_t h, uint64_t seed, void* stream) {
+  if (w < 1 || h < 1) return frcapi::fail(FR_ERR_VALIDATION, "bad watermark shape", "watermark.shape");
+  if (reinterpret_cast<uintptr_t>(wm) & 3u) return frcapi::fail(FR_ERR_UNSUPPORTED, "watermark must be 4-byte aligned");
+  const int64_t n = static_cast<int64_t>(w) * h;
+  img_watermark_kernel<<<grid_for(n, 256, 8), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<uint32_t*>(wm), n, seed);
+  FR_CUDA_LAUNCHED("img_generate_watermark");
+  return FR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,109 @@
+"""K5 image resize + watermark on the B200 vs the CPU oracle (bit-exact)."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def g():
+    from paper_2409_06941_b200 import gpu
+    gpu.glib()
+    return gpu
+
+
+def test_generators_match_oracle(g, sidetask_oracle):
+    o = sidetask_oracle
+    for (n, w, h, ch, seed, first) in [(2, 37, 11, 3, 5, 0), (1, 3840, 2160, 3, 1, 7), (3, 16, 16, 4, 9, 2)]:
+        got = g.img_generate(n, w, h, ch, seed, first).cpu().numpy()
+        want = o.img_generate(n, w, h, ch, seed, first)
+        assert np.array_equal(got, want)
+    assert np.array_equal(g.img_generate_watermark(1920, 1080, 7).cpu().numpy(),
+                          o.img_generate_watermark(1920, 1080, 7))
+
+
+@pytest.mark.parametrize("n", [1, 2, 5])
+def test_tma_2x_4k_bit_exact(g, sidetask_oracle, n):
+    plan = g.ImagePlan(3840, 2160, 1920, 1080)
+    assert plan.path == g.ImagePlan.TMA_2X
+    src = g.img_generate(n, 3840, 2160, seed=11 + n)
+    wm = g.img_generate_watermark(1920, 1080, seed=3)
+    dst = torch.full((n, 1080, 1920, 3), 0xAB, dtype=torch.uint8, device="cuda")
+    plan.run(src, dst, wm)
+    torch.cuda.synchronize()
+    want = sidetask_oracle.img_resize_watermark(src.cpu().numpy(), wm.cpu().numpy(), 1920, 1080)
+    assert np.array_equal(dst.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("sw,sh,dw,dh", [(32, 2, 16, 1), (64, 30, 32, 15), (1024, 6, 512, 3)])
+def test_tma_2x_small_shapes(g, sidetask_oracle, sw, sh, dw, dh):
+    plan = g.ImagePlan(sw, sh, dw, dh)
+    assert plan.path == g.ImagePlan.TMA_2X
+    src = g.img_generate(3, sw, sh, seed=4)
+    wm = g.img_generate_watermark(dw, dh, seed=8)
+    dst = torch.empty((3, dh, dw, 3), dtype=torch.uint8, device="cuda")
+    plan.run(src, dst, wm)
+    want = sidetask_oracle.img_resize_watermark(src.cpu().numpy(), wm.cpu().numpy(), dw, dh)
+    assert np.array_equal(dst.cpu().numpy(), want)
+
+
+def test_general_path_random_shapes(g, sidetask_oracle):
+    rng = np.random.default_rng(5)
+    for _ in range(40):
+        sh, sw, dh, dw = (int(x) for x in rng.integers(1, 300, 4))
+        plan = g.ImagePlan(sw, sh, dw, dh)
+        n = int(rng.integers(1, 3))
+        src = g.img_generate(n, sw, sh, seed=int(rng.integers(1 << 30)))
+        wm = g.img_generate_watermark(dw, dh, seed=int(rng.integers(1 << 30)))
+        dst = torch.empty((n, dh, dw, 3), dtype=torch.uint8, device="cuda")
+        plan.run(src, dst, wm)
+        want = sidetask_oracle.img_resize_watermark(src.cpu().numpy(), wm.cpu().numpy(), dw, dh)
+        assert np.array_equal(dst.cpu().numpy(), want), (sw, sh, dw, dh)
+
+
+def test_general_path_matches_cv2(g):
+    cv2 = pytest.importorskip("cv2")
+    plan = g.ImagePlan(641, 479, 320, 240)
+    assert plan.path == g.ImagePlan.GENERAL
+    src = g.img_generate(1, 641, 479, seed=2)
+    wm = torch.zeros((240, 320, 4), dtype=torch.uint8, device="cuda")  # alpha 0: pure resize
+    dst = torch.empty((1, 240, 320, 3), dtype=torch.uint8, device="cuda")
+    plan.run(src, dst, wm)
+    want = cv2.resize(src[0].cpu().numpy(), (320, 240), interpolation=cv2.INTER_LINEAR_EXACT)
+    assert np.array_equal(dst[0].cpu().numpy(), want)
+
+
+def test_edge_cases(g):
+    from paper_2409_06941_b200._abi import FreeRideError, ValidationError
+    plan = g.ImagePlan(64, 64, 32, 32)
+    src = torch.zeros((0, 64, 64, 3), dtype=torch.uint8, device="cuda")
+    dst = torch.zeros((0, 32, 32, 3), dtype=torch.uint8, device="cuda")
+    wm = torch.zeros((32, 32, 4), dtype=torch.uint8, device="cuda")
+    plan.run(src, dst, wm)  # n = 0: no launch, no error
+    big = torch.zeros(64 * 64 * 3 + 1, dtype=torch.uint8, device="cuda")
+    out1 = torch.zeros((1, 32, 32, 3), dtype=torch.uint8, device="cuda")
+    lib = g.glib()
+    rc = lib.fr_img_resize_watermark(plan._h, big.data_ptr() + 1, out1.data_ptr(), wm.data_ptr(), 1,
+                                     torch.cuda.current_stream().cuda_stream)
+    assert rc == 8  # FR_ERR_UNSUPPORTED: TMA path needs 16-byte alignment
+    with pytest.raises(ValidationError):
+        g.ImagePlan(0, 4, 2, 2)
+    with pytest.raises(ValueError):
+        plan.run(src.cpu(), dst, wm)
+
+
+def test_full_batch_64_bit_exact(g, sidetask_oracle):
+    """configs[1] at its full size: 64 4K images -> 1080p, every byte checked."""
+    n = 64
+    plan = g.ImagePlan(3840, 2160, 1920, 1080)
+    src = g.img_generate(n, 3840, 2160, seed=1)
+    wm = g.img_generate_watermark(1920, 1080, seed=7)
+    dst = torch.empty((n, 1080, 1920, 3), dtype=torch.uint8, device="cuda")
+    s = g.low_priority_stream()
+    torch.cuda.synchronize()
+    plan.run(src, dst, wm, stream=s)
+    s.synchronize()
+    got = dst.cpu().numpy()
+    want = sidetask_oracle.img_resize_watermark(src.cpu().numpy(), wm.cpu().numpy(), 1920, 1080)
+    assert np.array_equal(got, want)
