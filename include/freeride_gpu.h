@@ -42,10 +42,139 @@ int fr_img_plan_path(const fr_img_plan* plan, int32_t* path);
  * (RGBA, straight alpha): dst = (resize(src)*(255-a) + wm*a + 127) / 255 */
 int fr_img_resize_watermark(const fr_img_plan* plan, const uint8_t* src, uint8_t* dst,
                             const uint8_t* wm_rgba, int32_t n, void* stream);
+/* The watermark is a task constant: prepare it once (InitSideTask) into the
+ * plan's layout (TMA path: per pixel w*a+127 and 255-a in 16-bit lanes,
+ * group-transposed, 8 B/px; general path: RGBA copy, 4 B/px) and run the
+ * prepared variant per step.  fr_img_resize_watermark prepares into a
+ * plan-owned buffer on every call. */
+int fr_img_prepared_bytes(const fr_img_plan* plan, int64_t* bytes);
+int fr_img_prepare_watermark(const fr_img_plan* plan, const uint8_t* wm_rgba, void* prepared,
+                             void* stream);
+int fr_img_resize_watermark_prepared(const fr_img_plan* plan, const uint8_t* src, uint8_t* dst,
+                                     const void* prepared, int32_t n, void* stream);
 /* synthetic inputs (same counter-based arithmetic as oracle/sidetasks.c) */
 int fr_img_generate(uint8_t* dst, int32_t n, int32_t w, int32_t h, int32_t channels,
                     uint64_t seed, int32_t first_index, void* stream);
 int fr_img_generate_watermark(uint8_t* wm, int32_t w, int32_t h, uint64_t seed, void* stream);
+
+/* ------------------------------------------------ side-task plugin surface */
+/* The paper's overridable transition functions:
+ * CreateSideTask / InitSideTask / StartSideTask / RunNextStep /
+ * PauseSideTask / StopSideTask plus the loop-finished predicate.  Replaces
+ * the reference's synthetic SideTaskSpec body (task.hpp:33-50) and its
+ * TaskLookup callback (manager.hpp:52) with real GPU work.  Every hook
+ * returns a status; init/run_next_step enqueue asynchronously on `stream`
+ * (the worker's low-priority stream) and must not synchronise it. */
+typedef struct fr_side_task_vtable {
+  int (*create)(void* user);
+  int (*init)(void* user, void* stream);
+  int (*start)(void* user);
+  int (*run_next_step)(void* user, void* stream);
+  int (*pause)(void* user);
+  int (*stop)(void* user);
+  int (*finished)(void* user, int64_t steps_completed, int32_t* done);
+  void (*destroy)(void* user);
+  double work_units_per_step; /* px, edges, ... reported per completed step */
+} fr_side_task_vtable;
+
+/* Built-in side tasks (kernels above) behind the vtable. */
+typedef struct fr_image_task_config {
+  int32_t sw, sh, dw, dh;       /* 3840x2160 -> 1920x1080 */
+  int32_t batch;                /* images resident (device) or staged (host mode) */
+  int32_t images_per_step;      /* one RunNextStep = this many images */
+  int32_t host_io;              /* 1: inputs in pinned host memory, H2D/D2H per step */
+  int32_t reserved;
+  uint64_t seed;
+  int64_t total_steps;          /* <= 0: unbounded */
+} fr_image_task_config;
+int fr_image_task_create(const fr_image_task_config* cfg, fr_side_task_vtable* vt, void** user);
+/* bytes resident on the GPU once InitSideTask ran (memory_demand) */
+int fr_image_task_memory(const fr_image_task_config* cfg, double* gib);
+/* device pointers of the last processed batch slot (for checking) */
+int fr_image_task_buffers(void* user, const uint8_t** src, uint8_t** dst, const uint8_t** wm,
+                          int64_t* steps_done);
+
+/* ------------------------------------------------------ the GPU runtime */
+/* One GPU replaying stage `stage` of a p-stage 1F1B pipeline whose FP/BP
+ * ops are real bf16 tensor-core GEMMs (the stand-in), with one side-task
+ * worker: manager Alg. 1/2, the iterative interface and the program-directed
+ * gate (the reference's missing run_experiment, engine.hpp:97) executed in
+ * real time against device-clock bubble signals. */
+typedef struct fr_harness fr_harness;
+
+typedef struct fr_harness_config {
+  int32_t num_stages;
+  int32_t num_micro_batches;
+  int32_t stage;              /* the stage this GPU replays (replica mode) */
+  int32_t layers;             /* stand-in shape (per stage) */
+  int32_t hidden;
+  int32_t tokens;             /* micro-batch x sequence length */
+  int32_t ffn_mult;
+  int32_t profile_reps;       /* op timing repetitions (median) */
+  int32_t max_inflight_steps; /* pipelined dispatch depth, >= 1 */
+  int32_t gate_estimate;      /* 0 = profiled mean, 1 = max (config.hpp:17) */
+  double gpu_memory_total;    /* GiB, memory model for Alg. 1 */
+  double weight_mem;          /* GiB per stage; < 0 derive from the stand-in */
+  double activation_mem;      /* GiB per in-flight micro-batch; < 0 derive */
+  int64_t fp_ticks_override;  /* > 0: use instead of the measured op times */
+  int64_t bp_ticks_override;
+  int32_t profile_epochs;     /* dry-run epochs of the bubble profiler (0: from op times) */
+  int32_t reserved;
+} fr_harness_config;
+
+/* All durations in ns ticks (tick_seconds = 1e-9). */
+typedef struct fr_harness_profile {
+  fr_tick fp_ticks;
+  fr_tick bp_ticks;
+  fr_tick epoch_span;
+  fr_tick stage_bubble_ticks;   /* sum of this stage's bubbles per epoch */
+  double bubble_rate;           /* whole p-stage schedule (bubble_rate) */
+  double available_memory;      /* GiB on this stage (PipelineConfig) */
+  double fp_tflops;             /* stand-in tensor throughput, measured */
+  double bp_tflops;
+  int32_t n_bubbles;            /* this stage, per epoch */
+  int32_t reserved;
+  double clock_offset_err_ns;   /* host<->device clock calibration RTT/2 */
+} fr_harness_profile;
+
+typedef struct fr_run_report {
+  int32_t epochs;
+  int32_t with_tasks;
+  double makespan_s;            /* device time, run start -> last epoch end */
+  double bubble_s;              /* sum of actual bubbles on this run */
+  double used_s;                /* step time inside bubbles */
+  double overrun_s;             /* step time outside bubbles */
+  double work_units;            /* completed steps x work_units_per_step */
+  int64_t steps_launched;
+  int64_t steps_completed;
+  double dispatch_host_us;      /* mean host time per gate+launch */
+  double max_step_overrun_s;    /* worst step tail past its bubble end */
+  fr_stage_breakdown breakdown; /* bubble_breakdown (metrics.hpp:64), ns ticks */
+  int64_t pauses;
+  int64_t kills;                /* framework_enforce verdicts (limits.hpp:34) */
+} fr_run_report;
+
+int fr_harness_create(const fr_harness_config* cfg, fr_harness** out);
+int fr_harness_destroy(fr_harness* h);
+int fr_harness_get_profile(const fr_harness* h, fr_harness_profile* out);
+/* this stage's bubbles of one epoch (profile, undelayed, relative ticks) */
+int fr_harness_stage_bubbles(const fr_harness* h, fr_bubble* out, int32_t cap, int32_t* n);
+/* Submits a side task: profile_task by running `profile_steps` steps
+ * standalone (measured, CUDA events), then Alg. 1 over this GPU's worker.
+ * Ownership of `user` passes to the harness (vtable destroy). */
+int fr_harness_submit(fr_harness* h, const char* task_id, const fr_side_task_vtable* vt,
+                      void* user, double memory_demand_gib, int32_t profile_steps,
+                      fr_task_profile* profile, int32_t* assigned);
+/* profile_task from the task's steps in the last run (measured in bubbles,
+ * under training load): est = mean, max = worst, as in profiler.cpp:50-78 */
+int fr_harness_reprofile(fr_harness* h, const char* task_id, fr_task_profile* out);
+/* Runs `epochs` epochs; with_tasks=0 is the ΔT baseline. Blocks. */
+int fr_harness_run(fr_harness* h, int32_t epochs, int32_t with_tasks, fr_run_report* out);
+/* raw timelines of the last run, seconds from run start, (start, end) pairs */
+int fr_harness_timeline(const fr_harness* h, int32_t which /*0 ops,1 bubbles,2 steps*/,
+                        double* start_end, int64_t cap, int64_t* n);
+/* this GPU's kernel launch count in the last run (side-task steps + stand-in) */
+int fr_harness_launches(const fr_harness* h, int64_t* side_steps, int64_t* training_ops);
 
 #ifdef __cplusplus
 }

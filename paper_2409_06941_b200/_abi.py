@@ -396,6 +396,76 @@ GPU_PROTOTYPES = {
     "fr_img_plan_destroy": (C.c_int, [vp]),
     "fr_img_plan_path": (C.c_int, [vp, P(i32)]),
     "fr_img_resize_watermark": (C.c_int, [vp, vp, vp, vp, i32, vp]),
+    "fr_img_prepared_bytes": (C.c_int, [vp, P(i64)]),
+    "fr_img_prepare_watermark": (C.c_int, [vp, vp, vp, vp]),
+    "fr_img_resize_watermark_prepared": (C.c_int, [vp, vp, vp, vp, i32, vp]),
     "fr_img_generate": (C.c_int, [vp, i32, i32, i32, i32, u64, i32, vp]),
     "fr_img_generate_watermark": (C.c_int, [vp, i32, i32, u64, vp]),
 }
+
+
+class SideTaskVTableC(Struct):
+    _fields_ = [
+        ("create", C.CFUNCTYPE(C.c_int, vp)),
+        ("init", C.CFUNCTYPE(C.c_int, vp, vp)),
+        ("start", C.CFUNCTYPE(C.c_int, vp)),
+        ("run_next_step", C.CFUNCTYPE(C.c_int, vp, vp)),
+        ("pause", C.CFUNCTYPE(C.c_int, vp)),
+        ("stop", C.CFUNCTYPE(C.c_int, vp)),
+        ("finished", C.CFUNCTYPE(C.c_int, vp, C.c_int64, P(i32))),
+        ("destroy", C.CFUNCTYPE(None, vp)),
+        ("work_units_per_step", C.c_double),
+    ]
+
+
+class ImageTaskConfigC(Struct):
+    _fields_ = [
+        ("sw", i32), ("sh", i32), ("dw", i32), ("dh", i32),
+        ("batch", i32), ("images_per_step", i32), ("host_io", i32), ("reserved", i32),
+        ("seed", u64), ("total_steps", i64),
+    ]
+
+
+class HarnessConfigC(Struct):
+    _fields_ = [
+        ("num_stages", i32), ("num_micro_batches", i32), ("stage", i32), ("layers", i32),
+        ("hidden", i32), ("tokens", i32), ("ffn_mult", i32), ("profile_reps", i32),
+        ("max_inflight_steps", i32), ("gate_estimate", i32),
+        ("gpu_memory_total", dbl), ("weight_mem", dbl), ("activation_mem", dbl),
+        ("fp_ticks_override", i64), ("bp_ticks_override", i64),
+        ("profile_epochs", i32), ("reserved", i32),
+    ]
+
+
+class HarnessProfileC(Struct):
+    _fields_ = [
+        ("fp_ticks", tick), ("bp_ticks", tick), ("epoch_span", tick), ("stage_bubble_ticks", tick),
+        ("bubble_rate", dbl), ("available_memory", dbl), ("fp_tflops", dbl), ("bp_tflops", dbl),
+        ("n_bubbles", i32), ("reserved", i32), ("clock_offset_err_ns", dbl),
+    ]
+
+
+class RunReportC(Struct):
+    _fields_ = [
+        ("epochs", i32), ("with_tasks", i32),
+        ("makespan_s", dbl), ("bubble_s", dbl), ("used_s", dbl), ("overrun_s", dbl),
+        ("work_units", dbl), ("steps_launched", i64), ("steps_completed", i64),
+        ("dispatch_host_us", dbl), ("max_step_overrun_s", dbl),
+        ("breakdown", StageBreakdownC), ("pauses", i64), ("kills", i64),
+    ]
+
+
+GPU_PROTOTYPES.update({
+    "fr_image_task_create": (C.c_int, [P(ImageTaskConfigC), P(SideTaskVTableC), P(vp)]),
+    "fr_image_task_memory": (C.c_int, [P(ImageTaskConfigC), P(dbl)]),
+    "fr_image_task_buffers": (C.c_int, [vp, P(vp), P(vp), P(vp), P(i64)]),
+    "fr_harness_create": (C.c_int, [P(HarnessConfigC), P(vp)]),
+    "fr_harness_destroy": (C.c_int, [vp]),
+    "fr_harness_get_profile": (C.c_int, [vp, P(HarnessProfileC)]),
+    "fr_harness_stage_bubbles": (C.c_int, [vp, P(BubbleC), i32, P(i32)]),
+    "fr_harness_submit": (C.c_int, [vp, cp, P(SideTaskVTableC), vp, dbl, i32, P(TaskProfileC), P(i32)]),
+    "fr_harness_run": (C.c_int, [vp, i32, i32, P(RunReportC)]),
+    "fr_harness_reprofile": (C.c_int, [vp, cp, P(TaskProfileC)]),
+    "fr_harness_timeline": (C.c_int, [vp, i32, P(dbl), i64, P(i64)]),
+    "fr_harness_launches": (C.c_int, [vp, P(i64), P(i64)]),
+})

@@ -8,15 +8,20 @@
 // At exactly 2x every weight is 128, so px = (a + b + c + d + 2) >> 2.
 //
 // Fast path (sw = 2 dw, sh = 2 dh, dw % 16 == 0), B200-first:
-//   persistent CTAs (one per SM), S-stage smem ring per CTA; for each output
-//   row one elected thread issues TMA bulk copies (cp.async.bulk, UBLKCP) of
-//   the two contiguous source rows (evict-first) and the watermark row
-//   (evict-last: it is re-read by every image of the batch) against an
-//   mbarrier with expect_tx; all threads wait on the barrier, compute 8 output
-//   pixels each from conflict-free 16-byte smem reads, stage the row in smem,
-//   and the elected thread bulk-stores it (cp.async.bulk global<-shared).
-//   One __syncthreads per row; loads for S rows are always in flight, so HBM
-//   sees only full-line streaming requests.
+//  * the watermark is a task constant, so InitSideTask "prepares" it once:
+//    per pixel (w*a + 127) for R,G,B and (255 - a), packed into 16-bit lanes
+//    and laid out group-transposed so each thread's 64 B are one perfectly
+//    coalesced 16 B load per warp-lane (L2-resident, evict-last);
+//  * persistent CTAs (2 per SM) with an S-stage smem ring; one elected
+//    thread streams each output row's two contiguous source rows in with a
+//    TMA bulk copy (cp.async.bulk -> UBLKCP) completing on an mbarrier
+//    (expect_tx), and bulk-stores the finished output row from smem;
+//  * the math runs two 16-bit lanes per 32-bit register: PRMT unpacks and
+//    aligns byte pairs, one IADD3 forms (a+b+c+d+2), one IMAD blends R and G
+//    together (they share alpha), /255 is (t + 1 + (t>>8)) >> 8 done with two
+//    PRMTs and an IADD3, B uses umulhi(t, 2^32/255 rounded up).  Under the
+//    pipeline's power-capped SM clock the kernel must stay HBM-bound, so the
+//    instruction count per byte is what this layout minimises.
 #include <cmath>
 #include <vector>
 
@@ -28,32 +33,55 @@ namespace {
 constexpr int kImgThreads = 256;
 constexpr int kImgStages = 3;
 constexpr int kImgCtasPerSm = 2;
-
-__device__ __forceinline__ uint32_t lanes_lo(uint32_t w) { return w & 0x00FF00FFu; }
-__device__ __forceinline__ uint32_t lanes_hi(uint32_t w) { return (w >> 8) & 0x00FF00FFu; }
+constexpr uint32_t kLaneMask = 0x00FF00FFu;
+constexpr uint32_t kDiv255 = 16843010u;  // ceil(2^32 / 255): umulhi(t, .) = t / 255, t < 65408
 
 __device__ __forceinline__ uint32_t blend255(uint32_t px, uint32_t wmc, uint32_t alpha) {
   return (px * (255u - alpha) + wmc * alpha + 127u) / 255u;
 }
 
+// Prepared watermark: for output row y, 8-pixel group g and pair j (0..3),
+// uint4 {rg(p), bna(p), rg(p+1), bna(p+1)} at ((y*4 + j) * groups + g), p = 8g + 2j,
+// rg = (wR*a + 127) | (wG*a + 127) << 16, bna = (wB*a + 127) | (255 - a) << 16.
+__global__ void img_prepare_wm_kernel(const uint8_t* __restrict__ wm, uint4* __restrict__ out,
+                                      int dw, int dh) {
+  const int groups = dw >> 3;
+  const int64_t total = static_cast<int64_t>(dh) * groups * 4;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int g = static_cast<int>(i % groups);
+    const int64_t yj = i / groups;
+    const int j = static_cast<int>(yj % 4);
+    const int64_t y = yj / 4;
+    uint32_t v[4];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const uint8_t* px = wm + (y * dw + 8 * g + 2 * j + q) * 4;
+      const uint32_t a = px[3];
+      v[2 * q] = (px[0] * a + 127u) | ((px[1] * a + 127u) << 16);
+      v[2 * q + 1] = (px[2] * a + 127u) | ((255u - a) << 16);
+    }
+    out[(y * 4 + j) * groups + g] = make_uint4(v[0], v[1], v[2], v[3]);
+  }
+}
+
 template <int S>
 __global__ void __launch_bounds__(kImgThreads, kImgCtasPerSm)
     img_resize2x_wm_tma(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
-                        const uint8_t* __restrict__ wm, int dw, int dh, int64_t rows) {
+                        const uint4* __restrict__ wmp, int dw, int dh, uint32_t rows) {
   extern __shared__ __align__(128) uint8_t smem[];
   const uint32_t src_row = 6u * static_cast<uint32_t>(dw);  // one source row, RGB
-  const uint32_t wm_row = 4u * static_cast<uint32_t>(dw);
   const uint32_t out_row = 3u * static_cast<uint32_t>(dw);
   const uint32_t a_src = (2u * src_row + 127u) & ~127u;
-  const uint32_t a_wm = (wm_row + 127u) & ~127u;
   const uint32_t a_out = (out_row + 127u) & ~127u;
-  const uint32_t stage_bytes = a_src + a_wm + a_out;
+  const uint32_t stage_bytes = a_src + a_out;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
 
   const int tid = threadIdx.x;
-  const int64_t G = gridDim.x;
-  const int64_t first = blockIdx.x;
-  const int64_t nk = first < rows ? (rows - first + G - 1) / G : 0;
+  const uint32_t G = gridDim.x;
+  const uint32_t first = blockIdx.x;
+  const uint32_t nk = first < rows ? (rows - first + G - 1) / G : 0;
+  const int groups = dw >> 3;
 
   if (tid == 0) {
 #pragma unroll
@@ -62,84 +90,75 @@ __global__ void __launch_bounds__(kImgThreads, kImgCtasPerSm)
   }
   __syncthreads();
 
-  uint64_t pol_stream = 0, pol_keep = 0;
-  if (tid == 0) {
-    pol_stream = frk::policy_evict_first();
-    pol_keep = frk::policy_evict_last();
-  }
-  auto issue = [&](int64_t k) {
+  uint64_t pol_stream = 0;
+  if (tid == 0) pol_stream = frk::policy_evict_first();
+  auto issue = [&](uint32_t k) {
     const int s = static_cast<int>(k % S);
-    const int64_t r = first + k * G;
-    const int64_t img = r / dh;
-    const int64_t y = r - img * dh;
-    uint8_t* st = smem + s * stage_bytes;
-    frk::mbar_arrive_expect_tx(&full[s], 2u * src_row + wm_row);
-    frk::bulk_g2s(st, src + (img * 2 * dh + 2 * y) * static_cast<int64_t>(src_row), 2u * src_row,
+    const uint32_t r = first + k * G;
+    const uint32_t img = r / static_cast<uint32_t>(dh);
+    const uint32_t y = r - img * static_cast<uint32_t>(dh);
+    frk::mbar_arrive_expect_tx(&full[s], 2u * src_row);
+    frk::bulk_g2s(smem + s * stage_bytes,
+                  src + (static_cast<uint64_t>(img) * 2 * dh + 2 * y) * src_row, 2u * src_row,
                   &full[s], pol_stream);
-    frk::bulk_g2s(st + a_src, wm + y * static_cast<int64_t>(wm_row), wm_row, &full[s], pol_keep);
   };
   if (tid == 0)
-    for (int64_t k = 0; k < nk && k < S; ++k) issue(k);
+    for (uint32_t k = 0; k < nk && k < S; ++k) issue(k);
 
-  const int groups = dw >> 3;  // 8 output pixels per thread-iteration
-  for (int64_t k = 0; k < nk; ++k) {
+  uint32_t y = first % static_cast<uint32_t>(dh);  // output row of iteration k
+  for (uint32_t k = 0; k < nk; ++k) {
     const int s = static_cast<int>(k % S);
-    frk::mbar_wait(&full[s], static_cast<uint32_t>((k / S) & 1));
     uint8_t* st = smem + s * stage_bytes;
     const uint8_t* ra = st;
     const uint8_t* rb = st + src_row;
-    const uint8_t* wr = st + a_src;
-    uint8_t* orow = st + a_src + a_wm;
-
+    uint8_t* orow = st + a_src;
     for (int g = tid; g < groups; g += kImgThreads) {
-      uint32_t va[12], vb[12], wv[8];
+      // watermark first (L2): its latency overlaps the wait for the rows
+      uint32_t wv[16];
+      const uint4* pw = wmp + static_cast<size_t>(y) * 4 * groups + g;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint4 x = __ldg(pw + j * groups);
+        wv[4 * j + 0] = x.x; wv[4 * j + 1] = x.y; wv[4 * j + 2] = x.z; wv[4 * j + 3] = x.w;
+      }
+      frk::mbar_wait(&full[s], (k / S) & 1u);
+      uint32_t va[12], vb[12];
       const uint4* pa = reinterpret_cast<const uint4*>(ra + 48 * g);
       const uint4* pb = reinterpret_cast<const uint4*>(rb + 48 * g);
-      const uint4* pw = reinterpret_cast<const uint4*>(wr + 32 * g);
 #pragma unroll
       for (int i = 0; i < 3; ++i) {
-        const uint4 x = pa[i], y = pb[i];
+        const uint4 x = pa[i], z = pb[i];
         va[4 * i + 0] = x.x; va[4 * i + 1] = x.y; va[4 * i + 2] = x.z; va[4 * i + 3] = x.w;
-        vb[4 * i + 0] = y.x; vb[4 * i + 1] = y.y; vb[4 * i + 2] = y.z; vb[4 * i + 3] = y.w;
+        vb[4 * i + 0] = z.x; vb[4 * i + 1] = z.y; vb[4 * i + 2] = z.z; vb[4 * i + 3] = z.w;
       }
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const uint4 x = pw[i];
-        wv[4 * i + 0] = x.x; wv[4 * i + 1] = x.y; wv[4 * i + 2] = x.z; wv[4 * i + 3] = x.w;
-      }
-      // Vertical sums of the two source rows in 16-bit lanes: ev[i] holds
-      // bytes 4i and 4i+2, od[i] bytes 4i+1 and 4i+3 (each <= 510).
+      // vertical sums in 16-bit lanes: ev = bytes (0,2), od = bytes (1,3)
       uint32_t ev[12], od[12];
 #pragma unroll
       for (int i = 0; i < 12; ++i) {
-        ev[i] = lanes_lo(va[i]) + lanes_lo(vb[i]);
-        od[i] = lanes_hi(va[i]) + lanes_hi(vb[i]);
+        ev[i] = (va[i] & kLaneMask) + (vb[i] & kLaneMask);
+        od[i] = __byte_perm(va[i], 0u, 0x4341) + __byte_perm(vb[i], 0u, 0x4341);
       }
       uint32_t rgb[8];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {  // pixel pair (2q, 2q+1) = source words 3q..3q+2
         const uint32_t e0 = ev[3 * q], e1 = ev[3 * q + 1], e2 = ev[3 * q + 2];
         const uint32_t o0 = od[3 * q], o1 = od[3 * q + 1], o2 = od[3 * q + 2];
-        // Horizontal pairs aligned lane-for-lane with PRMT, then (s + 2) >> 2.
         uint32_t rg[2], bb;
-        rg[0] = __byte_perm(e0, o0, 0x5410) + __byte_perm(o0, e1, 0x5432);  // R0 | G0
-        rg[1] = __byte_perm(e1, o1, 0x7632) + __byte_perm(o2, e2, 0x7610);  // R1 | G1
-        bb = __byte_perm(e0, e2, 0x5432) + __byte_perm(o1, o2, 0x7610);     // B0 | B1
-        rg[0] = ((rg[0] + 0x00020002u) >> 2) & 0x00FF00FFu;
-        rg[1] = ((rg[1] + 0x00020002u) >> 2) & 0x00FF00FFu;
-        bb = ((bb + 0x00020002u) >> 2) & 0x00FF00FFu;
+        rg[0] = __byte_perm(e0, o0, 0x5410) + __byte_perm(o0, e1, 0x5432) + 0x00020002u;  // R0|G0
+        rg[1] = __byte_perm(e1, o1, 0x7632) + __byte_perm(o2, e2, 0x7610) + 0x00020002u;  // R1|G1
+        bb = __byte_perm(e0, e2, 0x5432) + __byte_perm(o1, o2, 0x7610) + 0x00020002u;     // B0|B1
+        rg[0] = (rg[0] >> 2) & kLaneMask;
+        rg[1] = (rg[1] >> 2) & kLaneMask;
+        bb = (bb >> 2) & kLaneMask;
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-          const uint32_t w = wv[2 * q + j];
-          const uint32_t a = w >> 24, na = 255u - a;
-          // R,G share the pixel's alpha: blend both 16-bit lanes in one IMAD
-          // chain, then floor(t / 255) = (t + 1 + (t >> 8)) >> 8 per lane
-          // (exact for t <= 65407, checked exhaustively in the tests).
-          const uint32_t t = rg[j] * na + (__byte_perm(w, 0u, 0x4140) * a + 0x007F007Fu);
-          const uint32_t qrg = ((t + 0x00010001u + ((t >> 8) & 0x00FF00FFu)) >> 8) & 0x00FF00FFu;
+          const uint32_t wrg = wv[4 * q + 2 * j], wbna = wv[4 * q + 2 * j + 1];
+          const uint32_t na = wbna >> 16;
+          const uint32_t t = rg[j] * na + wrg;  // R,G lanes share alpha
+          const uint32_t u = t + __byte_perm(t, 0u, 0x4341) + 0x00010001u;
+          const uint32_t qrg = __byte_perm(u, 0u, 0x4341);  // (t + 1 + (t>>8)) >> 8 per lane
           const uint32_t b = j ? (bb >> 16) : (bb & 0xFFFFu);
-          const uint32_t tb = b * na + ((w >> 16) & 0xFFu) * a + 127u;
-          const uint32_t qb = (tb + 1u + (tb >> 8)) >> 8;
+          const uint32_t qb = __umulhi(b * na + (wbna & 0xFFFFu), kDiv255);
           rgb[2 * q + j] = __byte_perm(qrg, qb, 0x0420);  // R G B _
         }
       }
@@ -154,11 +173,12 @@ __global__ void __launch_bounds__(kImgThreads, kImgCtasPerSm)
     if (tid == 0 && k + 1 >= S) frk::bulk_wait_read<S - 2>();
     __syncthreads();
     if (tid == 0) {
-      frk::bulk_s2g(dst + (first + k * G) * static_cast<int64_t>(out_row), orow, out_row,
-                    pol_stream);
+      frk::bulk_s2g(dst + static_cast<uint64_t>(first + k * G) * out_row, orow, out_row, pol_stream);
       frk::bulk_commit();
       if (k + S < nk) issue(k + S);
     }
+    y += G;
+    while (y >= static_cast<uint32_t>(dh)) y -= static_cast<uint32_t>(dh);
   }
   if (tid == 0) frk::bulk_wait<0>();
 }
@@ -251,14 +271,20 @@ int grid_for(int64_t work, int threads, int per_sm) {
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(sms) * per_sm)));
 }
 
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
 }  // namespace
 
 struct fr_img_plan {
   int sw = 0, sh = 0, dw = 0, dh = 0;
   int path = FR_IMG_PATH_GENERAL;
   int32_t* d_tab = nullptr;
+  void* d_wm = nullptr;  // plan-owned prepared watermark for fr_img_resize_watermark
   int smem = 0;
   int sms = 0;
+  size_t prepared_bytes() const {
+    return path == FR_IMG_PATH_TMA_2X ? static_cast<size_t>(dw) * dh * 8 : static_cast<size_t>(dw) * dh * 4;
+  }
 };
 
 extern "C" {
@@ -282,7 +308,7 @@ int fr_img_plan_create(int32_t sw, int32_t sh, int32_t dw, int32_t dh, fr_img_pl
   const bool two_x = sw == 2 * dw && sh == 2 * dh && dw % 16 == 0;
   if (two_x) {
     auto al = [](int x) { return (x + 127) & ~127; };
-    plan->smem = kImgStages * (al(12 * dw) + al(4 * dw) + al(3 * dw)) + kImgStages * 8;
+    plan->smem = kImgStages * (al(12 * dw) + al(3 * dw)) + kImgStages * 8;
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     if (plan->smem <= optin) {
@@ -302,11 +328,12 @@ int fr_img_plan_create(int32_t sw, int32_t sh, int32_t dw, int32_t dh, fr_img_pl
     e = cudaMalloc(&plan->d_tab, tab.size() * sizeof(int32_t));
     if (e == cudaSuccess)
       e = cudaMemcpy(plan->d_tab, tab.data(), tab.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) {
-      if (plan->d_tab) cudaFree(plan->d_tab);
-      delete plan;
-      return frcapi::cuda_status(e, "coefficient table upload");
-    }
+  }
+  if (e == cudaSuccess) e = cudaMalloc(&plan->d_wm, plan->prepared_bytes());
+  if (e != cudaSuccess) {
+    if (plan->d_tab) cudaFree(plan->d_tab);
+    delete plan;
+    return frcapi::cuda_status(e, "image plan setup");
   }
   *out = plan;
   return FR_OK;
@@ -315,6 +342,7 @@ int fr_img_plan_create(int32_t sw, int32_t sh, int32_t dw, int32_t dh, fr_img_pl
 int fr_img_plan_destroy(fr_img_plan* plan) {
   if (!plan) return FR_OK;
   if (plan->d_tab) cudaFree(plan->d_tab);
+  if (plan->d_wm) cudaFree(plan->d_wm);
   delete plan;
   return FR_OK;
 }
@@ -325,27 +353,62 @@ int fr_img_plan_path(const fr_img_plan* plan, int32_t* path) {
   return FR_OK;
 }
 
+int fr_img_prepared_bytes(const fr_img_plan* plan, int64_t* bytes) {
+  if (!plan || !bytes) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  *bytes = static_cast<int64_t>(plan->prepared_bytes());
+  return FR_OK;
+}
+
+int fr_img_prepare_watermark(const fr_img_plan* plan, const uint8_t* wm_rgba, void* prepared,
+                             void* stream) {
+  if (!plan || !wm_rgba || !prepared) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  auto s = static_cast<cudaStream_t>(stream);
+  if (plan->path == FR_IMG_PATH_TMA_2X) {
+    if (!aligned16(prepared)) return frcapi::fail(FR_ERR_UNSUPPORTED, "prepared watermark must be 16-byte aligned");
+    const int64_t total = static_cast<int64_t>(plan->dh) * (plan->dw >> 3) * 4;
+    img_prepare_wm_kernel<<<grid_for(total, 256, 8), 256, 0, s>>>(
+        wm_rgba, static_cast<uint4*>(prepared), plan->dw, plan->dh);
+  } else {
+    FR_CUDA_TRY(cudaMemcpyAsync(prepared, wm_rgba, plan->prepared_bytes(), cudaMemcpyDeviceToDevice, s));
+  }
+  FR_CUDA_LAUNCHED("img_prepare_watermark");
+  return FR_OK;
+}
+
+int fr_img_resize_watermark_prepared(const fr_img_plan* plan, const uint8_t* src, uint8_t* dst,
+                                     const void* prepared, int32_t n, void* stream) {
+  if (!plan || (n > 0 && (!src || !dst || !prepared))) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  if (n < 0) return frcapi::fail(FR_ERR_VALIDATION, "n must be >= 0", "n");
+  if (n == 0) return FR_OK;
+  auto s = static_cast<cudaStream_t>(stream);
+  if (plan->path == FR_IMG_PATH_TMA_2X) {
+    if (!aligned16(src) || !aligned16(dst) || !aligned16(prepared))
+      return frcapi::fail(FR_ERR_UNSUPPORTED, "TMA path needs 16-byte aligned buffers");
+    const int64_t rows = static_cast<int64_t>(n) * plan->dh;
+    if (rows >= (int64_t{1} << 31)) return frcapi::fail(FR_ERR_UNSUPPORTED, "too many rows in one step");
+    const int grid = static_cast<int>(std::min<int64_t>(rows, int64_t(plan->sms) * kImgCtasPerSm));
+    img_resize2x_wm_tma<kImgStages><<<grid, kImgThreads, plan->smem, s>>>(
+        src, dst, static_cast<const uint4*>(prepared), plan->dw, plan->dh, static_cast<uint32_t>(rows));
+  } else {
+    const int64_t total = static_cast<int64_t>(n) * plan->dw * plan->dh;
+    img_resize_wm_general<<<grid_for(total, 256, 8), 256, 0, s>>>(
+        src, dst, static_cast<const uint8_t*>(prepared), plan->d_tab, plan->sw, plan->sh, plan->dw,
+        plan->dh, total);
+  }
+  FR_CUDA_LAUNCHED("img_resize_watermark");
+  return FR_OK;
+}
+
 int fr_img_resize_watermark(const fr_img_plan* plan, const uint8_t* src, uint8_t* dst,
                             const uint8_t* wm, int32_t n, void* stream) {
   if (!plan || (n > 0 && (!src || !dst || !wm))) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
   if (n < 0) return frcapi::fail(FR_ERR_VALIDATION, "n must be >= 0", "n");
   if (n == 0) return FR_OK;
-  auto s = static_cast<cudaStream_t>(stream);
-  if (plan->path == FR_IMG_PATH_TMA_2X) {
-    const bool aligned = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst) |
-                           reinterpret_cast<uintptr_t>(wm)) & 15u) == 0;
-    if (!aligned) return frcapi::fail(FR_ERR_UNSUPPORTED, "TMA path needs 16-byte aligned buffers");
-    const int64_t rows = static_cast<int64_t>(n) * plan->dh;
-    const int grid = static_cast<int>(std::min<int64_t>(rows, int64_t(plan->sms) * kImgCtasPerSm));
-    img_resize2x_wm_tma<kImgStages><<<grid, kImgThreads, plan->smem, s>>>(src, dst, wm, plan->dw,
-                                                                        plan->dh, rows);
-  } else {
-    const int64_t total = static_cast<int64_t>(n) * plan->dw * plan->dh;
-    img_resize_wm_general<<<grid_for(total, 256, 8), 256, 0, s>>>(
-        src, dst, wm, plan->d_tab, plan->sw, plan->sh, plan->dw, plan->dh, total);
-  }
-  FR_CUDA_LAUNCHED("img_resize_watermark");
-  return FR_OK;
+  if (plan->path == FR_IMG_PATH_TMA_2X && (!aligned16(src) || !aligned16(dst)))
+    return frcapi::fail(FR_ERR_UNSUPPORTED, "TMA path needs 16-byte aligned buffers");
+  const int rc = fr_img_prepare_watermark(plan, wm, plan->d_wm, stream);
+  if (rc != FR_OK) return rc;
+  return fr_img_resize_watermark_prepared(plan, src, dst, plan->d_wm, n, stream);
 }
 
 int fr_img_generate(uint8_t* dst, int32_t n, int32_t w, int32_t h, int32_t ch, uint64_t seed,

@@ -1,0 +1,834 @@
+// The GPU bubble-harvesting runtime: one stage of a 1F1B pipeline of real
+// tensor-core GEMMs on a high-priority stream, and one side-task worker
+// that serves bubbles with bounded steps on a low-priority stream.
+//
+// This is the real-time counterpart of the reference's missing engine
+// (engine.hpp:94-98, semantics SPEC.md:466-517 / SURVEY.md Appendix B):
+//  * bubble signals come from the device (timeline.cu gap kernels) through a
+//    host-mapped ring: BubbleStarted when the stage's previous op completes,
+//    BubbleEnded when the next op's dependency arrives;
+//  * the manager runs Alg. 2 (on_bubble_started / on_bubble_ended) over this
+//    GPU's WorkerState, the task runs the five-state machine through
+//    apply_transition, and every RunNextStep passes iterative_run's
+//    program-directed gate (strict double compare, task.cpp:89-100) with the
+//    *projected* device start time of the step as `now`, so steps can be
+//    queued back to back without idling the GPU between them;
+//  * a pause takes effect when the in-flight steps drain (last_paused is the
+//    drain time) and framework_enforce (limits.cpp:21-26) judges it after the
+//    grace period.
+// Everything is timed on the device (globaltimer / CUDA events).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <deque>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "capi_util.hpp"
+#include "freeride_gpu.h"
+#include "host/freeride.hpp"
+#include "runtime/standin.hpp"
+#include "runtime/timeline.cuh"
+
+using namespace freeride;
+using namespace freeride::rt;
+
+namespace {
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+std::int64_t host_ns() {
+  return std::chrono::duration_cast<std::chrono::nanoseconds>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+struct HookError : std::runtime_error {
+  int code;
+  HookError(int c, const std::string& what) : std::runtime_error(what), code(c) {}
+};
+
+void hook(int rc, const char* name) {
+  if (rc != FR_OK) throw HookError(rc, std::string("side-task hook ") + name + " failed");
+}
+
+constexpr double kTick = 1e-9;  // runtime ticks are nanoseconds
+constexpr std::uint32_t kRingSlots = 1u << 16;
+constexpr std::uint32_t kBubbleIds = 1024;  // bubble ids per epoch in a ring code
+constexpr Tick kGraceTicks = 100'000'000;  // LimitConfig::grace_period (0.1 s), ns ticks
+
+struct Task {
+  std::string id;
+  fr_side_task_vtable vt{};
+  void* user = nullptr;
+  SideTaskRuntime rt;
+  TaskProfile prof;
+  bool initializing = false;
+  cudaEvent_t init_a = nullptr, init_b = nullptr;
+  bool init_recorded = false;
+  ~Task() {
+    if (init_a) cudaEventDestroy(init_a);
+    if (init_b) cudaEventDestroy(init_b);
+    if (vt.destroy && user) vt.destroy(user);
+  }
+};
+
+struct StepRec {
+  cudaEvent_t a, b;
+  Task* task;
+};
+
+}  // namespace
+
+struct fr_harness {
+  fr_harness_config cfg{};
+  int device = 0;
+  cudaStream_t train = nullptr, side = nullptr;
+  std::unique_ptr<StandIn> standin;
+  RingSlot* ring = nullptr;       // host view
+  RingSlot* ring_dev = nullptr;   // device view
+  TimelineCtl* ctl = nullptr;
+  std::uint64_t* stamp = nullptr;  // mapped
+  std::uint32_t* flag = nullptr;   // mapped
+  std::uint64_t* stamp_dev = nullptr;
+  std::uint32_t* flag_dev = nullptr;
+  std::int64_t clock_off = 0;      // device_ns = host_ns + clock_off
+  double clock_err = 0;
+  std::int64_t launch_lat = 5000;  // host launch -> device start, ns
+
+  // schedule of this stage (one epoch, undelayed)
+  PipelineConfig pcfg;
+  Tick fp = 0, bp = 0, span = 0;
+  double fp_tflops = 0, bp_tflops = 0, rate = 0, avail = 0;
+  std::vector<OpEvent> ops;              // issue order
+  std::vector<std::int64_t> ready;       // dependency-ready offset per op
+  std::vector<int> gap_bubble;           // per gap (2m+1): bubble index or -1
+  std::vector<Bubble> bubbles;           // this stage, one epoch, relative ticks
+
+  std::vector<WorkerState> workers;      // this process serves one worker
+  std::map<std::string, std::unique_ptr<Task>> tasks;
+
+  // last run
+  std::vector<double> op_se, bubble_se, step_se;
+  std::int64_t last_side_steps = 0, last_train_ops = 0;
+  std::vector<cudaEvent_t> pool;
+  std::size_t pool_used = 0;
+
+  cudaEvent_t ev() {
+    if (pool_used == pool.size()) {
+      cudaEvent_t e;
+      ck(cudaEventCreate(&e), "cudaEventCreate");
+      pool.push_back(e);
+    }
+    return pool[pool_used++];
+  }
+
+  ~fr_harness() {
+    if (train) cudaStreamSynchronize(train);
+    if (side) cudaStreamSynchronize(side);
+    tasks.clear();
+    standin.reset();
+    for (cudaEvent_t e : pool) cudaEventDestroy(e);
+    if (ring) cudaFreeHost(ring);
+    if (stamp) cudaFreeHost(stamp);
+    if (flag) cudaFreeHost(flag);
+    if (ctl) cudaFree(ctl);
+    if (train) cudaStreamDestroy(train);
+    if (side) cudaStreamDestroy(side);
+  }
+
+  void calibrate() {
+    // device_ns - host_ns is bracketed by [g - t1, g - t0] for every stamp;
+    // keep the tightest lower bound (error <= device->host visibility).
+    std::int64_t lo = INT64_MIN, hi = INT64_MAX, best_rtt = INT64_MAX, lat = 0;
+    for (std::uint32_t i = 1; i <= 64; ++i) {
+      const std::int64_t t0 = host_ns();
+      launch_stamp(stamp_dev, flag_dev, i, side);
+      while (*reinterpret_cast<volatile std::uint32_t*>(flag) != i) {
+      }
+      const std::int64_t t1 = host_ns();
+      const auto g = static_cast<std::int64_t>(*reinterpret_cast<volatile std::uint64_t*>(stamp));
+      lo = std::max(lo, g - t1);
+      hi = std::min(hi, g - t0);
+      if (t1 - t0 < best_rtt) {
+        best_rtt = t1 - t0;
+      }
+      lat = (i == 1) ? (g - t0) : std::min(lat, g - t0);
+    }
+    clock_off = lo;
+    clock_err = static_cast<double>(std::max<std::int64_t>(0, hi - lo));
+    launch_lat = std::max<std::int64_t>(1000, lat - lo);  // host call -> device start
+  }
+
+  std::int64_t dev_now() const { return host_ns() + clock_off; }
+
+  void build_schedule_from(Tick fpt, Tick bpt) {
+    const int p = cfg.num_stages, m = cfg.num_micro_batches, s = cfg.stage;
+    pcfg = PipelineConfig{};
+    pcfg.num_stages = p;
+    pcfg.num_micro_batches = m;
+    pcfg.fp_duration = {fpt};
+    pcfg.bp_duration = {bpt};
+    pcfg.num_epochs = 1;
+    pcfg.tick_seconds = kTick;
+    pcfg.gpu_memory_total = cfg.gpu_memory_total;
+    const double gib = 1024.0 * 1024.0 * 1024.0;
+    const double w = cfg.weight_mem >= 0 ? cfg.weight_mem
+                                         : static_cast<double>(standin->weight_bytes()) * 8.0 / gib;
+    const double a = cfg.activation_mem >= 0
+                         ? cfg.activation_mem
+                         : static_cast<double>(standin->activation_bytes()) / gib;
+    pcfg.stage_memory = default_stage_memory(p, cfg.gpu_memory_total, w, a);
+    const ScheduleTrace tr = build_schedule(pcfg);
+    const auto linked = extract_bubbles_linked(tr);
+    std::vector<Bubble> all;
+    for (const auto& lb : linked) all.push_back(lb.bubble);
+    rate = bubble_rate(tr, all);
+    span = tr.epoch_spans[0].second - tr.epoch_spans[0].first;
+    avail = pcfg.available_memory(s);
+    fp = fpt;
+    bp = bpt;
+    // this stage's ops in issue order with their cross-stage ready times
+    ops.clear();
+    ready.clear();
+    std::map<std::tuple<int, int, int>, const OpEvent*> at;  // (stage, kind, mb)
+    for (const OpEvent& o : tr.ops) at[{o.stage, static_cast<int>(o.kind), o.micro_batch}] = &o;
+    for (const auto& [k, mb] : stage_issue_order(s, p, m)) {
+      const OpEvent* o = at.at({s, static_cast<int>(k), mb});
+      ops.push_back(*o);
+      std::int64_t r = 0;
+      if (k == OpKind::FP && s > 0) r = at.at({s - 1, 0, mb})->end;
+      if (k == OpKind::BP && s < p - 1) r = at.at({s + 1, 1, mb})->end;
+      ready.push_back(r);
+    }
+    // map each of this stage's bubbles to the gap it occupies
+    gap_bubble.assign(ops.size() + 1, -1);
+    bubbles.clear();
+    for (const auto& lb : linked) {
+      if (lb.bubble.stage != s) continue;
+      int gap = static_cast<int>(ops.size());  // trailing
+      if (lb.next_op >= 0) {
+        const OpEvent& nx = tr.ops[static_cast<std::size_t>(lb.next_op)];
+        for (std::size_t i = 0; i < ops.size(); ++i)
+          if (ops[i].kind == nx.kind && ops[i].micro_batch == nx.micro_batch) gap = static_cast<int>(i);
+      }
+      gap_bubble[static_cast<std::size_t>(gap)] = static_cast<int>(bubbles.size());
+      bubbles.push_back(lb.bubble);
+    }
+  }
+
+  Tick measure_op(bool is_fp, int reps) {
+    std::vector<float> ms;
+    for (int i = 0; i < reps + 2; ++i) {
+      cudaEvent_t a = ev(), b = ev();
+      ck(cudaEventRecord(a, train), "record");
+      is_fp ? standin->launch_fp(train) : standin->launch_bp(train);
+      ck(cudaEventRecord(b, train), "record");
+      ck(cudaEventSynchronize(b), "sync");
+      float t = 0;
+      ck(cudaEventElapsedTime(&t, a, b), "elapsed");
+      if (i >= 2) ms.push_back(t);
+    }
+    pool_used = 0;
+    std::sort(ms.begin(), ms.end());
+    return static_cast<Tick>(std::llround(static_cast<double>(ms[ms.size() / 2]) * 1e6));
+  }
+
+  // Bubble profiler (§4.3: "runs DeepSpeed ... and automatically
+  // measures each bubble's duration"): first re-derive the op durations the
+  // stage actually shows inside a pipeline (idle gaps let the GPU boost, so
+  // back-to-back op timing is pessimistic), rebuild the schedule from them,
+  // then dry-run `epochs` epochs and take each bubble's median duration as
+  // its profiled duration -- the value StartSideTask carries as bubble end.
+  void profile_in_pipeline(int epochs) {
+    if (epochs <= 0) return;
+    fr_run_report rep{};
+    auto median = [](std::vector<double> v) {
+      std::sort(v.begin(), v.end());
+      return v.empty() ? 0.0 : v[v.size() / 2];
+    };
+    for (int pass = 0; pass < 2; ++pass) {
+      run(epochs, false, &rep);
+      std::vector<double> fpd, bpd;
+      for (std::size_t i = 0; i < op_se.size() / 2; ++i)
+        (ops[i % ops.size()].kind == OpKind::FP ? fpd : bpd).push_back(op_se[2 * i + 1] - op_se[2 * i]);
+      const Tick f = cfg.fp_ticks_override > 0 ? fp : static_cast<Tick>(std::llround(median(fpd) / kTick));
+      const Tick b = cfg.bp_ticks_override > 0 ? bp : static_cast<Tick>(std::llround(median(bpd) / kTick));
+      build_schedule_from(f, b);
+    }
+    run(epochs, false, &rep);
+    const std::size_t nb = bubbles.size();
+    if (nb == 0 || bubble_se.size() / 2 != nb * static_cast<std::size_t>(epochs)) return;
+    for (std::size_t j = 0; j < nb; ++j) {
+      std::vector<double> d;
+      for (int e = 0; e < epochs; ++e) {
+        const std::size_t k = static_cast<std::size_t>(e) * nb + j;
+        d.push_back(bubble_se[2 * k + 1] - bubble_se[2 * k]);
+      }
+      bubbles[j].duration = static_cast<Tick>(std::llround(median(d) / kTick));
+    }
+  }
+
+  // GateEstimate (config.hpp:17,24): profiled mean by default, max if asked.
+  double gate_est(const Task& t) const {
+    return cfg.gate_estimate == 1 ? t.prof.max_per_step_duration.value_or(0.0)
+                                  : t.prof.est_per_step_duration.value_or(0.0);
+  }
+
+  std::vector<Task*> step_task;  // task of each step of the last run
+
+  TaskView lookup(const std::string& id) const {
+    auto it = tasks.find(id);
+    if (it == tasks.end()) throw frcapi::CallbackStatus(FR_ERR_NOT_FOUND);
+    return TaskView{it->second->rt.state, it->second->initializing};
+  }
+
+  void run(int epochs, bool with_tasks, fr_run_report* rep);
+};
+
+namespace {
+
+double elapsed_s(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0;
+  ck(cudaEventElapsedTime(&ms, a, b), "cudaEventElapsedTime");
+  return static_cast<double>(ms) * 1e-3;
+}
+
+}  // namespace
+
+void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
+  pool_used = 0;
+  std::memset(ring, 0, sizeof(RingSlot) * kRingSlots);
+  calibrate();
+  ck(cudaDeviceSynchronize(), "pre-run sync");
+  const int nops = static_cast<int>(ops.size());
+  const int ngaps = nops + 1;
+
+  // ---- training-stream program for all epochs (enqueued by its own thread,
+  //      as a training framework would, so the worker never blocks on it)
+  struct EpochEvents {
+    std::vector<cudaEvent_t> op_start, op_end;
+    cudaEvent_t end;
+  };
+  std::vector<EpochEvents> eev(static_cast<std::size_t>(epochs));
+  for (auto& e : eev) {
+    e.op_start.resize(static_cast<std::size_t>(nops));
+    e.op_end.resize(static_cast<std::size_t>(nops));
+    for (int i = 0; i < nops; ++i) {
+      e.op_start[i] = ev();
+      e.op_end[i] = ev();
+    }
+    e.end = ev();
+  }
+  cudaEvent_t run_start = ev();
+  std::int64_t n_events = 0;
+  for (int g = 0; g < ngaps; ++g)
+    if (gap_bubble[static_cast<std::size_t>(g)] >= 0) n_events += 2;
+  n_events *= epochs;
+  if (n_events >= static_cast<std::int64_t>(kRingSlots))
+    throw std::runtime_error("too many epochs for the event ring in one run");
+
+  std::atomic<bool> train_failed{false};
+  std::string train_err;
+  std::thread trainer([&] {
+    try {
+      ck(cudaSetDevice(device), "cudaSetDevice");
+      ck(cudaEventRecord(run_start, train), "record");
+      std::int64_t slot = 0;
+      for (int e = 0; e < epochs; ++e) {
+        for (int g = 0; g < ngaps; ++g) {
+          GapArgs a{};
+          a.ctl = ctl;
+          a.ring = ring_dev;
+          a.ring_mask = kRingSlots - 1;
+          const int b = gap_bubble[static_cast<std::size_t>(g)];
+          a.slot_start = a.slot_end = -1;
+          if (b >= 0) {
+            const std::uint32_t id = static_cast<std::uint32_t>(e) * kBubbleIds + static_cast<std::uint32_t>(b);
+            a.slot_start = slot++;
+            a.slot_end = slot++;
+            a.code_start = ring_code(kEvBubbleStart, id);
+            a.code_end = ring_code(kEvBubbleEnd, id);
+          }
+          a.span_ns = span;
+          if (g < nops) {
+            a.mode = (e == 0 && g == 0) ? 2 : 0;
+            a.ready_ns = ready[static_cast<std::size_t>(g)];
+            launch_gap(a, train);
+            ck(cudaEventRecord(eev[e].op_start[g], train), "record");
+            ops[static_cast<std::size_t>(g)].kind == OpKind::FP ? standin->launch_fp(train)
+                                                               : standin->launch_bp(train);
+            ck(cudaEventRecord(eev[e].op_end[g], train), "record");
+          } else {
+            a.mode = 1;
+            a.ready_ns = 0;
+            launch_gap(a, train);
+            ck(cudaEventRecord(eev[e].end, train), "record");
+          }
+        }
+      }
+      ck(cudaGetLastError(), "training enqueue");
+    } catch (const std::exception& ex) {
+      train_err = ex.what();
+      train_failed = true;
+    }
+  });
+
+  // ---- the worker: Alg. 2 + iterative interface, in real time
+  WorkerState& ws = workers[0];
+  const auto view = [this](const std::string& id) { return lookup(id); };
+  std::vector<StepRec> steps;
+  std::deque<std::size_t> inflight;  // indices into steps
+  std::vector<std::pair<std::int64_t, std::int64_t>> init_spans;
+  Task* running = nullptr;
+  std::int64_t bubble_end_dev = 0;   // device ns (profiled end)
+  std::int64_t proj_end_dev = 0;     // projected end of the queued steps
+  bool pause_pending = false, gate_closed = false, kill_judged = false;
+  std::int64_t pause_issued_dev = 0;
+  std::int64_t launched = 0, completed = 0, pauses = 0, kills = 0;
+  double dispatch_ns = 0;
+  std::int64_t next_slot = 0;
+  const double step_units = [&] {
+    for (auto& kv : tasks) return kv.second->vt.work_units_per_step;
+    return 0.0;
+  }();
+  double units = 0;
+  const int depth = std::max(1, cfg.max_inflight_steps);
+
+  auto task_of = [&](const std::string& id) -> Task& { return *tasks.at(id); };
+  auto stop_task = [&](Task& t, Tick now) {
+    apply_transition(t.rt, TransitionKind::StopSideTask, now);
+    hook(t.vt.stop ? t.vt.stop(t.user) : FR_OK, "stop");
+    if (ws.current_task && *ws.current_task == t.id) ws.current_task.reset();  // Appendix B rule 8
+    if (running == &t) running = nullptr;
+  };
+  auto drain_completions = [&] {
+    while (!inflight.empty()) {
+      const cudaError_t q = cudaEventQuery(steps[inflight.front()].b);
+      if (q == cudaErrorNotReady) break;
+      ck(q, "step event");
+      Task* st = steps[inflight.front()].task;
+      inflight.pop_front();
+      ++completed;
+      units += step_units;
+      st->rt.steps_completed++;  // counted at step end (task.hpp:55)
+      // Re-anchor the projection: the next queued step started when this one
+      // ended (~now), so drift from mis-estimated step times cannot build up.
+      if (!inflight.empty()) {
+        const double est = gate_est(*st);
+        proj_end_dev = std::max<std::int64_t>(
+            proj_end_dev, dev_now() + static_cast<std::int64_t>(std::llround(est / kTick)) *
+                                          static_cast<std::int64_t>(inflight.size()));
+      }
+      if (running) {
+        int32_t done = 0;
+        if (running->vt.finished) hook(running->vt.finished(running->user, running->rt.steps_completed, &done), "finished");
+        if (done) stop_task(*running, dev_now());
+      }
+    }
+  };
+  auto finish_pause = [&] {
+    if (!pause_pending || !inflight.empty()) return;
+    pause_pending = false;
+    if (running && running->rt.state == SideTaskState::Running) {
+      const Tick now = dev_now();
+      apply_transition(running->rt, TransitionKind::PauseSideTask, now);
+      hook(running->vt.pause ? running->vt.pause(running->user) : FR_OK, "pause");
+      ++pauses;
+    }
+    running = nullptr;
+  };
+  auto finish_init = [&] {
+    for (auto& kv : tasks) {
+      Task& t = *kv.second;
+      if (!t.initializing) continue;
+      const cudaError_t q = cudaEventQuery(t.init_b);
+      if (q == cudaErrorNotReady) continue;
+      ck(q, "init event");
+      t.initializing = false;
+      apply_transition(t.rt, TransitionKind::InitSideTask, dev_now());
+      t.rt.assigned_worker = 0;
+    }
+  };
+
+  while (true) {
+    if (train_failed) {
+      trainer.join();
+      throw std::runtime_error("training stream: " + train_err);
+    }
+    // 1. bubble signals from the device
+    volatile RingSlot* sl = ring + (static_cast<std::uint64_t>(next_slot) & (kRingSlots - 1));
+    if (next_slot < n_events && sl->seq == static_cast<std::uint32_t>(next_slot + 1)) {
+      const std::uint32_t code = sl->code;
+      const auto t_dev = static_cast<std::int64_t>(sl->t_ns);
+      const std::int64_t seen = host_ns();
+      ++next_slot;
+      clock_off = std::max(clock_off, t_dev - seen);  // causality tightens the bound
+      const std::uint32_t kind = code >> 28, id = code & 0x0FFFFFFFu;
+      const Bubble& pb = bubbles[id % kBubbleIds];
+      if (with_tasks && kind == kEvBubbleStart) {
+        Bubble b = pb;
+        b.epoch = static_cast<int>(id / kBubbleIds);
+        b.start = t_dev;
+        for (const ManagerAction& act : on_bubble_started(ws, b, view)) {
+          Task& t = task_of(act.task_id);
+          if (act.kind == ManagerActionKind::IssueInit) {
+            if (!t.init_a) {
+              ck(cudaEventCreate(&t.init_a), "init event");
+              ck(cudaEventCreate(&t.init_b), "init event");
+            }
+            ck(cudaEventRecord(t.init_a, side), "record");
+            hook(t.vt.init(t.user, side), "init");
+            ck(cudaEventRecord(t.init_b, side), "record");
+            t.initializing = true;
+            t.init_recorded = true;
+          } else if (act.kind == ManagerActionKind::IssueStart) {
+            apply_transition(t.rt, TransitionKind::StartSideTask, t_dev);
+            hook(t.vt.start ? t.vt.start(t.user) : FR_OK, "start");
+            running = &t;
+            bubble_end_dev = t_dev + pb.duration;
+            proj_end_dev = 0;
+            gate_closed = false;
+          }
+        }
+      } else if (with_tasks && kind == kEvBubbleEnd) {
+        for (const ManagerAction& act : on_bubble_ended(ws, t_dev, view)) {
+          if (act.kind == ManagerActionKind::IssuePause) {
+            pause_pending = true;
+            kill_judged = false;
+            pause_issued_dev = t_dev;
+          }
+        }
+      }
+    }
+    if (!with_tasks && next_slot >= n_events) break;
+    // 2. step completions, init completion, pause drains
+    if (with_tasks) {
+      drain_completions();
+      finish_init();
+      finish_pause();
+      // 3. dispatch: the program-directed gate at the projected start time
+      while (running && !pause_pending && !gate_closed &&
+             running->rt.state == SideTaskState::Running &&
+             static_cast<int>(inflight.size()) < depth) {
+        const std::int64_t h0 = host_ns();
+        const std::int64_t now = h0 + clock_off;
+        const std::int64_t start = std::max(now + launch_lat, proj_end_dev);
+        const double est = gate_est(*running);
+        const Tick est_ticks = static_cast<Tick>(std::llround(est / kTick));
+        const IterativeDecision d = iterative_run(running->rt, bubble_end_dev, start, est, kTick, est_ticks);
+        if (!d.run) {
+          gate_closed = true;  // yield until the next transition
+          break;
+        }
+        StepRec r{ev(), ev(), running};
+        ck(cudaEventRecord(r.a, side), "record");
+        hook(running->vt.run_next_step(running->user, side), "run_next_step");
+        ck(cudaEventRecord(r.b, side), "record");
+        apply_transition(running->rt, TransitionKind::RunNextStep, start);
+        steps.push_back(r);
+        inflight.push_back(steps.size() - 1);
+        proj_end_dev = d.step_end;
+        ++launched;
+        dispatch_ns += static_cast<double>(host_ns() - h0);
+      }
+      // framework-enforced limit: a pause not observed within the grace
+      // period gets a Kill verdict (limits.cpp:21-26); kernels cannot be
+      // revoked, so the verdict is counted and reported.
+      if (pause_pending && !kill_judged && running &&
+          framework_enforce(running->rt.last_paused, pause_issued_dev, dev_now(), kGraceTicks) ==
+              Enforce::Kill) {
+        ++kills;
+        kill_judged = true;
+      }
+      if (next_slot >= n_events && inflight.empty() && !pause_pending) break;
+    }
+  }
+  trainer.join();
+  if (train_failed) throw std::runtime_error("training stream: " + train_err);
+  ck(cudaStreamSynchronize(train), "train sync");
+  ck(cudaStreamSynchronize(side), "side sync");
+  drain_completions();
+  finish_init();
+
+  // ---- device-timed accounting
+  op_se.clear();
+  bubble_se.clear();
+  step_se.clear();
+  BreakdownInput bi;
+  bi.num_stages = 1;
+  cudaEvent_t prev_end = run_start;  // the leading bubble starts at the epoch base
+  for (int e = 0; e < epochs; ++e) {
+    for (int i = 0; i < nops; ++i) {
+      const double a = elapsed_s(run_start, eev[e].op_start[i]);
+      const double b = elapsed_s(run_start, eev[e].op_end[i]);
+      op_se.push_back(a);
+      op_se.push_back(b);
+      if (gap_bubble[static_cast<std::size_t>(i)] >= 0) {
+        bubble_se.push_back(elapsed_s(run_start, prev_end));
+        bubble_se.push_back(a);
+      }
+      prev_end = eev[e].op_end[i];
+    }
+    if (gap_bubble[static_cast<std::size_t>(nops)] >= 0) {
+      bubble_se.push_back(elapsed_s(run_start, prev_end));
+      bubble_se.push_back(elapsed_s(run_start, eev[e].end));
+    }
+    prev_end = eev[e].end;
+  }
+  step_task.clear();
+  for (const StepRec& r : steps) {
+    step_se.push_back(elapsed_s(run_start, r.a));
+    step_se.push_back(elapsed_s(run_start, r.b));
+    step_task.push_back(r.task);
+  }
+  const double makespan = elapsed_s(run_start, eev[static_cast<std::size_t>(epochs) - 1].end);
+  double bubble_total = 0, used = 0, step_total = 0, worst = 0;
+  for (std::size_t i = 0; i < bubble_se.size(); i += 2) bubble_total += bubble_se[i + 1] - bubble_se[i];
+  std::size_t bi_idx = 0;
+  for (std::size_t i = 0; i < step_se.size(); i += 2) {
+    const double a = step_se[i], b = step_se[i + 1];
+    step_total += b - a;
+    while (bi_idx + 2 < bubble_se.size() && bubble_se[bi_idx + 1] <= a) bi_idx += 2;
+    double in = 0;
+    for (std::size_t j = bi_idx; j < bubble_se.size() && bubble_se[j] < b; j += 2)
+      in += std::max(0.0, std::min(b, bubble_se[j + 1]) - std::max(a, bubble_se[j]));
+    used += in;
+    if (bi_idx < bubble_se.size() && b > bubble_se[bi_idx + 1] && a < bubble_se[bi_idx + 1])
+      worst = std::max(worst, b - bubble_se[bi_idx + 1]);
+  }
+  // bubble_breakdown (metrics.hpp:64) over the measured timeline, ns ticks
+  auto tick_of = [](double s) { return static_cast<Tick>(std::llround(s / kTick)); };
+  for (std::size_t i = 0; i < bubble_se.size(); i += 2)
+    bi.bubbles.push_back(Bubble{0, 0, tick_of(bubble_se[i]), tick_of(bubble_se[i + 1]) - tick_of(bubble_se[i]), avail, BubbleType::C});
+  for (auto& kv : tasks) {
+    bi.profiles.push_back(kv.second->prof);
+    if (kv.second->rt.assigned_worker || kv.second->rt.state != SideTaskState::Submitted)
+      bi.assigns.push_back(AssignRecord{0, kv.first, 0});
+    if (kv.second->init_recorded && with_tasks) {
+      const double a = elapsed_s(run_start, kv.second->init_a);
+      const double b = elapsed_s(run_start, kv.second->init_b);
+      if (b > 0) bi.activities.push_back(ActivityRecord{tick_of(std::max(0.0, a)), tick_of(b), kv.first, 0, ActivityKind::Init, false});
+      kv.second->init_recorded = false;
+    }
+  }
+  for (std::size_t i = 0; i < step_se.size(); i += 2)
+    bi.activities.push_back(ActivityRecord{tick_of(step_se[i]), tick_of(step_se[i + 1]), "step", 0, ActivityKind::Step, false});
+  const std::vector<StageBreakdown> bd = bubble_breakdown(bi);
+
+  std::memset(rep, 0, sizeof(*rep));
+  rep->epochs = epochs;
+  rep->with_tasks = with_tasks;
+  rep->makespan_s = makespan;
+  rep->bubble_s = bubble_total;
+  rep->used_s = used;
+  rep->overrun_s = step_total - used;
+  rep->work_units = units;
+  rep->steps_launched = launched;
+  rep->steps_completed = completed;
+  rep->dispatch_host_us = launched ? dispatch_ns / static_cast<double>(launched) * 1e-3 : 0.0;
+  rep->max_step_overrun_s = worst;
+  rep->breakdown = fr_stage_breakdown{0, 0, bd[0].used_by_side_tasks, bd[0].runtime_overhead, bd[0].idle_oom, bd[0].idle_insufficient_time};
+  rep->pauses = pauses;
+  rep->kills = kills;
+  last_side_steps = launched;
+  last_train_ops = static_cast<std::int64_t>(epochs) * nops;
+}
+
+extern "C" {
+
+int fr_harness_create(const fr_harness_config* cfg, fr_harness** out) {
+  if (!cfg || !out) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  if (cfg->stage < 0 || cfg->stage >= cfg->num_stages)
+    return frcapi::fail(FR_ERR_VALIDATION, "stage must be in [0, num_stages)", "stage");
+  if (cfg->num_micro_batches < 1 || 2 * cfg->num_micro_batches + 1 >= static_cast<int>(kBubbleIds))
+    return frcapi::fail(FR_ERR_VALIDATION, "num_micro_batches out of range", "num_micro_batches");
+  auto h = std::make_unique<fr_harness>();
+  return frcapi::guard([&]() -> int {
+    h->cfg = *cfg;
+    ck(cudaGetDevice(&h->device), "cudaGetDevice");
+    int lo = 0, hi = 0;
+    ck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
+    ck(cudaStreamCreateWithPriority(&h->train, cudaStreamNonBlocking, hi), "train stream");
+    ck(cudaStreamCreateWithPriority(&h->side, cudaStreamNonBlocking, lo), "side stream");
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&h->ring), sizeof(RingSlot) * kRingSlots, cudaHostAllocMapped), "ring");
+    std::memset(h->ring, 0, sizeof(RingSlot) * kRingSlots);
+    ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->ring_dev), h->ring, 0), "ring dev");
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&h->stamp), 64, cudaHostAllocMapped), "stamp");
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&h->flag), 64, cudaHostAllocMapped), "flag");
+    *h->flag = 0;
+    ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->stamp_dev), h->stamp, 0), "stamp dev");
+    ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->flag_dev), h->flag, 0), "flag dev");
+    ck(cudaMalloc(&h->ctl, sizeof(TimelineCtl)), "ctl");
+    ck(cudaMemset(h->ctl, 0, sizeof(TimelineCtl)), "ctl");
+    StandInShape shape;
+    shape.layers = cfg->layers;
+    shape.hidden = cfg->hidden;
+    shape.tokens = cfg->tokens;
+    shape.ffn_mult = cfg->ffn_mult > 0 ? cfg->ffn_mult : 4;
+    h->standin = std::make_unique<StandIn>(shape);
+    h->standin->capture(h->train);
+    const int reps = std::max(1, cfg->profile_reps);
+    const Tick f = cfg->fp_ticks_override > 0 ? cfg->fp_ticks_override : h->measure_op(true, reps);
+    const Tick b = cfg->bp_ticks_override > 0 ? cfg->bp_ticks_override : h->measure_op(false, reps);
+    h->fp_tflops = h->standin->fp_flops() / (static_cast<double>(h->measure_op(true, 3)) * kTick) * 1e-12;
+    h->bp_tflops = h->standin->bp_flops() / (static_cast<double>(h->measure_op(false, 3)) * kTick) * 1e-12;
+    h->build_schedule_from(f, b);
+    h->profile_in_pipeline(cfg->profile_epochs);
+    h->workers.resize(1);
+    h->workers[0].worker_id = 0;
+    h->workers[0].gpu_mem = h->avail;
+    h->calibrate();
+    *out = h.release();
+    return FR_OK;
+  });
+}
+
+int fr_harness_destroy(fr_harness* h) {
+  delete h;
+  return FR_OK;
+}
+
+int fr_harness_get_profile(const fr_harness* h, fr_harness_profile* out) {
+  if (!h || !out) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  std::memset(out, 0, sizeof(*out));
+  out->fp_ticks = h->fp;
+  out->bp_ticks = h->bp;
+  out->epoch_span = h->span;
+  for (const Bubble& b : h->bubbles) out->stage_bubble_ticks += b.duration;
+  out->bubble_rate = h->rate;
+  out->available_memory = h->avail;
+  out->fp_tflops = h->fp_tflops;
+  out->bp_tflops = h->bp_tflops;
+  out->n_bubbles = static_cast<int32_t>(h->bubbles.size());
+  out->clock_offset_err_ns = h->clock_err;
+  return FR_OK;
+}
+
+int fr_harness_stage_bubbles(const fr_harness* h, fr_bubble* out, int32_t cap, int32_t* n) {
+  if (!h || !n) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  *n = static_cast<int32_t>(h->bubbles.size());
+  if (*n > cap) return frcapi::fail(FR_ERR_CAPACITY, "bubble buffer too small");
+  for (std::size_t i = 0; i < h->bubbles.size(); ++i) out[i] = frcapi::bubble_out(h->bubbles[i], -1, -1);
+  return FR_OK;
+}
+
+int fr_harness_submit(fr_harness* h, const char* task_id, const fr_side_task_vtable* vt,
+                      void* user, double mem, int32_t profile_steps, fr_task_profile* prof_out,
+                      int32_t* assigned) {
+  if (!h || !task_id || !vt || !vt->run_next_step || !vt->init)
+    return frcapi::fail(FR_ERR_ARGUMENT, "null argument / missing hook");
+  if (h->tasks.count(task_id)) return frcapi::fail(FR_ERR_VALIDATION, "duplicate task id", "id");
+  auto t = std::make_unique<Task>();
+  t->id = task_id;
+  t->vt = *vt;
+  t->user = user;
+  return frcapi::guard([&]() -> int {
+    t->rt.spec.id = task_id;
+    t->rt.spec.memory_demand = mem;
+    // profile_task (profiler.hpp:41): run the body standalone, time each
+    // RunNextStep on the device, est = mean, max = worst (ns ticks).
+    hook(vt->create ? vt->create(user) : FR_OK, "create");
+    hook(vt->init(user, h->side), "init");
+    const int n = std::max(1, profile_steps);
+    for (int i = 0; i < 2; ++i) hook(vt->run_next_step(user, h->side), "run_next_step");
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs;
+    for (int i = 0; i < n; ++i) {
+      cudaEvent_t a = h->ev(), b = h->ev();
+      ck(cudaEventRecord(a, h->side), "record");
+      hook(vt->run_next_step(user, h->side), "run_next_step");
+      ck(cudaEventRecord(b, h->side), "record");
+      ck(cudaEventSynchronize(b), "profile step");  // standalone: one step at a time
+      evs.push_back({a, b});
+    }
+    Tick busy = 0, longest = 0;
+    for (auto& [a, b] : evs) {
+      const Tick d = static_cast<Tick>(std::llround(elapsed_s(a, b) / kTick));
+      busy += d;
+      longest = std::max(longest, d);
+    }
+    h->pool_used = 0;
+    hook(vt->stop ? vt->stop(user) : FR_OK, "stop");  // profiling instance torn down
+    TaskProfile p;
+    p.task_id = task_id;
+    p.profiled_steps = n;
+    p.est_per_step_duration = ticks_to_seconds(busy, kTick) / n;
+    p.max_per_step_duration = ticks_to_seconds(longest, kTick);
+    p.est_memory = mem;
+    t->prof = p;
+    const SubmitOutcome o = submit_task(p, h->workers);  // Alg. 1
+    if (assigned) *assigned = o.assigned;
+    if (prof_out) frcapi::profile_out(p, prof_out);
+    if (o.assigned) {
+      apply_transition(t->rt, TransitionKind::CreateSideTask, 0);
+      hook(vt->create ? vt->create(user) : FR_OK, "create");
+      h->tasks[task_id] = std::move(t);
+    } else {
+      t->user = nullptr;  // rejected: ownership stays with the caller
+    }
+    return FR_OK;
+  });
+}
+
+int fr_harness_run(fr_harness* h, int32_t epochs, int32_t with_tasks, fr_run_report* out) {
+  if (!h || !out) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  if (epochs < 1) return frcapi::fail(FR_ERR_VALIDATION, "epochs must be >= 1", "epochs");
+  try {
+    h->run(epochs, with_tasks != 0, out);
+    return FR_OK;
+  } catch (const HookError& e) {
+    return frcapi::fail(e.code, e.what());
+  } catch (const std::exception& e) {
+    return frcapi::fail(FR_ERR_INVARIANT, e.what());
+  }
+}
+
+int fr_harness_reprofile(fr_harness* h, const char* task_id, fr_task_profile* out) {
+  if (!h || !task_id) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  auto it = h->tasks.find(task_id);
+  if (it == h->tasks.end()) return frcapi::fail(FR_ERR_NOT_FOUND, "unknown task");
+  Task& t = *it->second;
+  Tick busy = 0, longest = 0;
+  int n = 0;
+  for (std::size_t i = 0; i < h->step_task.size(); ++i) {
+    if (h->step_task[i] != &t) continue;
+    const Tick d = static_cast<Tick>(std::llround((h->step_se[2 * i + 1] - h->step_se[2 * i]) / kTick));
+    busy += d;
+    longest = std::max(longest, d);
+    ++n;
+  }
+  if (n == 0) return frcapi::fail(FR_ERR_VALIDATION, "task ran no step in the last run", "task");
+  t.prof.profiled_steps = n;
+  t.prof.est_per_step_duration = ticks_to_seconds(busy, kTick) / n;
+  t.prof.max_per_step_duration = ticks_to_seconds(longest, kTick);
+  if (out) frcapi::profile_out(t.prof, out);
+  return FR_OK;
+}
+
+int fr_harness_timeline(const fr_harness* h, int32_t which, double* se, int64_t cap, int64_t* n) {
+  if (!h || !n) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  const std::vector<double>* v = which == 0 ? &h->op_se : which == 1 ? &h->bubble_se : &h->step_se;
+  *n = static_cast<int64_t>(v->size() / 2);
+  if (*n > cap) return frcapi::fail(FR_ERR_CAPACITY, "timeline buffer too small");
+  std::copy(v->begin(), v->end(), se);
+  return FR_OK;
+}
+
+int fr_harness_launches(const fr_harness* h, int64_t* side_steps, int64_t* training_ops) {
+  if (!h) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  if (side_steps) *side_steps = h->last_side_steps;
+  if (training_ops) *training_ops = h->last_train_ops;
+  return FR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,168 @@
+// Built-in image side task: InitSideTask materialises a batch
+// of 4K frames and the watermark on the GPU (or in pinned host memory for the
+// end-to-end mode), every RunNextStep resizes + watermarks `images_per_step`
+// frames with the K5 kernel, StopSideTask releases everything.  Device memory
+// is stream-ordered (cudaMallocAsync / cudaFreeAsync) so no transition ever
+// synchronises the device -- a cudaFree inside a bubble would stall the
+// training stream's host thread.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <new>
+
+#include "capi_util.hpp"
+#include "freeride_gpu.h"
+
+namespace {
+
+struct ImageTask {
+  fr_image_task_config cfg{};
+  fr_img_plan* plan = nullptr;
+  uint8_t* src = nullptr;  // device: batch (resident) or one step (host_io)
+  uint8_t* dst = nullptr;
+  uint8_t* wm = nullptr;
+  void* wmp = nullptr;  // prepared watermark (fr_img_prepare_watermark)
+  uint8_t* h_src = nullptr;  // pinned host batch (host_io)
+  uint8_t* h_dst = nullptr;
+  int64_t cursor = 0;
+  int64_t steps = 0;
+  cudaStream_t last = nullptr;
+
+  std::size_t src_img() const { return static_cast<std::size_t>(cfg.sw) * cfg.sh * 3; }
+  std::size_t dst_img() const { return static_cast<std::size_t>(cfg.dw) * cfg.dh * 3; }
+};
+
+int cu(cudaError_t e, const char* what) {
+  return e == cudaSuccess ? FR_OK : frcapi::fail(FR_ERR_CUDA_BASE + static_cast<int>(e), std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+int release(ImageTask* t, cudaStream_t s) {
+  int rc = FR_OK;
+  for (void** p : {reinterpret_cast<void**>(&t->src), reinterpret_cast<void**>(&t->dst),
+                   reinterpret_cast<void**>(&t->wm), &t->wmp})
+    if (*p) {
+      if (rc == FR_OK) rc = cu(cudaFreeAsync(*p, s), "cudaFreeAsync");
+      *p = nullptr;
+    }
+  return rc;
+}
+
+int img_create(void* u) {
+  auto* t = static_cast<ImageTask*>(u);
+  if (!t->plan) return fr_img_plan_create(t->cfg.sw, t->cfg.sh, t->cfg.dw, t->cfg.dh, &t->plan);
+  return FR_OK;
+}
+
+int img_init(void* u, void* stream) {
+  auto* t = static_cast<ImageTask*>(u);
+  auto s = static_cast<cudaStream_t>(stream);
+  t->last = s;
+  const fr_image_task_config& c = t->cfg;
+  const std::size_t resident = c.host_io ? static_cast<std::size_t>(c.images_per_step) : static_cast<std::size_t>(c.batch);
+  int rc = cu(cudaMallocAsync(reinterpret_cast<void**>(&t->src), resident * t->src_img(), s), "src");
+  if (rc == FR_OK) rc = cu(cudaMallocAsync(reinterpret_cast<void**>(&t->dst), resident * t->dst_img(), s), "dst");
+  if (rc == FR_OK) rc = cu(cudaMallocAsync(reinterpret_cast<void**>(&t->wm), static_cast<std::size_t>(c.dw) * c.dh * 4, s), "wm");
+  int64_t pbytes = 0;
+  if (rc == FR_OK) rc = fr_img_prepared_bytes(t->plan, &pbytes);
+  if (rc == FR_OK) rc = cu(cudaMallocAsync(&t->wmp, static_cast<std::size_t>(pbytes), s), "prepared wm");
+  if (rc == FR_OK) rc = fr_img_generate_watermark(t->wm, c.dw, c.dh, c.seed ^ 0x77ull, s);
+  if (rc == FR_OK) rc = fr_img_prepare_watermark(t->plan, t->wm, t->wmp, s);
+  if (rc != FR_OK) return rc;
+  if (!c.host_io) return fr_img_generate(t->src, c.batch, c.sw, c.sh, 3, c.seed, 0, s);
+  if (!t->h_src) {  // host frames: generated once, kept across Stop/Init cycles
+    rc = cu(cudaMallocHost(reinterpret_cast<void**>(&t->h_src), static_cast<std::size_t>(c.batch) * t->src_img()), "pinned src");
+    if (rc == FR_OK) rc = cu(cudaMallocHost(reinterpret_cast<void**>(&t->h_dst), static_cast<std::size_t>(c.batch) * t->dst_img()), "pinned dst");
+    for (int i = 0; rc == FR_OK && i < c.batch; i += c.images_per_step) {
+      const int n = std::min(c.images_per_step, c.batch - i);
+      rc = fr_img_generate(t->src, n, c.sw, c.sh, 3, c.seed, i, s);
+      if (rc == FR_OK) rc = cu(cudaMemcpyAsync(t->h_src + i * t->src_img(), t->src, n * t->src_img(), cudaMemcpyDeviceToHost, s), "D2H frames");
+    }
+  }
+  return rc;
+}
+
+int img_step(void* u, void* stream) {
+  auto* t = static_cast<ImageTask*>(u);
+  auto s = static_cast<cudaStream_t>(stream);
+  t->last = s;
+  const fr_image_task_config& c = t->cfg;
+  const int64_t i0 = t->cursor;
+  const int n = c.images_per_step;
+  int rc;
+  if (c.host_io) {
+    rc = cu(cudaMemcpyAsync(t->src, t->h_src + i0 * t->src_img(), n * t->src_img(), cudaMemcpyHostToDevice, s), "H2D step");
+    if (rc == FR_OK) rc = fr_img_resize_watermark_prepared(t->plan, t->src, t->dst, t->wmp, n, s);
+    if (rc == FR_OK) rc = cu(cudaMemcpyAsync(t->h_dst + i0 * t->dst_img(), t->dst, n * t->dst_img(), cudaMemcpyDeviceToHost, s), "D2H step");
+  } else {
+    rc = fr_img_resize_watermark_prepared(t->plan, t->src + i0 * t->src_img(), t->dst + i0 * t->dst_img(), t->wmp, n, s);
+  }
+  if (rc != FR_OK) return rc;
+  t->cursor = (i0 + n) % c.batch;
+  t->steps++;
+  return FR_OK;
+}
+
+int img_stop(void* u) {
+  auto* t = static_cast<ImageTask*>(u);
+  return release(t, t->last);
+}
+
+int img_finished(void* u, int64_t done, int32_t* out) {
+  auto* t = static_cast<ImageTask*>(u);
+  *out = t->cfg.total_steps > 0 && done >= t->cfg.total_steps;
+  return FR_OK;
+}
+
+void img_destroy(void* u) {
+  auto* t = static_cast<ImageTask*>(u);
+  if (t->last) cudaStreamSynchronize(t->last);
+  release(t, t->last);
+  if (t->last) cudaStreamSynchronize(t->last);
+  if (t->h_src) cudaFreeHost(t->h_src);
+  if (t->h_dst) cudaFreeHost(t->h_dst);
+  fr_img_plan_destroy(t->plan);
+  delete t;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fr_image_task_memory(const fr_image_task_config* c, double* gib) {
+  if (!c || !gib) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  const double resident = c->host_io ? c->images_per_step : c->batch;
+  const double bytes = resident * (double(c->sw) * c->sh * 3 + double(c->dw) * c->dh * 3) + double(c->dw) * c->dh * 12;
+  *gib = bytes / (1024.0 * 1024.0 * 1024.0);
+  return FR_OK;
+}
+
+int fr_image_task_create(const fr_image_task_config* c, fr_side_task_vtable* vt, void** user) {
+  if (!c || !vt || !user) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  if (c->batch < 1 || c->images_per_step < 1 || c->batch % c->images_per_step != 0)
+    return frcapi::fail(FR_ERR_VALIDATION, "batch must be a positive multiple of images_per_step", "images_per_step");
+  auto* t = new (std::nothrow) ImageTask;
+  if (!t) return frcapi::fail(FR_ERR_INVARIANT, "out of host memory");
+  t->cfg = *c;
+  std::memset(vt, 0, sizeof(*vt));
+  vt->create = img_create;
+  vt->init = img_init;
+  vt->run_next_step = img_step;
+  vt->stop = img_stop;
+  vt->finished = img_finished;
+  vt->destroy = img_destroy;
+  vt->work_units_per_step = double(c->images_per_step) * c->dw * c->dh;  // output pixels
+  *user = t;
+  return FR_OK;
+}
+
+int fr_image_task_buffers(void* user, const uint8_t** src, uint8_t** dst, const uint8_t** wm, int64_t* steps) {
+  auto* t = static_cast<ImageTask*>(user);
+  if (!t) return frcapi::fail(FR_ERR_ARGUMENT, "null task");
+  if (src) *src = t->src;
+  if (dst) *dst = t->dst;
+  if (wm) *wm = t->wm;
+  if (steps) *steps = t->steps;
+  return FR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,79 @@
+#include <cuda_bf16.h>
+
+#include "kernels/common.cuh"
+#include "runtime/timeline.cuh"
+
+namespace freeride::rt {
+
+namespace {
+
+__device__ __forceinline__ void publish(RingSlot* ring, std::uint32_t mask, std::int64_t slot,
+                                        std::uint32_t code, std::uint64_t t) {
+  RingSlot* p = ring + (static_cast<std::uint64_t>(slot) & mask);
+  volatile RingSlot* v = p;
+  v->t_ns = t;
+  v->code = code;
+  __threadfence_system();
+  v->seq = static_cast<std::uint32_t>(slot + 1);
+  __threadfence_system();
+}
+
+// Single-thread kernel: wait for the dependency-ready time of the next op
+// (relative to the epoch base), emitting bubble start/end around the wait.
+__global__ void gap_kernel(GapArgs a) {
+  const std::uint64_t now = frk::globaltimer_ns();
+  std::uint64_t base = a.ctl->base_ns;
+  if (a.mode == 2) {  // the run's first epoch starts now
+    base = now;
+    a.ctl->base_ns = base;
+  }
+  if (a.slot_start >= 0) publish(a.ring, a.ring_mask, a.slot_start, a.code_start, now);
+  std::uint64_t target;
+  if (a.mode == 1) {
+    // synchronous epoch boundary: no earlier than base + span, never before
+    // this stage's own last op has finished (now)
+    target = base + static_cast<std::uint64_t>(a.span_ns);
+    if (target < now) target = now;
+  } else {
+    target = base + static_cast<std::uint64_t>(a.ready_ns);
+  }
+  std::uint64_t t = now;
+  while (t < target) {
+    const std::uint64_t left = target - t;
+    __nanosleep(left > 4000 ? 2000u : 64u);
+    t = frk::globaltimer_ns();
+  }
+  if (a.mode == 1) a.ctl->base_ns = target;
+  a.ctl->last_ns = t;
+  if (a.slot_end >= 0) publish(a.ring, a.ring_mask, a.slot_end, a.code_end, t);
+}
+
+__global__ void stamp_kernel(std::uint64_t* out, volatile std::uint32_t* flag, std::uint32_t val) {
+  *reinterpret_cast<volatile std::uint64_t*>(out) = frk::globaltimer_ns();
+  __threadfence_system();
+  *flag = val;
+  __threadfence_system();
+}
+
+__global__ void fill_bf16_kernel(__nv_bfloat16* p, std::size_t n, std::uint64_t seed) {
+  for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
+    const std::uint64_t h = frk::splitmix64(seed * 0x9E3779B97F4A7C15ull + i);
+    p[i] = __float2bfloat16((static_cast<float>(h >> 40) * (1.0f / 16777216.0f) - 0.5f) * 0.25f);
+  }
+}
+
+}  // namespace
+
+void launch_gap(const GapArgs& a, cudaStream_t s) { gap_kernel<<<1, 1, 0, s>>>(a); }
+
+void launch_stamp(std::uint64_t* out, volatile std::uint32_t* flag, std::uint32_t val,
+                  cudaStream_t s) {
+  stamp_kernel<<<1, 1, 0, s>>>(out, flag, val);
+}
+
+void fill_random_bf16(void* p, std::size_t n, std::uint64_t seed, cudaStream_t s) {
+  fill_bf16_kernel<<<1184, 256, 0, s>>>(static_cast<__nv_bfloat16*>(p), n, seed);
+}
+
+}  // namespace freeride::rt

@@ -84,6 +84,22 @@ class ImagePlan:
                                              _stream(stream)))
         return dst
 
+    def prepare(self, wm: torch.Tensor, stream=None) -> torch.Tensor:
+        """Prepared (premultiplied, plan-layout) copy of an RGBA watermark."""
+        n = C.c_int64()
+        check(glib().fr_img_prepared_bytes(self._h, C.byref(n)))
+        out = torch.empty(n.value, dtype=torch.uint8, device=wm.device)
+        check(glib().fr_img_prepare_watermark(self._h, _ptr(wm), _ptr(out), _stream(stream)))
+        return out
+
+    def run_prepared(self, src: torch.Tensor, dst: torch.Tensor, prepared: torch.Tensor, stream=None):
+        n = src.shape[0]
+        if tuple(src.shape[1:]) != (self.sh, self.sw, 3) or tuple(dst.shape) != (n, self.dh, self.dw, 3):
+            raise ValueError("image shapes do not match the plan")
+        check(glib().fr_img_resize_watermark_prepared(self._h, _ptr(src), _ptr(dst), _ptr(prepared), n,
+                                                      _stream(stream)))
+        return dst
+
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value and _glib is not None:
@@ -95,6 +111,106 @@ def img_generate(n, w, h, channels=3, seed=1, first_index=0, device="cuda", stre
     out = torch.empty((n, h, w, channels), dtype=torch.uint8, device=device)
     check(glib().fr_img_generate(_ptr(out), n, w, h, channels, seed, first_index, _stream(stream)))
     return out
+
+
+class ImageTask:
+    """Built-in image side task (fr_image_task_create) -- a vtable + handle
+    whose ownership passes to the Harness on submit."""
+
+    def __init__(self, sw=3840, sh=2160, dw=1920, dh=1080, batch=64, images_per_step=8,
+                 host_io=False, seed=1, total_steps=0):
+        self.cfg = A.ImageTaskConfigC(sw=sw, sh=sh, dw=dw, dh=dh, batch=batch,
+                                      images_per_step=images_per_step, host_io=int(host_io),
+                                      seed=seed, total_steps=total_steps)
+        self.vt = A.SideTaskVTableC()
+        self.user = C.c_void_p()
+        check(glib().fr_image_task_create(C.byref(self.cfg), C.byref(self.vt), C.byref(self.user)))
+        gib = C.c_double()
+        check(glib().fr_image_task_memory(C.byref(self.cfg), C.byref(gib)))
+        self.memory_gib = gib.value
+        self.units_per_step = self.vt.work_units_per_step
+        # per-step algorithmic HBM bytes (src + dst per image; the watermark
+        # is read once per step and stays L2-resident across its images)
+        self.bytes_per_step = images_per_step * (sw * sh * 3 + dw * dh * 3) + dw * dh * 8
+        self.h2d_per_step = images_per_step * sw * sh * 3 if host_io else 0
+        self.d2h_per_step = images_per_step * dw * dh * 3 if host_io else 0
+
+
+class Harness:
+    """fr_harness: one GPU replaying stage `stage` of a p-stage 1F1B pipeline
+    of bf16 GEMM stand-ins, with a side-task worker harvesting its bubbles."""
+
+    def __init__(self, num_stages=4, num_micro_batches=4, stage=0, layers=6, hidden=2048,
+                 tokens=8192, ffn_mult=4, profile_reps=5, max_inflight_steps=2, gate_estimate=0,
+                 gpu_memory_total=178.0, weight_mem=-1.0, activation_mem=-1.0,
+                 fp_ticks=0, bp_ticks=0, profile_epochs=3):
+        self.cfg = A.HarnessConfigC(
+            num_stages=num_stages, num_micro_batches=num_micro_batches, stage=stage, layers=layers,
+            hidden=hidden, tokens=tokens, ffn_mult=ffn_mult, profile_reps=profile_reps,
+            max_inflight_steps=max_inflight_steps, gate_estimate=gate_estimate,
+            gpu_memory_total=gpu_memory_total, weight_mem=weight_mem,
+            activation_mem=activation_mem, fp_ticks_override=fp_ticks, bp_ticks_override=bp_ticks,
+            profile_epochs=profile_epochs)
+        h = C.c_void_p()
+        check(glib().fr_harness_create(C.byref(self.cfg), C.byref(h)))
+        self._h = h
+        self._tasks = []
+
+    def profile(self) -> dict:
+        p = A.HarnessProfileC()
+        check(glib().fr_harness_get_profile(self._h, C.byref(p)))
+        return p.as_dict()
+
+    def stage_bubbles(self):
+        out = (A.BubbleC * 1024)()
+        n = C.c_int32()
+        check(glib().fr_harness_stage_bubbles(self._h, out, 1024, C.byref(n)))
+        return [out[i].as_dict() for i in range(n.value)]
+
+    def submit(self, task_id: str, task, profile_steps=32):
+        prof = A.TaskProfileC()
+        assigned = C.c_int32()
+        check(glib().fr_harness_submit(self._h, task_id.encode(), C.byref(task.vt), task.user,
+                                       task.memory_gib, profile_steps, C.byref(prof),
+                                       C.byref(assigned)))
+        self._tasks.append(task)  # keep the ctypes vtable alive
+        return bool(assigned.value), prof.as_dict()
+
+    def reprofile(self, task_id: str) -> dict:
+        """Re-estimate a task's per-step duration from its steps in the last run."""
+        prof = A.TaskProfileC()
+        check(glib().fr_harness_reprofile(self._h, task_id.encode(), C.byref(prof)))
+        return prof.as_dict()
+
+    def run(self, epochs: int, with_tasks: bool = True) -> dict:
+        r = A.RunReportC()
+        check(glib().fr_harness_run(self._h, epochs, int(with_tasks), C.byref(r)))
+        d = r.as_dict()
+        d["breakdown"] = r.breakdown.as_dict()
+        return d
+
+    def timeline(self, which: int):
+        n = C.c_int64()
+        cap = 1 << 20
+        buf = (C.c_double * (2 * cap))()
+        check(glib().fr_harness_timeline(self._h, which, buf, cap, C.byref(n)))
+        return [(buf[2 * i], buf[2 * i + 1]) for i in range(n.value)]
+
+    def launches(self):
+        a, b = C.c_int64(), C.c_int64()
+        check(glib().fr_harness_launches(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            glib().fr_harness_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
 
 
 def img_generate_watermark(w, h, seed=7, device="cuda", stream=None):

@@ -1,0 +1,67 @@
+"""The GPU bubble-harvesting runtime: a 4-stage 1F1B stage replay with the
+image side task, checked for the north-star properties on a small stand-in."""
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def g():
+    from paper_2409_06941_b200 import gpu
+    gpu.glib()
+    return gpu
+
+
+def small_harness(g, stage, **kw):
+    return g.Harness(num_stages=4, num_micro_batches=4, stage=stage, layers=2, hidden=2048,
+                     tokens=8192, profile_reps=3, profile_epochs=2, **kw)
+
+
+@pytest.mark.parametrize("stage", [0, 3])
+def test_profile_matches_reference_schedule(g, product, stage):
+    h = small_harness(g, stage)
+    p = h.profile()
+    assert abs(p["bubble_rate"] - 3 / 7) < 1e-12          # (p-1)/(m+p-1), any fp/bp
+    from paper_2409_06941_b200.bubblesim import PipelineConfig
+    cfg = PipelineConfig(4, 4, [p["fp_ticks"]], [p["bp_ticks"]], 1, 178.0, [1.0] * 4, 1e-9)
+    tr = product.build_schedule(cfg)
+    want = [b for b in product.extract_bubbles(tr) if b.stage == stage]
+    got = h.stage_bubbles()
+    assert len(got) == len(want) == p["n_bubbles"]
+    assert p["epoch_span"] == tr.epoch_spans[0][1] - tr.epoch_spans[0][0]
+    h.close()
+
+
+def test_harvest_fills_bubbles_without_slowing_training(g):
+    h = small_harness(g, stage=1)
+    ok, prof = h.submit("image", g.ImageTask(batch=16, images_per_step=2), profile_steps=16)
+    assert ok and prof["est_per_step_duration"] > 0
+    warm = h.run(2, True)                      # InitSideTask lands in the first bubble
+    assert warm["steps_completed"] > 0
+    h.reprofile("image")
+    base = h.run(4, False)
+    r = h.run(4, True)
+    assert r["steps_completed"] == r["steps_launched"] > 0
+    assert r["used_s"] / r["bubble_s"] > 0.6
+    assert r["overrun_s"] < 0.05 * r["used_s"]
+    dt = (r["makespan_s"] - base["makespan_s"]) / base["makespan_s"]
+    assert dt < 0.01                           # north star: ΔT <= 1 %
+    bd = r["breakdown"]
+    total = bd["used_by_side_tasks"] + bd["runtime_overhead"] + bd["idle_oom"] + bd["idle_insufficient_time"]
+    bubbles_ns = sum(round(b * 1e9) - round(a * 1e9) for a, b in h.timeline(1))
+    assert abs(total - bubbles_ns) <= len(h.timeline(1)) + 1   # conservation (metrics.hpp:51-62)
+    assert r["kills"] == 0
+    side, train = h.launches()
+    assert side == r["steps_launched"] and train == 4 * 8
+    h.close()
+
+
+def test_rejected_when_memory_does_not_fit(g):
+    h = g.Harness(num_stages=4, num_micro_batches=4, stage=0, layers=1, profile_reps=2,
+                  profile_epochs=1, gpu_memory_total=178.0, weight_mem=170.0, activation_mem=1.0)
+    # stage 0 keeps 170 + 4*1 GiB: 4 GiB left, a 64-frame batch needs ~2.2 GiB -> fits;
+    # an 256-frame batch (~8.7 GiB) must be rejected by Alg. 1 (strict filter)
+    ok_small, _ = h.submit("small", g.ImageTask(batch=64, images_per_step=8), profile_steps=4)
+    ok_big, _ = h.submit("big", g.ImageTask(batch=256, images_per_step=8), profile_steps=4)
+    assert ok_small and not ok_big
+    h.close()

@@ -36,6 +36,26 @@ def test_tma_2x_4k_bit_exact(g, sidetask_oracle, n):
     assert np.array_equal(dst.cpu().numpy(), want)
 
 
+def test_prepared_watermark_path_bit_exact(g, sidetask_oracle):
+    """The task's path: watermark prepared once, per-step kernel on the prepared form."""
+    plan = g.ImagePlan(3840, 2160, 1920, 1080)
+    src = g.img_generate(3, 3840, 2160, seed=21)
+    wm = g.img_generate_watermark(1920, 1080, seed=22)
+    prepared = plan.prepare(wm)
+    assert prepared.numel() == 1920 * 1080 * 8
+    dst = torch.empty((3, 1080, 1920, 3), dtype=torch.uint8, device="cuda")
+    plan.run_prepared(src, dst, prepared)
+    want = sidetask_oracle.img_resize_watermark(src.cpu().numpy(), wm.cpu().numpy(), 1920, 1080)
+    assert np.array_equal(dst.cpu().numpy(), want)
+    # extreme alphas: fully opaque / fully transparent watermark
+    for a in (0, 255):
+        wm2 = wm.clone()
+        wm2[..., 3] = a
+        plan.run_prepared(src[:1], dst[:1], plan.prepare(wm2))
+        want = sidetask_oracle.img_resize_watermark(src[:1].cpu().numpy(), wm2.cpu().numpy(), 1920, 1080)
+        assert np.array_equal(dst[:1].cpu().numpy(), want)
+
+
 @pytest.mark.parametrize("sw,sh,dw,dh", [(32, 2, 16, 1), (64, 30, 32, 15), (1024, 6, 512, 3)])
 def test_tma_2x_small_shapes(g, sidetask_oracle, sw, sh, dw, dh):
     plan = g.ImagePlan(sw, sh, dw, dh)
