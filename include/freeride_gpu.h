@@ -165,6 +165,9 @@ int fr_harness_stage_bubbles(const fr_harness* h, fr_bubble* out, int32_t cap, i
 int fr_harness_submit(fr_harness* h, const char* task_id, const fr_side_task_vtable* vt,
                       void* user, double memory_demand_gib, int32_t profile_steps,
                       fr_task_profile* profile, int32_t* assigned);
+/* StopSideTask (task.hpp:21) between runs: releases the task's GPU state and
+ * clears the worker's CurrentTask / queue entry (SURVEY.md Appendix B rule 8) */
+int fr_harness_stop_task(fr_harness* h, const char* task_id);
 /* profile_task from the task's steps in the last run (measured in bubbles,
  * under training load): est = mean, max = worst, as in profiler.cpp:50-78 */
 int fr_harness_reprofile(fr_harness* h, const char* task_id, fr_task_profile* out);

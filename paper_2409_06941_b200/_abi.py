@@ -466,6 +466,7 @@ GPU_PROTOTYPES.update({
     "fr_harness_submit": (C.c_int, [vp, cp, P(SideTaskVTableC), vp, dbl, i32, P(TaskProfileC), P(i32)]),
     "fr_harness_run": (C.c_int, [vp, i32, i32, P(RunReportC)]),
     "fr_harness_reprofile": (C.c_int, [vp, cp, P(TaskProfileC)]),
+    "fr_harness_stop_task": (C.c_int, [vp, cp]),
     "fr_harness_timeline": (C.c_int, [vp, i32, P(dbl), i64, P(i64)]),
     "fr_harness_launches": (C.c_int, [vp, P(i64), P(i64)]),
 })

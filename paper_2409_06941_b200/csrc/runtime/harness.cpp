@@ -461,6 +461,38 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
     }
   };
 
+  // Alg. 2 lines 8-17 on a BubbleStarted signal at device time t_dev.
+  bool deferred_start = false;
+  std::int64_t deferred_t = 0;
+  std::uint32_t deferred_id = 0;
+  auto start_bubble = [&](std::int64_t t_dev, std::uint32_t id) {
+    const Bubble& pb = bubbles[id % kBubbleIds];
+    Bubble b = pb;
+    b.epoch = static_cast<int>(id / kBubbleIds);
+    b.start = t_dev;
+    for (const ManagerAction& act : on_bubble_started(ws, b, view)) {
+      Task& t = task_of(act.task_id);
+      if (act.kind == ManagerActionKind::IssueInit) {
+        if (!t.init_a) {
+          ck(cudaEventCreate(&t.init_a), "init event");
+          ck(cudaEventCreate(&t.init_b), "init event");
+        }
+        ck(cudaEventRecord(t.init_a, side), "record");
+        hook(t.vt.init(t.user, side), "init");
+        ck(cudaEventRecord(t.init_b, side), "record");
+        t.initializing = true;
+        t.init_recorded = true;
+      } else if (act.kind == ManagerActionKind::IssueStart) {
+        apply_transition(t.rt, TransitionKind::StartSideTask, t_dev);
+        hook(t.vt.start ? t.vt.start(t.user) : FR_OK, "start");
+        running = &t;
+        bubble_end_dev = t_dev + pb.duration;  // StartSideTask carries the bubble end
+        proj_end_dev = 0;
+        gate_closed = false;
+      }
+    }
+  };
+
   while (true) {
     if (train_failed) {
       trainer.join();
@@ -475,32 +507,18 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
       ++next_slot;
       clock_off = std::max(clock_off, t_dev - seen);  // causality tightens the bound
       const std::uint32_t kind = code >> 28, id = code & 0x0FFFFFFFu;
-      const Bubble& pb = bubbles[id % kBubbleIds];
-      if (with_tasks && kind == kEvBubbleStart) {
-        Bubble b = pb;
-        b.epoch = static_cast<int>(id / kBubbleIds);
-        b.start = t_dev;
-        for (const ManagerAction& act : on_bubble_started(ws, b, view)) {
-          Task& t = task_of(act.task_id);
-          if (act.kind == ManagerActionKind::IssueInit) {
-            if (!t.init_a) {
-              ck(cudaEventCreate(&t.init_a), "init event");
-              ck(cudaEventCreate(&t.init_b), "init event");
-            }
-            ck(cudaEventRecord(t.init_a, side), "record");
-            hook(t.vt.init(t.user, side), "init");
-            ck(cudaEventRecord(t.init_b, side), "record");
-            t.initializing = true;
-            t.init_recorded = true;
-          } else if (act.kind == ManagerActionKind::IssueStart) {
-            apply_transition(t.rt, TransitionKind::StartSideTask, t_dev);
-            hook(t.vt.start ? t.vt.start(t.user) : FR_OK, "start");
-            running = &t;
-            bubble_end_dev = t_dev + pb.duration;
-            proj_end_dev = 0;
-            gate_closed = false;
-          }
-        }
+      if (with_tasks && kind == kEvBubbleStart && pause_pending) {
+        // The previous bubble's pause is still draining (a step in flight):
+        // hold this BubbleStarted until the pause lands, so Alg. 2 sees the
+        // task PAUSED exactly as it would had the pause been instantaneous.
+        deferred_start = true;
+        deferred_t = t_dev;
+        deferred_id = id;
+      } else if (with_tasks && kind == kEvBubbleStart) {
+        start_bubble(t_dev, id);
+      } else if (with_tasks && kind == kEvBubbleEnd && deferred_start) {
+        deferred_start = false;  // the held bubble ended before the pause landed
+        on_bubble_ended(ws, t_dev, view);
       } else if (with_tasks && kind == kEvBubbleEnd) {
         for (const ManagerAction& act : on_bubble_ended(ws, t_dev, view)) {
           if (act.kind == ManagerActionKind::IssuePause) {
@@ -510,6 +528,10 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
           }
         }
       }
+    }
+    if (with_tasks && deferred_start && !pause_pending) {
+      deferred_start = false;
+      start_bubble(deferred_t, deferred_id);
     }
     if (!with_tasks && next_slot >= n_events) break;
     // 2. step completions, init completion, pause drains
@@ -791,6 +813,24 @@ int fr_harness_run(fr_harness* h, int32_t epochs, int32_t with_tasks, fr_run_rep
   } catch (const std::exception& e) {
     return frcapi::fail(FR_ERR_INVARIANT, e.what());
   }
+}
+
+int fr_harness_stop_task(fr_harness* h, const char* task_id) {
+  if (!h || !task_id) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  auto it = h->tasks.find(task_id);
+  if (it == h->tasks.end()) return frcapi::fail(FR_ERR_NOT_FOUND, "unknown task");
+  Task& t = *it->second;
+  return frcapi::guard([&]() -> int {
+    if (t.rt.state != SideTaskState::Stopped) {
+      apply_transition(t.rt, TransitionKind::StopSideTask, 0);  // {CREATED,PAUSED,RUNNING} -> STOPPED
+      if (t.rt.memory_allocated == 0.0 && t.vt.stop) hook(t.vt.stop(t.user), "stop");
+    }
+    WorkerState& ws = h->workers[0];
+    if (ws.current_task && *ws.current_task == t.id) ws.current_task.reset();  // Appendix B rule 8
+    ws.task_queue.erase(std::remove(ws.task_queue.begin(), ws.task_queue.end(), t.id), ws.task_queue.end());
+    ck(cudaStreamSynchronize(h->side), "side sync");
+    return FR_OK;
+  });
 }
 
 int fr_harness_reprofile(fr_harness* h, const char* task_id, fr_task_profile* out) {

@@ -182,6 +182,9 @@ class Harness:
         check(glib().fr_harness_reprofile(self._h, task_id.encode(), C.byref(prof)))
         return prof.as_dict()
 
+    def stop_task(self, task_id: str):
+        check(glib().fr_harness_stop_task(self._h, task_id.encode()))
+
     def run(self, epochs: int, with_tasks: bool = True) -> dict:
         r = A.RunReportC()
         check(glib().fr_harness_run(self._h, epochs, int(with_tasks), C.byref(r)))
