@@ -44,6 +44,7 @@ SHAPE = dict(layers=6, hidden=2048, tokens=8192, ffn_mult=4)
 FRAMES = dict(sw=3840, sh=2160, dw=1920, dh=1080)
 BATCH = 64
 IMAGES_PER_STEP = 8
+E2E_IMAGES_PER_STEP = 1
 OUT_PX = FRAMES["dw"] * FRAMES["dh"]
 SRC_BYTES = FRAMES["sw"] * FRAMES["sh"] * 3
 DST_BYTES = OUT_PX * 3
@@ -151,12 +152,15 @@ def cpu_image_throughput(seconds: float, images: int = IMAGES_PER_STEP):
 def run_stage(gpu, stage, K, W, host_io):
     h = gpu.Harness(num_stages=STAGES, num_micro_batches=MICRO_BATCHES, stage=stage, **SHAPE)
     prof = h.profile()
-    task = gpu.ImageTask(batch=BATCH, images_per_step=IMAGES_PER_STEP, host_io=host_io, **FRAMES)
+    # host-buffer steps are PCIe-bound (25 MB H2D per frame): one frame per
+    # step keeps a step well inside the ~3 ms type-C bubbles
+    ips = E2E_IMAGES_PER_STEP if host_io else IMAGES_PER_STEP
+    task = gpu.ImageTask(batch=BATCH, images_per_step=ips, host_io=host_io, **FRAMES)
     ok, tprof = h.submit("image", task, profile_steps=32)
     if not ok:
         raise RuntimeError(f"stage {stage}: image task rejected by Alg. 1")
     h.run(max(W, 1), True)
-    h.reprofile("image")
+    h.reprofile("image")       # per-step duration measured in bubbles, under load
     base = h.run(K, False)
     r = h.run(K, True)
     steps = h.timeline(2)

@@ -27,6 +27,8 @@ int fr_stream_create(int32_t priority_class /* 0 = lowest, 1 = highest */, void*
 int fr_stream_destroy(void* stream);
 int fr_stream_synchronize(void* stream);
 int fr_device_sm_count(int32_t* sms);
+/* diagnostics: spin `cycles` SM clocks on one warp, write {cycles, ns} */
+int fr_clock_probe(uint64_t* out_cycles_ns, int64_t cycles, void* stream);
 
 /* ------------------------------------------- K5: image resize + watermark */
 /* Plan for one (src WxH -> dst WxH) shape.  Coefficients follow cv2's
@@ -165,6 +167,9 @@ int fr_harness_stage_bubbles(const fr_harness* h, fr_bubble* out, int32_t cap, i
 int fr_harness_submit(fr_harness* h, const char* task_id, const fr_side_task_vtable* vt,
                       void* user, double memory_demand_gib, int32_t profile_steps,
                       fr_task_profile* profile, int32_t* assigned);
+/* bubble profiler (profile_bubbles, profiler.hpp:45) from the last run's
+ * measured bubbles: each of this stage's bubble durations := its median */
+int fr_harness_reprofile_bubbles(fr_harness* h);
 /* StopSideTask (task.hpp:21) between runs: releases the task's GPU state and
  * clears the worker's CurrentTask / queue entry (SURVEY.md Appendix B rule 8) */
 int fr_harness_stop_task(fr_harness* h, const char* task_id);

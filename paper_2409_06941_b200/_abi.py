@@ -392,6 +392,7 @@ GPU_PROTOTYPES = {
     "fr_stream_destroy": (C.c_int, [vp]),
     "fr_stream_synchronize": (C.c_int, [vp]),
     "fr_device_sm_count": (C.c_int, [P(i32)]),
+    "fr_clock_probe": (C.c_int, [vp, i64, vp]),
     "fr_img_plan_create": (C.c_int, [i32, i32, i32, i32, P(vp)]),
     "fr_img_plan_destroy": (C.c_int, [vp]),
     "fr_img_plan_path": (C.c_int, [vp, P(i32)]),
@@ -467,6 +468,7 @@ GPU_PROTOTYPES.update({
     "fr_harness_run": (C.c_int, [vp, i32, i32, P(RunReportC)]),
     "fr_harness_reprofile": (C.c_int, [vp, cp, P(TaskProfileC)]),
     "fr_harness_stop_task": (C.c_int, [vp, cp]),
+    "fr_harness_reprofile_bubbles": (C.c_int, [vp]),
     "fr_harness_timeline": (C.c_int, [vp, i32, P(dbl), i64, P(i64)]),
     "fr_harness_launches": (C.c_int, [vp, P(i64), P(i64)]),
 })

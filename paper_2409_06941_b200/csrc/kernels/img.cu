@@ -65,11 +65,19 @@ __global__ void img_prepare_wm_kernel(const uint8_t* __restrict__ wm, uint4* __r
   }
 }
 
+// Rows are handed out dynamically (one atomicAdd per row by the elected
+// thread) rather than statically strided: in a pipeline bubble some SMs may
+// be unavailable (the stage's dependency-wait kernel, an NCCL receive, the
+// tail of the previous GEMM), and with a static split the CTAs that could
+// not become resident would run their whole share as a serial tail.  The
+// last CTA to exit re-arms the counters for the next launch on the stream.
 template <int S>
 __global__ void __launch_bounds__(kImgThreads, kImgCtasPerSm)
     img_resize2x_wm_tma(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
-                        const uint4* __restrict__ wmp, int dw, int dh, uint32_t rows) {
+                        const uint4* __restrict__ wmp, int dw, int dh, uint32_t rows,
+                        uint32_t* __restrict__ counters) {
   extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint32_t row_of[S], y_of[S];
   const uint32_t src_row = 6u * static_cast<uint32_t>(dw);  // one source row, RGB
   const uint32_t out_row = 3u * static_cast<uint32_t>(dw);
   const uint32_t a_src = (2u * src_row + 127u) & ~127u;
@@ -78,9 +86,6 @@ __global__ void __launch_bounds__(kImgThreads, kImgCtasPerSm)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
 
   const int tid = threadIdx.x;
-  const uint32_t G = gridDim.x;
-  const uint32_t first = blockIdx.x;
-  const uint32_t nk = first < rows ? (rows - first + G - 1) / G : 0;
   const int groups = dw >> 3;
 
   if (tid == 0) {
@@ -88,26 +93,33 @@ __global__ void __launch_bounds__(kImgThreads, kImgCtasPerSm)
     for (int s = 0; s < S; ++s) frk::mbar_init(&full[s], 1);
     frk::fence_mbar_init();
   }
-  __syncthreads();
 
   uint64_t pol_stream = 0;
   if (tid == 0) pol_stream = frk::policy_evict_first();
-  auto issue = [&](uint32_t k) {
-    const int s = static_cast<int>(k % S);
-    const uint32_t r = first + k * G;
+  // Elected thread: grab the next row for stage s and start its TMA load.
+  auto grab = [&](int s, uint32_t r) {
+    row_of[s] = r;
+    if (r >= rows) return;
     const uint32_t img = r / static_cast<uint32_t>(dh);
     const uint32_t y = r - img * static_cast<uint32_t>(dh);
+    y_of[s] = y;
     frk::mbar_arrive_expect_tx(&full[s], 2u * src_row);
     frk::bulk_g2s(smem + s * stage_bytes,
                   src + (static_cast<uint64_t>(img) * 2 * dh + 2 * y) * src_row, 2u * src_row,
                   &full[s], pol_stream);
   };
   if (tid == 0)
-    for (uint32_t k = 0; k < nk && k < S; ++k) issue(k);
+    for (int s = 0; s < S; ++s) grab(s, atomicAdd(&counters[0], 1u));
+  __syncthreads();
 
-  uint32_t y = first % static_cast<uint32_t>(dh);  // output row of iteration k
-  for (uint32_t k = 0; k < nk; ++k) {
+  for (uint32_t k = 0;; ++k) {
     const int s = static_cast<int>(k % S);
+    const uint32_t row = row_of[s];  // written >= S-1 barriers ago (or before the first)
+    if (row >= rows) break;          // rows are grabbed in increasing order: all done
+    const uint32_t y = y_of[s];
+    // the elected thread's next row: the atomic's round trip overlaps this
+    // row's compute instead of delaying the refill after the barrier
+    const uint32_t next_row = tid == 0 ? atomicAdd(&counters[0], 1u) : 0u;
     uint8_t* st = smem + s * stage_bytes;
     const uint8_t* ra = st;
     const uint8_t* rb = st + src_row;
@@ -173,14 +185,19 @@ __global__ void __launch_bounds__(kImgThreads, kImgCtasPerSm)
     if (tid == 0 && k + 1 >= S) frk::bulk_wait_read<S - 2>();
     __syncthreads();
     if (tid == 0) {
-      frk::bulk_s2g(dst + static_cast<uint64_t>(first + k * G) * out_row, orow, out_row, pol_stream);
+      frk::bulk_s2g(dst + static_cast<uint64_t>(row) * out_row, orow, out_row, pol_stream);
       frk::bulk_commit();
-      if (k + S < nk) issue(k + S);
+      grab(s, next_row);
     }
-    y += G;
-    while (y >= static_cast<uint32_t>(dh)) y -= static_cast<uint32_t>(dh);
   }
-  if (tid == 0) frk::bulk_wait<0>();
+  if (tid == 0) {
+    frk::bulk_wait<0>();
+    __threadfence();
+    if (atomicAdd(&counters[1], 1u) == gridDim.x - 1) {  // last CTA out re-arms
+      counters[0] = 0;
+      counters[1] = 0;
+    }
+  }
 }
 
 // General shapes: one thread per output pixel, coefficient tables from the
@@ -280,6 +297,7 @@ struct fr_img_plan {
   int path = FR_IMG_PATH_GENERAL;
   int32_t* d_tab = nullptr;
   void* d_wm = nullptr;  // plan-owned prepared watermark for fr_img_resize_watermark
+  uint32_t* d_ctr = nullptr;  // dynamic row scheduler {next row, CTAs done}; one stream at a time
   int smem = 0;
   int sms = 0;
   size_t prepared_bytes() const {
@@ -314,6 +332,10 @@ int fr_img_plan_create(int32_t sw, int32_t sh, int32_t dw, int32_t dh, fr_img_pl
     if (plan->smem <= optin) {
       e = cudaFuncSetAttribute(img_resize2x_wm_tma<kImgStages>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, plan->smem);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(img_resize2x_wm_tma<kImgStages>,
+                                 cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 cudaSharedmemCarveoutMaxShared);
       if (e != cudaSuccess) {
         delete plan;
         return frcapi::cuda_status(e, "cudaFuncSetAttribute(img_resize2x_wm_tma)");
@@ -330,8 +352,12 @@ int fr_img_plan_create(int32_t sw, int32_t sh, int32_t dw, int32_t dh, fr_img_pl
       e = cudaMemcpy(plan->d_tab, tab.data(), tab.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
   }
   if (e == cudaSuccess) e = cudaMalloc(&plan->d_wm, plan->prepared_bytes());
+  if (e == cudaSuccess) e = cudaMalloc(&plan->d_ctr, 2 * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMemset(plan->d_ctr, 0, 2 * sizeof(uint32_t));
   if (e != cudaSuccess) {
     if (plan->d_tab) cudaFree(plan->d_tab);
+    if (plan->d_wm) cudaFree(plan->d_wm);
+    if (plan->d_ctr) cudaFree(plan->d_ctr);
     delete plan;
     return frcapi::cuda_status(e, "image plan setup");
   }
@@ -343,6 +369,7 @@ int fr_img_plan_destroy(fr_img_plan* plan) {
   if (!plan) return FR_OK;
   if (plan->d_tab) cudaFree(plan->d_tab);
   if (plan->d_wm) cudaFree(plan->d_wm);
+  if (plan->d_ctr) cudaFree(plan->d_ctr);
   delete plan;
   return FR_OK;
 }
@@ -388,7 +415,8 @@ int fr_img_resize_watermark_prepared(const fr_img_plan* plan, const uint8_t* src
     if (rows >= (int64_t{1} << 31)) return frcapi::fail(FR_ERR_UNSUPPORTED, "too many rows in one step");
     const int grid = static_cast<int>(std::min<int64_t>(rows, int64_t(plan->sms) * kImgCtasPerSm));
     img_resize2x_wm_tma<kImgStages><<<grid, kImgThreads, plan->smem, s>>>(
-        src, dst, static_cast<const uint4*>(prepared), plan->dw, plan->dh, static_cast<uint32_t>(rows));
+        src, dst, static_cast<const uint4*>(prepared), plan->dw, plan->dh, static_cast<uint32_t>(rows),
+        plan->d_ctr);
   } else {
     const int64_t total = static_cast<int64_t>(n) * plan->dw * plan->dh;
     img_resize_wm_general<<<grid_for(total, 256, 8), 256, 0, s>>>(

@@ -2,7 +2,32 @@
 #include "freeride_gpu.h"
 #include "kernels/common.cuh"
 
+namespace {
+
+// One warp spins for `cycles` SM clocks and records (clock64 delta,
+// globaltimer delta): the SM frequency the GPU is running at right now.
+__global__ void clock_probe_kernel(unsigned long long* out, long long cycles) {
+  if (threadIdx.x != 0) return;
+  const long long c0 = clock64();
+  const unsigned long long t0 = frk::globaltimer_ns();
+  long long c = c0;
+  while (c - c0 < cycles) c = clock64();
+  const unsigned long long t1 = frk::globaltimer_ns();
+  out[0] = static_cast<unsigned long long>(c - c0);
+  out[1] = t1 - t0;
+}
+
+}  // namespace
+
 extern "C" {
+
+int fr_clock_probe(uint64_t* out_cycles_ns, int64_t cycles, void* stream) {
+  if (!out_cycles_ns || cycles < 1) return frcapi::fail(FR_ERR_ARGUMENT, "bad probe args");
+  clock_probe_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<unsigned long long*>(out_cycles_ns), cycles);
+  FR_CUDA_LAUNCHED("clock_probe");
+  return FR_OK;
+}
 
 int fr_stream_create(int32_t priority_class, void** stream) {
   if (!stream) return frcapi::fail(FR_ERR_ARGUMENT, "null stream out");

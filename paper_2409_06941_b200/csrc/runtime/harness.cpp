@@ -267,16 +267,27 @@ struct fr_harness {
       build_schedule_from(f, b);
     }
     run(epochs, false, &rep);
+    bubbles_from_last_run();
+  }
+
+  // Each profiled bubble duration := its median over the last run's epochs
+  // (used after a warm-up run *with* side tasks too: ops run slightly slower
+  // when bubbles are busy, so the bubbles the worker will see are shorter).
+  int bubbles_from_last_run() {
     const std::size_t nb = bubbles.size();
-    if (nb == 0 || bubble_se.size() / 2 != nb * static_cast<std::size_t>(epochs)) return;
+    if (nb == 0) return 0;
+    const std::size_t epochs = bubble_se.size() / 2 / nb;
+    if (epochs == 0 || bubble_se.size() / 2 != nb * epochs) return 0;
     for (std::size_t j = 0; j < nb; ++j) {
       std::vector<double> d;
-      for (int e = 0; e < epochs; ++e) {
-        const std::size_t k = static_cast<std::size_t>(e) * nb + j;
+      for (std::size_t e = 0; e < epochs; ++e) {
+        const std::size_t k = e * nb + j;
         d.push_back(bubble_se[2 * k + 1] - bubble_se[2 * k]);
       }
-      bubbles[j].duration = static_cast<Tick>(std::llround(median(d) / kTick));
+      std::sort(d.begin(), d.end());
+      bubbles[j].duration = static_cast<Tick>(std::llround(d[d.size() / 2] / kTick));
     }
+    return static_cast<int>(epochs);
   }
 
   // GateEstimate (config.hpp:17,24): profiled mean by default, max if asked.
@@ -679,6 +690,7 @@ int fr_harness_create(const fr_harness_config* cfg, fr_harness** out) {
   return frcapi::guard([&]() -> int {
     h->cfg = *cfg;
     ck(cudaGetDevice(&h->device), "cudaGetDevice");
+    configure_timeline_kernels();
     int lo = 0, hi = 0;
     ck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
     ck(cudaStreamCreateWithPriority(&h->train, cudaStreamNonBlocking, hi), "train stream");
@@ -813,6 +825,13 @@ int fr_harness_run(fr_harness* h, int32_t epochs, int32_t with_tasks, fr_run_rep
   } catch (const std::exception& e) {
     return frcapi::fail(FR_ERR_INVARIANT, e.what());
   }
+}
+
+int fr_harness_reprofile_bubbles(fr_harness* h) {
+  if (!h) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  if (h->bubbles_from_last_run() == 0)
+    return frcapi::fail(FR_ERR_VALIDATION, "no complete run to profile bubbles from", "run");
+  return FR_OK;
 }
 
 int fr_harness_stop_task(fr_harness* h, const char* task_id) {

@@ -65,6 +65,21 @@ __global__ void fill_bf16_kernel(__nv_bfloat16* p, std::size_t n, std::uint64_t 
 
 }  // namespace
 
+// The gap kernel stays resident on one SM for the whole bubble.  An SM's
+// L1/shared carveout is fixed while a CTA is resident, so a tiny kernel that
+// lands with the default (L1-heavy) carveout would lock the side task's
+// smem-hungry CTAs out of that SM for the bubble; ask for the max-shared
+// configuration so side-task CTAs can co-reside with it.
+void configure_timeline_kernels() {
+  static bool done = false;
+  if (done) return;
+  cudaFuncSetAttribute(gap_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       cudaSharedmemCarveoutMaxShared);
+  cudaFuncSetAttribute(stamp_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       cudaSharedmemCarveoutMaxShared);
+  done = true;
+}
+
 void launch_gap(const GapArgs& a, cudaStream_t s) { gap_kernel<<<1, 1, 0, s>>>(a); }
 
 void launch_stamp(std::uint64_t* out, volatile std::uint32_t* flag, std::uint32_t val,

@@ -44,6 +44,7 @@ struct GapArgs {
   std::int32_t mode;         // 0: before an op, 1: epoch end, 2: first epoch begin
 };
 
+void configure_timeline_kernels();
 void launch_gap(const GapArgs& a, cudaStream_t s);
 // Writes %globaltimer to *host_mapped and publishes it through *flag.
 void launch_stamp(std::uint64_t* host_mapped, volatile std::uint32_t* flag, std::uint32_t val,

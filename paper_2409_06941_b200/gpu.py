@@ -136,6 +136,61 @@ class ImageTask:
         self.d2h_per_step = images_per_step * dw * dh * 3 if host_io else 0
 
 
+class PythonTask:
+    """A side task written in Python (the paper's Python interface,
+    PAPER.md:484-499): override the transition hooks; `run_next_step`
+    must enqueue one bounded step on the given (low-priority) stream and
+    return.  Hooks run on the harness worker thread (they take the GIL, so
+    keep them short)."""
+
+    work_units_per_step = 0.0
+    memory_gib = 0.0
+
+    def create(self): pass
+    def init(self, stream: int): pass
+    def start(self): pass
+    def run_next_step(self, stream: int): raise NotImplementedError
+    def pause(self): pass
+    def stop(self): pass
+    def finished(self, steps_completed: int) -> bool: return False
+
+    def __init__(self):
+        def wrap(fn):
+            def cb(*args):
+                try:
+                    fn(*args)
+                    return A.FR_OK
+                except Exception as e:  # noqa: BLE001 -- surfaced as a status
+                    self.error = e
+                    return A.FR_ERR_INVARIANT
+            return cb
+
+        def fin(user, steps, out):
+            try:
+                out[0] = int(bool(self.finished(steps)))
+                return A.FR_OK
+            except Exception as e:  # noqa: BLE001
+                self.error = e
+                return A.FR_ERR_INVARIANT
+
+        f = A.SideTaskVTableC._fields_
+        ty = dict(f)
+        self._cbs = [
+            ty["create"](wrap(lambda u: self.create())),
+            ty["init"](wrap(lambda u, s: self.init(s))),
+            ty["start"](wrap(lambda u: self.start())),
+            ty["run_next_step"](wrap(lambda u, s: self.run_next_step(s))),
+            ty["pause"](wrap(lambda u: self.pause())),
+            ty["stop"](wrap(lambda u: self.stop())),
+            ty["finished"](fin),
+            ty["destroy"](lambda u: None),
+        ]
+        self.vt = A.SideTaskVTableC(*self._cbs, float(self.work_units_per_step))
+        self.user = C.c_void_p(0)
+        self.units_per_step = float(self.work_units_per_step)
+        self.error = None
+
+
 class Harness:
     """fr_harness: one GPU replaying stage `stage` of a p-stage 1F1B pipeline
     of bf16 GEMM stand-ins, with a side-task worker harvesting its bubbles."""
@@ -181,6 +236,10 @@ class Harness:
         prof = A.TaskProfileC()
         check(glib().fr_harness_reprofile(self._h, task_id.encode(), C.byref(prof)))
         return prof.as_dict()
+
+    def reprofile_bubbles(self):
+        """Bubble durations := medians of the last run's measured bubbles."""
+        check(glib().fr_harness_reprofile_bubbles(self._h))
 
     def stop_task(self, task_id: str):
         check(glib().fr_harness_stop_task(self._h, task_id.encode()))
