@@ -27,6 +27,8 @@ int fr_stream_create(int32_t priority_class /* 0 = lowest, 1 = highest */, void*
 int fr_stream_destroy(void* stream);
 int fr_stream_synchronize(void* stream);
 int fr_device_sm_count(int32_t* sms);
+/* synchronous copy between any host/device buffers (unified addressing) */
+int fr_memcpy(void* dst, const void* src, int64_t bytes);
 /* diagnostics: spin `cycles` SM clocks on one warp, write {cycles, ns} */
 int fr_clock_probe(uint64_t* out_cycles_ns, int64_t cycles, void* stream);
 
@@ -58,6 +60,28 @@ int fr_img_resize_watermark_prepared(const fr_img_plan* plan, const uint8_t* src
 int fr_img_generate(uint8_t* dst, int32_t n, int32_t w, int32_t h, int32_t channels,
                     uint64_t seed, int32_t first_index, void* stream);
 int fr_img_generate_watermark(uint8_t* wm, int32_t w, int32_t h, uint64_t seed, void* stream);
+
+/* ------------------------------------------------ K1/K2: PageRank (pull) */
+/* Incoming-CSR graph on the device.  fr_pr_graph_rmat generates RMAT edges
+ * (a,b,c = .57,.19,.19; counter-based, identical to oracle/sidetasks.c),
+ * drops self loops and duplicates and builds the CSR sorted by (dst, src).
+ * Synchronous (setup, not a step). */
+typedef struct fr_pr_graph fr_pr_graph;
+typedef struct fr_pr_state fr_pr_state;
+int fr_pr_graph_rmat(int32_t scale, int32_t edge_factor, uint64_t seed, void* stream,
+                     fr_pr_graph** out);
+int fr_pr_graph_destroy(fr_pr_graph* g);
+int fr_pr_graph_info(const fr_pr_graph* g, int32_t* V, int64_t* E, int32_t* n_blocks);
+/* device pointers: offsets[V+1], col_idx[E], outdeg[V] */
+int fr_pr_graph_csr(const fr_pr_graph* g, const int32_t** offsets, const int32_t** col_idx,
+                    const int32_t** outdeg);
+int fr_pr_state_create(const fr_pr_graph* g, fr_pr_state** out);
+int fr_pr_state_destroy(fr_pr_state* st);
+/* r = 1/V, c = r * inv_outdeg */
+int fr_pr_reset(fr_pr_state* st, void* stream);
+/* `iters` pull iterations: r' = (1-d)/V + d * A_in^T c ; c' = r' * inv_outdeg */
+int fr_pr_step(fr_pr_state* st, int32_t iters, float damping, void* stream);
+int fr_pr_ranks(const fr_pr_state* st, const float** r, int64_t* iterations);
 
 /* ------------------------------------------------ side-task plugin surface */
 /* The paper's overridable transition functions:
@@ -95,6 +119,20 @@ int fr_image_task_memory(const fr_image_task_config* cfg, double* gib);
 /* device pointers of the last processed batch slot (for checking) */
 int fr_image_task_buffers(void* user, const uint8_t** src, uint8_t** dst, const uint8_t** wm,
                           int64_t* steps_done);
+
+typedef struct fr_pagerank_task_config {
+  int32_t scale;          /* RMAT scale: V = 2^scale */
+  int32_t edge_factor;    /* edges generated = edge_factor * V (before dedup) */
+  uint64_t seed;
+  int32_t iters_per_step; /* pull iterations per RunNextStep */
+  float damping;          /* 0.85 */
+  int64_t total_steps;    /* <= 0: unbounded */
+} fr_pagerank_task_config;
+/* builds the graph immediately (work_units_per_step = E * iters_per_step) */
+int fr_pagerank_task_create(const fr_pagerank_task_config* cfg, fr_side_task_vtable* vt,
+                            void** user);
+int fr_pagerank_task_info(void* user, int32_t* V, int64_t* E, double* memory_gib,
+                          const float** ranks, int64_t* iterations);
 
 /* ------------------------------------------------------ the GPU runtime */
 /* One GPU replaying stage `stage` of a p-stage 1F1B pipeline whose FP/BP

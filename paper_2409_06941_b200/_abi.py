@@ -393,6 +393,7 @@ GPU_PROTOTYPES = {
     "fr_stream_synchronize": (C.c_int, [vp]),
     "fr_device_sm_count": (C.c_int, [P(i32)]),
     "fr_clock_probe": (C.c_int, [vp, i64, vp]),
+    "fr_memcpy": (C.c_int, [vp, vp, i64]),
     "fr_img_plan_create": (C.c_int, [i32, i32, i32, i32, P(vp)]),
     "fr_img_plan_destroy": (C.c_int, [vp]),
     "fr_img_plan_path": (C.c_int, [vp, P(i32)]),
@@ -425,6 +426,26 @@ class ImageTaskConfigC(Struct):
         ("batch", i32), ("images_per_step", i32), ("host_io", i32), ("reserved", i32),
         ("seed", u64), ("total_steps", i64),
     ]
+
+
+class PageRankTaskConfigC(Struct):
+    _fields_ = [("scale", i32), ("edge_factor", i32), ("seed", u64), ("iters_per_step", i32),
+                ("damping", C.c_float), ("total_steps", i64)]
+
+
+GPU_PROTOTYPES.update({
+    "fr_pr_graph_rmat": (C.c_int, [i32, i32, u64, vp, P(vp)]),
+    "fr_pr_graph_destroy": (C.c_int, [vp]),
+    "fr_pr_graph_info": (C.c_int, [vp, P(i32), P(i64), P(i32)]),
+    "fr_pr_graph_csr": (C.c_int, [vp, P(vp), P(vp), P(vp)]),
+    "fr_pr_state_create": (C.c_int, [vp, P(vp)]),
+    "fr_pr_state_destroy": (C.c_int, [vp]),
+    "fr_pr_reset": (C.c_int, [vp, vp]),
+    "fr_pr_step": (C.c_int, [vp, i32, C.c_float, vp]),
+    "fr_pr_ranks": (C.c_int, [vp, P(vp), P(i64)]),
+    "fr_pagerank_task_create": (C.c_int, [P(PageRankTaskConfigC), P(SideTaskVTableC), P(vp)]),
+    "fr_pagerank_task_info": (C.c_int, [vp, P(i32), P(i64), P(dbl), P(vp), P(i64)]),
+})
 
 
 class HarnessConfigC(Struct):

@@ -29,6 +29,12 @@ int fr_clock_probe(uint64_t* out_cycles_ns, int64_t cycles, void* stream) {
   return FR_OK;
 }
 
+int fr_memcpy(void* dst, const void* src, int64_t bytes) {
+  if (bytes < 0) return frcapi::fail(FR_ERR_ARGUMENT, "negative size");
+  if (bytes) FR_CUDA_TRY(cudaMemcpy(dst, src, static_cast<size_t>(bytes), cudaMemcpyDefault));
+  return FR_OK;
+}
+
 int fr_stream_create(int32_t priority_class, void** stream) {
   if (!stream) return frcapi::fail(FR_ERR_ARGUMENT, "null stream out");
   int least = 0, greatest = 0;  // CUDA: numerically lower = higher priority

@@ -136,6 +136,94 @@ class ImageTask:
         self.d2h_per_step = images_per_step * dw * dh * 3 if host_io else 0
 
 
+def _dev_copy(ptr: int, n: int, dtype) -> torch.Tensor:
+    """Copy n elements from a raw device pointer owned by the library."""
+    out = torch.empty(n, dtype=dtype, device="cuda")
+    if n:
+        check(glib().fr_memcpy(out.data_ptr(), ptr, n * out.element_size()))
+    return out
+
+
+class PageRankGraph:
+    """fr_pr_graph: RMAT graph as an incoming CSR on the device."""
+
+    def __init__(self, scale=20, edge_factor=16, seed=1, stream=None):
+        h = C.c_void_p()
+        check(glib().fr_pr_graph_rmat(scale, edge_factor, seed, _stream(stream), C.byref(h)))
+        self._h = h
+        V, E, nb = C.c_int32(), C.c_int64(), C.c_int32()
+        check(glib().fr_pr_graph_info(h, C.byref(V), C.byref(E), C.byref(nb)))
+        self.V, self.E, self.n_blocks = V.value, E.value, nb.value
+
+    def csr(self):
+        o, c, d = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        check(glib().fr_pr_graph_csr(self._h, C.byref(o), C.byref(c), C.byref(d)))
+        torch.cuda.synchronize()
+        return (_dev_copy(o.value, self.V + 1, torch.int32), _dev_copy(c.value, self.E, torch.int32),
+                _dev_copy(d.value, self.V, torch.int32))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _glib is not None:
+            _glib.fr_pr_graph_destroy(h)
+            self._h = None
+
+
+class PageRankState:
+    def __init__(self, graph: PageRankGraph):
+        self.graph = graph
+        h = C.c_void_p()
+        check(glib().fr_pr_state_create(graph._h, C.byref(h)))
+        self._h = h
+
+    def reset(self, stream=None):
+        check(glib().fr_pr_reset(self._h, _stream(stream)))
+
+    def step(self, iters=1, damping=0.85, stream=None):
+        check(glib().fr_pr_step(self._h, iters, damping, _stream(stream)))
+
+    def ranks(self) -> torch.Tensor:
+        p, it = C.c_void_p(), C.c_int64()
+        check(glib().fr_pr_ranks(self._h, C.byref(p), C.byref(it)))
+        torch.cuda.synchronize()
+        return _dev_copy(p.value, self.graph.V, torch.float32)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _glib is not None:
+            _glib.fr_pr_state_destroy(h)
+            self._h = None
+
+
+class PageRankTask:
+    """Built-in PageRank side task (fr_pagerank_task_create)."""
+
+    def __init__(self, scale=20, edge_factor=16, seed=1, iters_per_step=1, damping=0.85,
+                 total_steps=0):
+        self.cfg = A.PageRankTaskConfigC(scale=scale, edge_factor=edge_factor, seed=seed,
+                                         iters_per_step=iters_per_step, damping=damping,
+                                         total_steps=total_steps)
+        self.vt = A.SideTaskVTableC()
+        self.user = C.c_void_p()
+        check(glib().fr_pagerank_task_create(C.byref(self.cfg), C.byref(self.vt), C.byref(self.user)))
+        V, E, gib = C.c_int32(), C.c_int64(), C.c_double()
+        check(glib().fr_pagerank_task_info(self.user, C.byref(V), C.byref(E), C.byref(gib), None, None))
+        self.V, self.E, self.memory_gib = V.value, E.value, gib.value
+        self.units_per_step = self.vt.work_units_per_step
+        # compulsory bytes per pull iteration: offsets + col_idx + c gather
+        # source (read once) + inv_outdeg + r' and c' writes
+        self.bytes_per_step = iters_per_step * (4 * (self.V + 1) + 4 * self.E + 16 * self.V)
+        self.h2d_per_step = self.d2h_per_step = 0
+
+    def ranks(self):
+        p, it = C.c_void_p(), C.c_int64()
+        check(glib().fr_pagerank_task_info(self.user, None, None, None, C.byref(p), C.byref(it)))
+        if not p.value:
+            return None, it.value
+        torch.cuda.synchronize()
+        return _dev_copy(p.value, self.V, torch.float32), it.value
+
+
 class PythonTask:
     """A side task written in Python (the paper's Python interface,
     PAPER.md:484-499): override the transition hooks; `run_next_step`

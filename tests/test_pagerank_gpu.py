@@ -1,0 +1,83 @@
+"""K1/K2 PageRank on the B200 vs the CPU oracle: identical graph (bit-exact
+CSR), ranks within L1 <= 1e-6 after a fixed iteration count (north star)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def g():
+    from paper_2409_06941_b200 import gpu
+    gpu.glib()
+    return gpu
+
+
+@pytest.fixture(scope="module")
+def rmat20(g, sidetask_oracle):
+    graph = g.PageRankGraph(scale=20, edge_factor=16, seed=1)
+    src, dst = sidetask_oracle.rmat_edges(20, 16, seed=1)
+    csr = sidetask_oracle.build_pull_csr(1 << 20, src, dst)
+    return graph, csr
+
+
+@pytest.mark.parametrize("scale,ef,seed", [(1, 4, 3), (6, 8, 2), (12, 16, 5)])
+def test_graph_build_matches_oracle_small(g, sidetask_oracle, scale, ef, seed):
+    graph = g.PageRankGraph(scale=scale, edge_factor=ef, seed=seed)
+    src, dst = sidetask_oracle.rmat_edges(scale, ef, seed=seed)
+    off, col, outdeg = sidetask_oracle.build_pull_csr(1 << scale, src, dst)
+    o2, c2, d2 = (t.cpu().numpy() for t in graph.csr())
+    assert graph.E == len(col)
+    assert np.array_equal(o2, off) and np.array_equal(c2, col) and np.array_equal(d2, outdeg)
+
+
+def test_graph_build_matches_oracle_scale20(rmat20):
+    graph, (off, col, outdeg) = rmat20
+    o2, c2, d2 = (t.cpu().numpy() for t in graph.csr())
+    assert graph.V == 1 << 20 and graph.E == len(col)
+    assert np.array_equal(o2, off) and np.array_equal(c2, col) and np.array_equal(d2, outdeg)
+    assert (outdeg == 0).mean() > 0.3  # RMAT: dangling-heavy, the dropped-mass rule matters
+
+
+@pytest.mark.parametrize("iters", [1, 20])
+def test_ranks_l1_scale20(g, sidetask_oracle, rmat20, iters):
+    graph, (off, col, outdeg) = rmat20
+    st = g.PageRankState(graph)
+    st.reset()
+    st.step(iters, 0.85)
+    got = st.ranks().double().cpu().numpy()
+    want = sidetask_oracle.pr_run(off, col, outdeg, iters, 0.85)
+    l1 = np.abs(got - want).sum()
+    assert l1 <= 1e-6, l1
+    assert want.sum() < 1.0  # dangling mass dropped, not redistributed
+
+
+def test_ranks_l1_small_and_stepwise(g, sidetask_oracle):
+    graph = g.PageRankGraph(scale=14, edge_factor=8, seed=9)
+    src, dst = sidetask_oracle.rmat_edges(14, 8, seed=9)
+    off, col, outdeg = sidetask_oracle.build_pull_csr(1 << 14, src, dst)
+    st = g.PageRankState(graph)
+    st.reset()
+    for _ in range(7):      # 7 steps of 3 iterations == 21 iterations
+        st.step(3, 0.85)
+    got = st.ranks().double().cpu().numpy()
+    want = sidetask_oracle.pr_run(off, col, outdeg, 21, 0.85)
+    assert np.abs(got - want).sum() <= 1e-6
+
+
+def test_pagerank_task_in_bubbles(g, sidetask_oracle):
+    h = g.Harness(num_stages=4, num_micro_batches=4, stage=2, layers=2, profile_reps=2,
+                  profile_epochs=1)
+    task = g.PageRankTask(scale=16, edge_factor=16, seed=4, iters_per_step=2)
+    ok, prof = h.submit("pagerank", task, profile_steps=8)
+    assert ok
+    h.run(2, True)
+    r = h.run(2, True)
+    assert r["steps_completed"] > 0
+    ranks, iters = task.ranks()
+    assert iters > 0 and iters % 2 == 0
+    src, dst = sidetask_oracle.rmat_edges(16, 16, seed=4)
+    off, col, outdeg = sidetask_oracle.build_pull_csr(1 << 16, src, dst)
+    want = sidetask_oracle.pr_run(off, col, outdeg, iters, 0.85)
+    assert np.abs(ranks.double().cpu().numpy() - want).sum() <= 1e-6
+    h.close()
