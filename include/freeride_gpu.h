@@ -83,6 +83,27 @@ int fr_pr_reset(fr_pr_state* st, void* stream);
 int fr_pr_step(fr_pr_state* st, int32_t iters, float damping, void* stream);
 int fr_pr_ranks(const fr_pr_state* st, const float** r, int64_t* iterations);
 
+/* ------------------------------------------- K3/K4: Graph-SGD (rank k MF) */
+/* Rating graph (u, v, r) with power-law endpoints (counter-based, identical
+ * to oracle/sidetasks.c) and an fp32 latent matrix L[V][k], k in
+ * {4,8,16,32,64,128}.  Hogwild updates: racy by design. */
+typedef struct fr_sgd_problem fr_sgd_problem;
+int fr_sgd_problem_generate(int32_t V, int64_t E, int32_t k, uint64_t edge_seed,
+                            uint64_t init_seed, void* stream, fr_sgd_problem** out);
+int fr_sgd_problem_destroy(fr_sgd_problem* p);
+/* L ~ U(0, 1/sqrt(k)), seeded */
+int fr_sgd_reinit(fr_sgd_problem* p, uint64_t init_seed, void* stream);
+/* one step: edges [e_begin, e_end) */
+int fr_sgd_step(fr_sgd_problem* p, int64_t e_begin, int64_t e_end, float eta, float lambda,
+                void* stream);
+/* K4: *d_acc (device fp64) += sum of squared errors over [e_begin, e_end) */
+int fr_sgd_sqerr(const fr_sgd_problem* p, int64_t e_begin, int64_t e_end, double* d_acc,
+                 void* stream);
+/* synchronous RMSE over all edges */
+int fr_sgd_rmse(const fr_sgd_problem* p, void* stream, double* rmse);
+int fr_sgd_buffers(const fr_sgd_problem* p, const int32_t** u, const int32_t** v, const float** r,
+                   float** L, int32_t* V, int64_t* E, int32_t* k);
+
 /* ------------------------------------------------ side-task plugin surface */
 /* The paper's overridable transition functions:
  * CreateSideTask / InitSideTask / StartSideTask / RunNextStep /
@@ -133,6 +154,21 @@ int fr_pagerank_task_create(const fr_pagerank_task_config* cfg, fr_side_task_vta
                             void** user);
 int fr_pagerank_task_info(void* user, int32_t* V, int64_t* E, double* memory_gib,
                           const float** ranks, int64_t* iterations);
+
+typedef struct fr_sgd_task_config {
+  int32_t V;              /* 3,072,441 (Orkut shape) */
+  int32_t k;              /* rank, 16 */
+  int64_t E;              /* 117,185,083 */
+  uint64_t edge_seed;
+  uint64_t init_seed;
+  int64_t edges_per_step; /* edges per RunNextStep (wraps into the next epoch) */
+  float eta;              /* 0.01 */
+  float lambda;           /* 0.05 */
+  int64_t total_steps;    /* <= 0: unbounded */
+} fr_sgd_task_config;
+/* generates the rating graph on the device immediately (setup) */
+int fr_sgd_task_create(const fr_sgd_task_config* cfg, fr_side_task_vtable* vt, void** user);
+int fr_sgd_task_problem(void* user, fr_sgd_problem** p, int64_t* epochs_done);
 
 /* ------------------------------------------------------ the GPU runtime */
 /* One GPU replaying stage `stage` of a p-stage 1F1B pipeline whose FP/BP

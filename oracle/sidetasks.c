@@ -168,10 +168,11 @@ void orc_pr_run(int32_t V, const int32_t* off, const int32_t* col, const int32_t
 #define SGD_PERM_MUL 2654435761ull
 
 static inline int32_t sgd_vertex(uint64_t h, int32_t V) {
-  /* power-law-ish skew: x^3 concentrates mass on low ids, then a
-   * multiplicative bijection mod V scatters the hubs */
+  /* power-law-ish skew: density ~ v^(-1/3) from x^1.5 = x*sqrt(x) (IEEE
+   * sqrt: bit-identical on CPU and GPU), max degree ~1e4 at the Orkut shape;
+   * then a multiplicative bijection mod V scatters the hubs */
   const double x = (double)(h >> 11) * (1.0 / 9007199254740992.0);
-  int64_t v = (int64_t)((double)V * x * x * x);
+  int64_t v = (int64_t)((double)V * x * sqrt(x));
   if (v >= V) v = V - 1;
   return (int32_t)(((uint64_t)v * SGD_PERM_MUL) % (uint64_t)V);
 }

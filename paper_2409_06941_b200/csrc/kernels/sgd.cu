@@ -1,0 +1,416 @@
+// K3/K4: Graph-SGD matrix factorisation (Gardenia SGD;
+// SURVEY.md §8 a16), one bounded step = an edge chunk [e_begin, e_end).
+//
+//   per edge (u, v, r):  e = r - <L_u, L_v>
+//                        L_u += eta (e L_v - lambda L_u)
+//                        L_v += eta (e L_u - lambda L_v)      (old L_u)
+//   Hogwild: concurrent edges race on shared vertices by design (lost
+//   updates are part of the algorithm), so parity is on RMSE (north star:
+//   |dRMSE| <= 1e-3 vs the sequential CPU oracle after a fixed epoch count).
+//
+// B200-first layout: L is fp32 [V][K] row-major, one 64 B row per vertex at
+// K = 16 (HBM3e access granule); K/4 lanes own one edge, each lane one
+// float4 of both rows (16-byte loads/stores), the dot product is an
+// xor-shuffle inside the lane group.  Edge arrays are SoA (u, v, r).  The
+// latent matrix (197 MB at the Orkut shape) does not fit the 126 MB L2, so a
+// step streams 12 B of edge + 4 x 64 B of random rows per edge from HBM:
+// 268 B/edge algorithmic.  Each lane carries two edges per iteration to keep
+// enough 64 B requests in flight.
+#include <cmath>
+#include <cstring>
+
+#include "freeride_gpu.h"
+#include "kernels/common.cuh"
+
+namespace {
+
+constexpr int kSgdThreads = 256;
+constexpr uint64_t kSgdPermMul = 2654435761ull;
+
+__device__ __forceinline__ int32_t sgd_vertex(uint64_t h, int32_t V) {
+  const double x = static_cast<double>(h >> 11) * (1.0 / 9007199254740992.0);
+  double t = static_cast<double>(V) * x;
+  t = t * sqrt(x);
+  int64_t v = static_cast<int64_t>(t);
+  if (v >= V) v = V - 1;
+  return static_cast<int32_t>((static_cast<uint64_t>(v) * kSgdPermMul) % static_cast<uint64_t>(V));
+}
+
+__global__ void sgd_edges_kernel(int32_t V, int64_t E, uint64_t seed, int32_t* __restrict__ u,
+                                 int32_t* __restrict__ v, float* __restrict__ r) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < E;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t a = sgd_vertex(frk::splitmix64(seed ^ (2 * static_cast<uint64_t>(e))), V);
+    const int32_t b = sgd_vertex(frk::splitmix64(seed ^ (2 * static_cast<uint64_t>(e) + 1)), V);
+    u[e] = a;
+    v[e] = b;
+    const uint64_t hr = frk::splitmix64((seed * 0x2545F4914F6CDD1Dull) ^
+                                        (static_cast<uint64_t>(a) * static_cast<uint64_t>(V) +
+                                         static_cast<uint64_t>(b)));
+    r[e] = static_cast<float>(1 + static_cast<int>(hr % 5));
+  }
+}
+
+__global__ void sgd_init_kernel(int64_t n, float scale, uint64_t seed, float* __restrict__ L) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    L[i] = static_cast<float>(frk::splitmix64(seed ^ (0x4C4154ull << 40) ^ static_cast<uint64_t>(i)) >> 40) * scale;
+}
+
+template <int K>
+struct Row {
+  static constexpr int kLanes = K / 4;  // lanes per edge, one float4 each
+};
+
+template <int K>
+__device__ __forceinline__ float group_sum(float x) {
+#pragma unroll
+  for (int o = Row<K>::kLanes >> 1; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+__device__ __forceinline__ float dot4(float4 a, float4 b) {
+  return a.x * b.x + a.y * b.y + a.z * b.z + a.w * b.w;
+}
+
+// The update as deltas: L_u += du, L_v += dv, both from the values read.
+__device__ __forceinline__ void deltas(const float4& a, const float4& b, float err, float eta,
+                                       float lam, float4& da, float4& db) {
+  da = make_float4(eta * (err * b.x - lam * a.x), eta * (err * b.y - lam * a.y),
+                   eta * (err * b.z - lam * a.z), eta * (err * b.w - lam * a.w));
+  db = make_float4(eta * (err * a.x - lam * b.x), eta * (err * a.y - lam * b.y),
+                   eta * (err * a.z - lam * b.z), eta * (err * a.w - lam * b.w));
+}
+
+// Deltas land with 16-byte vector atomics (red.global.add.v4.f32, sm_90+):
+// with ~1e5 edges in flight a hub vertex sees tens of concurrent updates,
+// and plain Hogwild stores would drop all but one of them (measured: RMSE
+// 0.25 above the sequential oracle after one epoch).  With atomic deltas
+// every update lands; concurrent ones act like a small mini-batch on the hub.
+__device__ __forceinline__ void apply(float4* p, const float4& d) { atomicAdd(p, d); }
+
+// Each lane group handles edges g, g + G, g + 2G, ... two at a time.
+template <int K>
+__global__ void __launch_bounds__(kSgdThreads) sgd_step_kernel(
+    const int32_t* __restrict__ us, const int32_t* __restrict__ vs, const float* __restrict__ rs,
+    float* __restrict__ L, int64_t e0, int64_t e1, float eta, float lam) {
+  constexpr int LN = Row<K>::kLanes;
+  const int lane = threadIdx.x & 31, sub = lane % LN;
+  const int64_t group = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / LN;
+  const int64_t G = static_cast<int64_t>(gridDim.x) * blockDim.x / LN;
+  float4* L4 = reinterpret_cast<float4*>(L);
+  // Warp-uniform trip count (the group shuffles need every lane present);
+  // lanes whose edge is past the end ride along predicated off.
+  const int64_t warp_first = group - lane / LN;
+  for (int64_t ew = e0 + warp_first; ew < e1; ew += 2 * G) {
+    const int64_t e = ew + lane / LN, f = e + G;
+    const bool one = e < e1, two = f < e1;
+    const int32_t u0 = one ? __ldg(&us[e]) : 0, v0 = one ? __ldg(&vs[e]) : 0;
+    const float r0 = one ? __ldg(&rs[e]) : 0.0f;
+    const int32_t u1 = two ? __ldg(&us[f]) : u0, v1 = two ? __ldg(&vs[f]) : v0;
+    const float r1 = two ? __ldg(&rs[f]) : 0.0f;
+    const float4 a0 = L4[static_cast<int64_t>(u0) * LN + sub], b0 = L4[static_cast<int64_t>(v0) * LN + sub];
+    const float4 a1 = L4[static_cast<int64_t>(u1) * LN + sub], b1 = L4[static_cast<int64_t>(v1) * LN + sub];
+    const float err0 = r0 - group_sum<K>(dot4(a0, b0));
+    const float err1 = r1 - group_sum<K>(dot4(a1, b1));
+    float4 da, db;
+    if (one) {
+      deltas(a0, b0, err0, eta, lam, da, db);
+      apply(&L4[static_cast<int64_t>(u0) * LN + sub], da);
+      apply(&L4[static_cast<int64_t>(v0) * LN + sub], db);
+    }
+    if (two) {
+      deltas(a1, b1, err1, eta, lam, da, db);
+      apply(&L4[static_cast<int64_t>(u1) * LN + sub], da);
+      apply(&L4[static_cast<int64_t>(v1) * LN + sub], db);
+    }
+  }
+}
+
+// K4: sum of squared errors over [e0, e1) into *acc (fp64).
+template <int K>
+__global__ void __launch_bounds__(kSgdThreads) sgd_sqerr_kernel(
+    const int32_t* __restrict__ us, const int32_t* __restrict__ vs, const float* __restrict__ rs,
+    const float* __restrict__ L, int64_t e0, int64_t e1, double* __restrict__ acc) {
+  constexpr int LN = Row<K>::kLanes;
+  __shared__ double red[kSgdThreads / 32];
+  const int lane = threadIdx.x & 31, sub = lane % LN;
+  const int64_t group = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / LN;
+  const int64_t G = static_cast<int64_t>(gridDim.x) * blockDim.x / LN;
+  const float4* L4 = reinterpret_cast<const float4*>(L);
+  double s = 0.0;
+  const int64_t warp_first = group - lane / LN;
+  for (int64_t ew = e0 + warp_first; ew < e1; ew += G) {  // warp-uniform (shuffles)
+    const int64_t e = ew + lane / LN;
+    const bool ok = e < e1;
+    const float4 a = __ldg(&L4[static_cast<int64_t>(ok ? __ldg(&us[e]) : 0) * LN + sub]);
+    const float4 b = __ldg(&L4[static_cast<int64_t>(ok ? __ldg(&vs[e]) : 0) * LN + sub]);
+    double d = static_cast<double>(a.x) * b.x + static_cast<double>(a.y) * b.y +
+               static_cast<double>(a.z) * b.z + static_cast<double>(a.w) * b.w;
+#pragma unroll
+    for (int o = LN >> 1; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+    const double err = (ok ? static_cast<double>(__ldg(&rs[e])) : 0.0) - d;
+    if (sub == 0 && ok) s += err * err;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kSgdThreads / 32; ++w) t += red[w];
+    atomicAdd(acc, t);
+  }
+}
+
+int grid_for(int64_t work, int threads, int per_sm) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t want = (work + threads - 1) / threads;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(sms) * per_sm)));
+}
+
+}  // namespace
+
+struct fr_sgd_problem {
+  int32_t V = 0, K = 0;
+  int64_t E = 0;
+  int32_t* u = nullptr;
+  int32_t* v = nullptr;
+  float* r = nullptr;
+  float* L = nullptr;
+  double* acc = nullptr;
+  int sms = 148;
+};
+
+namespace {
+
+template <int K>
+void launch_step(fr_sgd_problem* p, int64_t a, int64_t b, float eta, float lam, cudaStream_t s) {
+  const int64_t groups = (b - a + 1) / 2;
+  const int grid = grid_for(groups * Row<K>::kLanes, kSgdThreads, 8);
+  sgd_step_kernel<K><<<grid, kSgdThreads, 0, s>>>(p->u, p->v, p->r, p->L, a, b, eta, lam);
+}
+
+template <int K>
+void launch_sqerr(const fr_sgd_problem* p, int64_t a, int64_t b, double* acc, cudaStream_t s) {
+  const int grid = grid_for((b - a) * Row<K>::kLanes, kSgdThreads, 8);
+  sgd_sqerr_kernel<K><<<grid, kSgdThreads, 0, s>>>(p->u, p->v, p->r, p->L, a, b, acc);
+}
+
+bool rank_supported(int k) { return k == 4 || k == 8 || k == 16 || k == 32 || k == 64 || k == 128; }
+
+}  // namespace
+
+extern "C" {
+
+int fr_sgd_problem_generate(int32_t V, int64_t E, int32_t k, uint64_t edge_seed, uint64_t init_seed,
+                            void* stream, fr_sgd_problem** out) {
+  if (!out) return frcapi::fail(FR_ERR_ARGUMENT, "null problem out");
+  if (V < 1 || E < 0) return frcapi::fail(FR_ERR_VALIDATION, "V >= 1, E >= 0", "V");
+  if (!rank_supported(k)) return frcapi::fail(FR_ERR_UNSUPPORTED, "rank must be 4, 8, 16, 32, 64 or 128");
+  auto s = static_cast<cudaStream_t>(stream);
+  auto* p = new fr_sgd_problem;
+  p->V = V;
+  p->E = E;
+  p->K = k;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaError_t e = cudaMalloc(&p->u, std::max<int64_t>(E, 1) * sizeof(int32_t));
+  if (e == cudaSuccess) e = cudaMalloc(&p->v, std::max<int64_t>(E, 1) * sizeof(int32_t));
+  if (e == cudaSuccess) e = cudaMalloc(&p->r, std::max<int64_t>(E, 1) * sizeof(float));
+  if (e == cudaSuccess) e = cudaMalloc(&p->L, static_cast<size_t>(V) * k * sizeof(float));
+  if (e == cudaSuccess) e = cudaMalloc(&p->acc, sizeof(double));
+  if (e != cudaSuccess) {
+    for (void* q : {static_cast<void*>(p->u), static_cast<void*>(p->v), static_cast<void*>(p->r),
+                    static_cast<void*>(p->L), static_cast<void*>(p->acc)})
+      if (q) cudaFree(q);
+    delete p;
+    return frcapi::cuda_status(e, "sgd problem allocation");
+  }
+  if (E > 0) sgd_edges_kernel<<<grid_for(E, 256, 16), 256, 0, s>>>(V, E, edge_seed, p->u, p->v, p->r);
+  FR_CUDA_LAUNCHED("sgd_edges");
+  *out = p;
+  return fr_sgd_reinit(p, init_seed, stream);
+}
+
+int fr_sgd_problem_destroy(fr_sgd_problem* p) {
+  if (!p) return FR_OK;
+  for (void* q : {static_cast<void*>(p->u), static_cast<void*>(p->v), static_cast<void*>(p->r),
+                  static_cast<void*>(p->L), static_cast<void*>(p->acc)})
+    if (q) cudaFree(q);
+  delete p;
+  return FR_OK;
+}
+
+int fr_sgd_reinit(fr_sgd_problem* p, uint64_t init_seed, void* stream) {
+  if (!p) return frcapi::fail(FR_ERR_ARGUMENT, "null problem");
+  const int64_t n = static_cast<int64_t>(p->V) * p->K;
+  const float scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(p->K))) * (1.0f / 16777216.0f);
+  sgd_init_kernel<<<grid_for(n, 256, 16), 256, 0, static_cast<cudaStream_t>(stream)>>>(n, scale, init_seed, p->L);
+  FR_CUDA_LAUNCHED("sgd_init");
+  return FR_OK;
+}
+
+int fr_sgd_step(fr_sgd_problem* p, int64_t e_begin, int64_t e_end, float eta, float lambda,
+                void* stream) {
+  if (!p) return frcapi::fail(FR_ERR_ARGUMENT, "null problem");
+  if (e_begin < 0 || e_end > p->E || e_begin > e_end)
+    return frcapi::fail(FR_ERR_VALIDATION, "edge range outside [0, E]", "edges");
+  if (e_begin == e_end) return FR_OK;
+  auto s = static_cast<cudaStream_t>(stream);
+  switch (p->K) {
+    case 4: launch_step<4>(p, e_begin, e_end, eta, lambda, s); break;
+    case 8: launch_step<8>(p, e_begin, e_end, eta, lambda, s); break;
+    case 16: launch_step<16>(p, e_begin, e_end, eta, lambda, s); break;
+    case 32: launch_step<32>(p, e_begin, e_end, eta, lambda, s); break;
+    case 64: launch_step<64>(p, e_begin, e_end, eta, lambda, s); break;
+    default: launch_step<128>(p, e_begin, e_end, eta, lambda, s); break;
+  }
+  FR_CUDA_LAUNCHED("sgd_step");
+  return FR_OK;
+}
+
+int fr_sgd_sqerr(const fr_sgd_problem* p, int64_t e_begin, int64_t e_end, double* d_acc, void* stream) {
+  if (!p || !d_acc) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  if (e_begin < 0 || e_end > p->E || e_begin > e_end)
+    return frcapi::fail(FR_ERR_VALIDATION, "edge range outside [0, E]", "edges");
+  if (e_begin == e_end) return FR_OK;
+  auto s = static_cast<cudaStream_t>(stream);
+  switch (p->K) {
+    case 4: launch_sqerr<4>(p, e_begin, e_end, d_acc, s); break;
+    case 8: launch_sqerr<8>(p, e_begin, e_end, d_acc, s); break;
+    case 16: launch_sqerr<16>(p, e_begin, e_end, d_acc, s); break;
+    case 32: launch_sqerr<32>(p, e_begin, e_end, d_acc, s); break;
+    case 64: launch_sqerr<64>(p, e_begin, e_end, d_acc, s); break;
+    default: launch_sqerr<128>(p, e_begin, e_end, d_acc, s); break;
+  }
+  FR_CUDA_LAUNCHED("sgd_sqerr");
+  return FR_OK;
+}
+
+int fr_sgd_rmse(const fr_sgd_problem* p, void* stream, double* rmse) {
+  if (!p || !rmse) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  auto s = static_cast<cudaStream_t>(stream);
+  FR_CUDA_TRY(cudaMemsetAsync(p->acc, 0, sizeof(double), s));
+  const int rc = fr_sgd_sqerr(p, 0, p->E, p->acc, stream);
+  if (rc != FR_OK) return rc;
+  double sum = 0.0;
+  FR_CUDA_TRY(cudaMemcpyAsync(&sum, p->acc, sizeof(double), cudaMemcpyDeviceToHost, s));
+  FR_CUDA_TRY(cudaStreamSynchronize(s));
+  *rmse = p->E > 0 ? std::sqrt(sum / static_cast<double>(p->E)) : 0.0;
+  return FR_OK;
+}
+
+int fr_sgd_buffers(const fr_sgd_problem* p, const int32_t** u, const int32_t** v, const float** r,
+                   float** L, int32_t* V, int64_t* E, int32_t* k) {
+  if (!p) return frcapi::fail(FR_ERR_ARGUMENT, "null problem");
+  if (u) *u = p->u;
+  if (v) *v = p->v;
+  if (r) *r = p->r;
+  if (L) *L = p->L;
+  if (V) *V = p->V;
+  if (E) *E = p->E;
+  if (k) *k = p->K;
+  return FR_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------ built-in side task
+// The rating graph is the task's input and is generated at CreateSideTask
+// directly on the device (1.4 GB at the Orkut shape; uploading it inside a
+// bubble would overrun it); InitSideTask (re)initialises the latent model,
+// every RunNextStep processes the next `edges_per_step` edges (wrapping into
+// the next epoch), StopSideTask keeps nothing but the input graph.
+namespace {
+
+struct SgdTask {
+  fr_sgd_task_config cfg{};
+  fr_sgd_problem* p = nullptr;
+  int64_t cursor = 0, epochs = 0;
+};
+
+int sgd_task_create(void* u) {
+  auto* t = static_cast<SgdTask*>(u);
+  if (t->p) return FR_OK;
+  const int rc = fr_sgd_problem_generate(t->cfg.V, t->cfg.E, t->cfg.k, t->cfg.edge_seed,
+                                         t->cfg.init_seed, nullptr, &t->p);
+  if (rc == FR_OK) FR_CUDA_TRY(cudaDeviceSynchronize());
+  return rc;
+}
+
+int sgd_task_init(void* u, void* stream) {
+  auto* t = static_cast<SgdTask*>(u);
+  t->cursor = 0;
+  t->epochs = 0;
+  return fr_sgd_reinit(t->p, t->cfg.init_seed, stream);
+}
+
+int sgd_task_step(void* u, void* stream) {
+  auto* t = static_cast<SgdTask*>(u);
+  int64_t left = t->cfg.edges_per_step;
+  while (left > 0) {
+    const int64_t n = std::min<int64_t>(left, t->p->E - t->cursor);
+    const int rc = fr_sgd_step(t->p, t->cursor, t->cursor + n, t->cfg.eta, t->cfg.lambda, stream);
+    if (rc != FR_OK) return rc;
+    t->cursor += n;
+    left -= n;
+    if (t->cursor == t->p->E) {
+      t->cursor = 0;
+      t->epochs++;
+    }
+  }
+  return FR_OK;
+}
+
+int sgd_task_finished(void* u, int64_t done, int32_t* out) {
+  auto* t = static_cast<SgdTask*>(u);
+  *out = t->cfg.total_steps > 0 && done >= t->cfg.total_steps;
+  return FR_OK;
+}
+
+void sgd_task_destroy(void* u) {
+  auto* t = static_cast<SgdTask*>(u);
+  cudaDeviceSynchronize();
+  fr_sgd_problem_destroy(t->p);
+  delete t;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fr_sgd_task_create(const fr_sgd_task_config* c, fr_side_task_vtable* vt, void** user) {
+  if (!c || !vt || !user) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  if (c->edges_per_step < 1 || c->E < 1)
+    return frcapi::fail(FR_ERR_VALIDATION, "E and edges_per_step must be >= 1", "edges_per_step");
+  auto* t = new SgdTask;
+  t->cfg = *c;
+  const int rc = sgd_task_create(t);
+  if (rc != FR_OK) {
+    delete t;
+    return rc;
+  }
+  std::memset(vt, 0, sizeof(*vt));
+  vt->create = sgd_task_create;
+  vt->init = sgd_task_init;
+  vt->run_next_step = sgd_task_step;
+  vt->finished = sgd_task_finished;
+  vt->destroy = sgd_task_destroy;
+  vt->work_units_per_step = static_cast<double>(c->edges_per_step);  // edges
+  *user = t;
+  return FR_OK;
+}
+
+int fr_sgd_task_problem(void* user, fr_sgd_problem** p, int64_t* epochs_done) {
+  auto* t = static_cast<SgdTask*>(user);
+  if (!t) return frcapi::fail(FR_ERR_ARGUMENT, "null task");
+  if (p) *p = t->p;
+  if (epochs_done) *epochs_done = t->epochs;
+  return FR_OK;
+}
+
+}  // extern "C"

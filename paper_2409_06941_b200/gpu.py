@@ -224,6 +224,76 @@ class PageRankTask:
         return _dev_copy(p.value, self.V, torch.float32), it.value
 
 
+class SgdProblem:
+    """fr_sgd_problem: rating graph + fp32 latent matrix on the device."""
+
+    def __init__(self, V=3072441, E=117185083, k=16, edge_seed=2, init_seed=3, stream=None,
+                 handle=None):
+        self._owned = handle is None
+        if handle is None:
+            handle = C.c_void_p()
+            check(glib().fr_sgd_problem_generate(V, E, k, edge_seed, init_seed, _stream(stream),
+                                                 C.byref(handle)))
+        self._h = handle
+        u, v, r, L = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p()
+        Vc, Ec, kc = C.c_int32(), C.c_int64(), C.c_int32()
+        check(glib().fr_sgd_buffers(self._h, C.byref(u), C.byref(v), C.byref(r), C.byref(L),
+                                    C.byref(Vc), C.byref(Ec), C.byref(kc)))
+        self.V, self.E, self.k = Vc.value, Ec.value, kc.value
+        self._ptr = dict(u=u.value, v=v.value, r=r.value, L=L.value)
+
+    def reinit(self, seed=3, stream=None):
+        check(glib().fr_sgd_reinit(self._h, seed, _stream(stream)))
+
+    def step(self, e_begin, e_end, eta=0.01, lam=0.05, stream=None):
+        check(glib().fr_sgd_step(self._h, e_begin, e_end, eta, lam, _stream(stream)))
+
+    def epoch(self, eta=0.01, lam=0.05, stream=None):
+        self.step(0, self.E, eta, lam, stream)
+
+    def rmse(self, stream=None) -> float:
+        out = C.c_double()
+        check(glib().fr_sgd_rmse(self._h, _stream(stream), C.byref(out)))
+        return out.value
+
+    def edges(self):
+        torch.cuda.synchronize()
+        return (_dev_copy(self._ptr["u"], self.E, torch.int32), _dev_copy(self._ptr["v"], self.E, torch.int32),
+                _dev_copy(self._ptr["r"], self.E, torch.float32))
+
+    def latent(self):
+        torch.cuda.synchronize()
+        return _dev_copy(self._ptr["L"], self.V * self.k, torch.float32).view(self.V, self.k)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if self._owned and h is not None and h.value and _glib is not None:
+            _glib.fr_sgd_problem_destroy(h)
+            self._h = None
+
+
+class SgdTask:
+    """Built-in Graph-SGD side task (fr_sgd_task_create)."""
+
+    def __init__(self, V=3072441, E=117185083, k=16, edge_seed=2, init_seed=3,
+                 edges_per_step=1 << 21, eta=0.01, lam=0.05, total_steps=0):
+        self.cfg = A.SgdTaskConfigC(V=V, k=k, E=E, edge_seed=edge_seed, init_seed=init_seed,
+                                    edges_per_step=edges_per_step, eta=eta, lambda_=lam,
+                                    total_steps=total_steps)
+        self.vt = A.SideTaskVTableC()
+        self.user = C.c_void_p()
+        check(glib().fr_sgd_task_create(C.byref(self.cfg), C.byref(self.vt), C.byref(self.user)))
+        self.memory_gib = (E * 12 + V * k * 4) / 2 ** 30
+        self.units_per_step = self.vt.work_units_per_step
+        self.bytes_per_step = edges_per_step * (12 + 4 * 4 * k)   # 268 B/edge at k = 16
+        self.h2d_per_step = self.d2h_per_step = 0
+
+    def problem(self):
+        p, ep = C.c_void_p(), C.c_int64()
+        check(glib().fr_sgd_task_problem(self.user, C.byref(p), C.byref(ep)))
+        return SgdProblem(handle=p), ep.value
+
+
 class PythonTask:
     """A side task written in Python (the paper's Python interface,
     PAPER.md:484-499): override the transition hooks; `run_next_step`
