@@ -3,7 +3,7 @@
  * hot path (FreeRide, arXiv 2409.06941).
  *
  * Every entry point below replaces one function of the reference's C++ API
- * (`bubblesim`, /root/reference/proj/include/bubblesim/*.hpp); the cited
+ * (`bubblesim`, /root/reference/proj/include/bubblesim/<module>.hpp); the cited
  * file:line is the declaration it stands in for.  The rules of the boundary:
  *
  *   - no exceptions cross it: every call returns an int status (FR_OK = 0);
@@ -393,6 +393,49 @@ typedef struct fr_breakdown_input {
   int64_t n_activities;
   const fr_activity_record* activities;
 } fr_breakdown_input;
+
+/* ------------------------------------------------------------ engine (L5) */
+typedef struct fr_runtime_options {  /* RuntimeOptions  config.hpp:19-27 */
+  fr_tick check_overhead;
+  fr_tick rpc_latency;
+  double step_jitter;
+  int32_t profile_steps;
+  int32_t gate_estimate;             /* 0 mean, 1 max (GateEstimate config.hpp:17) */
+} fr_runtime_options;
+
+typedef struct fr_experiment_config { /* ExperimentConfig config.hpp:36-46 */
+  fr_pipeline_config pipeline;
+  const fr_side_task_spec* tasks;
+  int32_t n_tasks;
+  int32_t reserved;
+  fr_limit_config limits;
+  fr_runtime_options runtime;
+} fr_experiment_config;
+
+typedef struct fr_run_trace fr_run_trace; /* RunTrace engine.hpp:75-92 */
+
+typedef struct fr_run_trace_counts {
+  int64_t ops, bubbles, submits, assigns, rejects, rpcs, transitions, activities, kills,
+      dispositions;
+  fr_tick makespan;
+} fr_run_trace_counts;
+
+/* run_experiment  engine.hpp:97-98 (declared, never implemented by the
+ * reference; rules in DESIGN.md §6).  Deterministic in (config, with_tasks, seed). */
+int fr_run_experiment(const fr_experiment_config* cfg, int32_t with_tasks, uint64_t seed,
+                      fr_run_trace** out);
+void fr_run_trace_destroy(fr_run_trace* t);
+int fr_run_trace_get_counts(const fr_run_trace* t, fr_run_trace_counts* out);
+int fr_run_trace_ops(const fr_run_trace* t, fr_op_event* out, int64_t cap);
+int fr_run_trace_bubbles(const fr_run_trace* t, fr_bubble* out, int64_t cap);
+/* which: 0 submits, 1 assigns, 2 rejects */
+int fr_run_trace_assigns(const fr_run_trace* t, int32_t which, fr_assign_record* out, int64_t cap);
+/* which: 0 transitions, 1 rpcs */
+int fr_run_trace_transitions(const fr_run_trace* t, int32_t which, fr_transition_record* out,
+                             int64_t cap);
+int fr_run_trace_activities(const fr_run_trace* t, fr_activity_record* out, int64_t cap);
+int fr_run_trace_kills(const fr_run_trace* t, fr_kill_record* out, int64_t cap);
+int fr_run_trace_dispositions(const fr_run_trace* t, fr_disposition_record* out, int64_t cap);
 
 /* time_increase  metrics.hpp:25 */
 int fr_time_increase(double t_no_seconds, double t_with_seconds, double* out);

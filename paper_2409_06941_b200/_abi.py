@@ -310,6 +310,23 @@ class BreakdownInputC(Struct):
     ]
 
 
+class RuntimeOptionsC(Struct):
+    _fields_ = [("check_overhead", tick), ("rpc_latency", tick), ("step_jitter", C.c_double),
+                ("profile_steps", C.c_int32), ("gate_estimate", C.c_int32)]
+
+
+class ExperimentConfigC(Struct):
+    _fields_ = [("pipeline", PipelineConfigC), ("tasks", C.POINTER(SideTaskSpecC)),
+                ("n_tasks", C.c_int32), ("reserved", C.c_int32), ("limits", LimitConfigC),
+                ("runtime", RuntimeOptionsC)]
+
+
+class RunTraceCountsC(Struct):
+    _fields_ = [(n, C.c_int64) for n in ("ops", "bubbles", "submits", "assigns", "rejects", "rpcs",
+                                         "transitions", "activities", "kills", "dispositions")] + \
+               [("makespan", tick)]
+
+
 LOOKUP_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_char_p, C.POINTER(TaskViewC))
 
 P = C.POINTER
@@ -352,6 +369,21 @@ HOST_PROTOTYPES = {
     "fr_time_increase": (C.c_int, [dbl, dbl, P(dbl)]),
     "fr_cost_savings": (C.c_int, [dbl, dbl, P(TaskWorkC), i32, P(PriceConfigC), P(CostBreakdownC)]),
     "fr_bubble_breakdown": (C.c_int, [P(BreakdownInputC), P(StageBreakdownC)]),
+}
+
+
+# the engine rows (the reference declares run_experiment but has no .cpp)
+ENGINE_PROTOTYPES = {
+    "fr_run_experiment": (C.c_int, [P(ExperimentConfigC), i32, u64, P(vp)]),
+    "fr_run_trace_destroy": (None, [vp]),
+    "fr_run_trace_get_counts": (C.c_int, [vp, P(RunTraceCountsC)]),
+    "fr_run_trace_ops": (C.c_int, [vp, P(OpEventC), i64]),
+    "fr_run_trace_bubbles": (C.c_int, [vp, P(BubbleC), i64]),
+    "fr_run_trace_assigns": (C.c_int, [vp, i32, P(AssignRecordC), i64]),
+    "fr_run_trace_transitions": (C.c_int, [vp, i32, P(TransitionRecordC), i64]),
+    "fr_run_trace_activities": (C.c_int, [vp, P(ActivityRecordC), i64]),
+    "fr_run_trace_kills": (C.c_int, [vp, P(KillRecordC), i64]),
+    "fr_run_trace_dispositions": (C.c_int, [vp, P(DispositionRecordC), i64]),
 }
 
 

@@ -431,6 +431,63 @@ class BubbleSim:
 
     def __init__(self, lib: C.CDLL):
         self.lib = A.bind(lib, A.HOST_PROTOTYPES)
+        self.has_engine = hasattr(lib, "fr_run_experiment")
+        if self.has_engine:
+            A.bind(lib, A.ENGINE_PROTOTYPES)
+
+    # ----------------------------------------------------------- engine.hpp
+    def run_experiment(self, cfg: PipelineConfig, tasks: Sequence[SideTaskSpec], seed: int,
+                       with_tasks: bool = True, check_overhead: int = 1, rpc_latency: int = 0,
+                       step_jitter: float = 0.0, profile_steps: int = 32, gate_max: bool = False,
+                       limits: LimitConfig = LimitConfig()) -> dict:  # engine.hpp:97-98
+        """RunTrace as plain tuples: ops (stage, kind, mb, epoch, start, end);
+        bubbles (stage, epoch, start, duration, avail, btype); submits/assigns/
+        rejects (t, task, worker); rpcs/transitions (t, task, kind, worker);
+        activities (start, end, task, worker, kind, clipped); kills
+        (t, task, worker, reason); dispositions (task, disposition, steps, worker)."""
+        if not self.has_engine:
+            raise FreeRideError("library has no engine (the reference declares run_experiment only)")
+        c = _Cfg(cfg)
+        arr = (A.SideTaskSpecC * max(1, len(tasks)))(*[_spec_c(t) for t in tasks])
+        ec = A.ExperimentConfigC(pipeline=c.c, tasks=arr, n_tasks=len(tasks),
+                                 limits=A.LimitConfigC(limits.grace_period, limits.memory_headroom,
+                                                       limits.reclamation_delay),
+                                 runtime=A.RuntimeOptionsC(check_overhead, rpc_latency, step_jitter,
+                                                           profile_steps, int(gate_max)))
+        h = C.c_void_p()
+        self._check(self.lib.fr_run_experiment(C.byref(ec), int(with_tasks), seed, C.byref(h)))
+        try:
+            n = A.RunTraceCountsC()
+            self._check(self.lib.fr_run_trace_get_counts(h, C.byref(n)))
+
+            def get(fn, ctype, count, *pre):
+                buf = (ctype * max(1, count))()
+                self._check(fn(h, *pre, buf, count))
+                return [buf[i] for i in range(count)]
+
+            out = {"makespan": n.makespan}
+            out["ops"] = [(o.stage, o.kind, o.micro_batch, o.epoch, o.start, o.end)
+                          for o in get(self.lib.fr_run_trace_ops, A.OpEventC, n.ops)]
+            out["bubbles"] = [(b.stage, b.epoch, b.start, b.duration, b.available_memory, b.btype)
+                              for b in get(self.lib.fr_run_trace_bubbles, A.BubbleC, n.bubbles)]
+            for name, which, cnt in (("submits", 0, n.submits), ("assigns", 1, n.assigns),
+                                     ("rejects", 2, n.rejects)):
+                out[name] = [(r.t, r.task.decode(), r.worker)
+                             for r in get(self.lib.fr_run_trace_assigns, A.AssignRecordC, cnt, which)]
+            for name, which, cnt in (("transitions", 0, n.transitions), ("rpcs", 1, n.rpcs)):
+                out[name] = [(r.t, r.task.decode(), r.kind, r.worker)
+                             for r in get(self.lib.fr_run_trace_transitions, A.TransitionRecordC, cnt, which)]
+            out["activities"] = [(a.start, a.end, a.task.decode(), a.worker, a.kind, bool(a.clipped))
+                                 for a in get(self.lib.fr_run_trace_activities, A.ActivityRecordC, n.activities)]
+            out["kills"] = [(k.t, k.task.decode(), k.worker, k.reason)
+                            for k in get(self.lib.fr_run_trace_kills, A.KillRecordC, n.kills)]
+            out["dispositions"] = [(d.task.decode(), d.disposition, d.steps_completed,
+                                    d.worker if d.has_worker else None)
+                                   for d in get(self.lib.fr_run_trace_dispositions, A.DispositionRecordC,
+                                                n.dispositions)]
+            return out
+        finally:
+            self.lib.fr_run_trace_destroy(h)
 
     def _check(self, rc: int):
         A.raise_for(self.lib, rc)

@@ -342,6 +342,44 @@ struct BreakdownInput {
   std::vector<ActivityRecord> activities;
 };
 
+// ---------------------------------------------------------------- engine.hpp
+enum class GateEstimate { Mean = 0, Max = 1 };  // config.hpp:17
+
+struct RuntimeOptions {  // config.hpp:19-27
+  Tick check_overhead = 1;
+  Tick rpc_latency = 0;
+  double step_jitter = 0.0;
+  int profile_steps = 32;
+  GateEstimate gate_estimate = GateEstimate::Mean;
+};
+
+struct ExperimentConfig {  // config.hpp:36-46 (JSON, prices and sweep out of scope)
+  PipelineConfig pipeline;
+  std::vector<SideTaskSpec> tasks;
+  LimitConfig limits;
+  RuntimeOptions runtime;
+  std::uint64_t seed = 0;
+};
+
+struct RunTrace {  // engine.hpp:75-92
+  std::vector<OpEvent> ops;
+  std::vector<Bubble> bubbles;            // as signalled on the delayed timeline
+  std::vector<AssignRecord> submits;      // worker -1
+  std::vector<AssignRecord> assigns;
+  std::vector<AssignRecord> rejects;      // worker -1
+  std::vector<RpcRecord> rpcs;
+  std::vector<TransitionRecord> transitions;
+  std::vector<ActivityRecord> activities;
+  std::vector<KillRecord> kills;
+  std::vector<DispositionRecord> dispositions;
+  std::vector<TaskProfile> profiles;
+  Tick makespan = 0;
+};
+
+// engine.hpp:97-98 -- the reference declares it and never implements it; the
+// rules are SURVEY.md Appendix B with the ambiguities fixed in DESIGN.md §6.
+RunTrace run_experiment(const ExperimentConfig& config, bool with_tasks, std::uint64_t seed);
+
 double time_increase(double t_no_seconds, double t_with_seconds);
 CostBreakdown cost_savings(double t_no_seconds, double delta_t, const std::vector<TaskWork>& work,
                            const PriceConfig& prices);
