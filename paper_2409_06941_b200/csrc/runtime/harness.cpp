@@ -409,10 +409,6 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
   std::int64_t launched = 0, completed = 0, pauses = 0, kills = 0;
   double dispatch_ns = 0;
   std::int64_t next_slot = 0;
-  const double step_units = [&] {
-    for (auto& kv : tasks) return kv.second->vt.work_units_per_step;
-    return 0.0;
-  }();
   double units = 0;
   const int depth = std::max(1, cfg.max_inflight_steps);
 
@@ -431,7 +427,7 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
       Task* st = steps[inflight.front()].task;
       inflight.pop_front();
       ++completed;
-      units += step_units;
+      units += st->vt.work_units_per_step;  // the completing step's own task
       st->rt.steps_completed++;  // counted at step end (task.hpp:55)
       // Re-anchor the projection: the next queued step started when this one
       // ended (~now), so drift from mis-estimated step times cannot build up.

@@ -65,3 +65,21 @@ def test_rejected_when_memory_does_not_fit(g):
     ok_big, _ = h.submit("big", g.ImageTask(batch=256, images_per_step=8), profile_steps=4)
     assert ok_small and not ok_big
     h.close()
+
+
+def test_work_units_credit_the_completing_task(g):
+    """Several tasks over one harness's life: each run credits its own task's units."""
+    h = small_harness(g, stage=1)
+    a = g.ImageTask(batch=8, images_per_step=4)
+    ok, _ = h.submit("a_img4", a, profile_steps=4)
+    h.run(2, True)
+    r = h.run(2, True)
+    assert r["work_units"] == r["steps_completed"] * 4 * 1920 * 1080
+    h.stop_task("a_img4")
+    b = g.ImageTask(batch=8, images_per_step=1)
+    ok, _ = h.submit("b_img1", b, profile_steps=4)
+    h.run(2, True)
+    r = h.run(2, True)
+    assert r["steps_completed"] > 0
+    assert r["work_units"] == r["steps_completed"] * 1920 * 1080
+    h.close()
