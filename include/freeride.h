@@ -289,6 +289,9 @@ int fr_manager_worker_info(const fr_manager* mgr, int32_t worker, fr_worker_info
 /* i-th queued task id (0 = front, earliest submitted) */
 int fr_manager_queue_at(const fr_manager* mgr, int32_t worker, int32_t i, char* buf,
                         int32_t cap);
+/* mirror a remote worker's queue (distributed Alg. 1: every rank rebuilds the
+ * gathered WorkerStates and runs the same deterministic select_worker) */
+int fr_manager_push_task(fr_manager* mgr, int32_t worker, const char* task_id);
 /* engine housekeeping (Appendix B rule 8): clear or set CurrentTask */
 int fr_manager_set_current_task(fr_manager* mgr, int32_t worker, const char* task_id_or_null);
 /* select_worker  manager.hpp:33 ; *worker = -1 when none qualifies */
@@ -393,6 +396,24 @@ typedef struct fr_breakdown_input {
   int64_t n_activities;
   const fr_activity_record* activities;
 } fr_breakdown_input;
+
+/* ---------------------------------------- pipeline P2P plan (multi-GPU) */
+/* One point-to-point operation of stage `stage`'s 1F1B loop (not in the
+ * reference, which simulates stages on one timeline): at op
+ * boundary `group` (0..2m; group g sits before op g, after op g-1) the stage
+ * sends op g-1's output and receives op g's input in ONE send/recv group
+ * (ncclGroupStart/End).  Pairing the two in one group is what keeps 1F1B
+ * deadlock-free under rendezvous semantics (tests/test_p2p_plan.py). */
+typedef struct fr_p2p_op {
+  int32_t group;     /* op boundary index, 0..2m */
+  int32_t is_send;   /* 1 send, 0 recv */
+  int32_t peer;      /* stage +-1 */
+  int32_t kind;      /* FR_OP_FP: activation, FR_OP_BP: gradient */
+  int32_t micro_batch;
+} fr_p2p_op;
+/* ops in execution order; cap >= 4*m always suffices */
+int fr_pipeline_p2p_plan(int32_t stage, int32_t num_stages, int32_t num_micro_batches,
+                         fr_p2p_op* out, int64_t cap, int64_t* n_out);
 
 /* ------------------------------------------------------------ engine (L5) */
 typedef struct fr_runtime_options {  /* RuntimeOptions  config.hpp:19-27 */

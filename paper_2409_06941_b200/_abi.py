@@ -372,8 +372,14 @@ HOST_PROTOTYPES = {
 }
 
 
+class P2POpC(Struct):
+    _fields_ = [("group", i32), ("is_send", i32), ("peer", i32), ("kind", i32), ("micro_batch", i32)]
+
+
 # the engine rows (the reference declares run_experiment but has no .cpp)
 ENGINE_PROTOTYPES = {
+    "fr_pipeline_p2p_plan": (C.c_int, [i32, i32, i32, P(P2POpC), i64, P(i64)]),
+    "fr_manager_push_task": (C.c_int, [vp, i32, cp]),
     "fr_run_experiment": (C.c_int, [P(ExperimentConfigC), i32, u64, P(vp)]),
     "fr_run_trace_destroy": (None, [vp]),
     "fr_run_trace_get_counts": (C.c_int, [vp, P(RunTraceCountsC)]),

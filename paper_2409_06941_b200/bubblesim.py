@@ -421,6 +421,10 @@ class WorkerStates:
         i = self.info(w)
         return len(i["task_queue"]) + (1 if i["current_task"] is not None else 0)
 
+    def push_task(self, w: int, task_id: str):
+        """Mirror a (remote) worker's queued task (distributed Alg. 1)."""
+        self._api._check(self._lib.fr_manager_push_task(self._h, w, _id(task_id)))
+
     def set_current_task(self, w: int, task_id: Optional[str]):
         self._api._check(self._lib.fr_manager_set_current_task(
             self._h, w, None if task_id is None else _id(task_id)))
@@ -434,6 +438,15 @@ class BubbleSim:
         self.has_engine = hasattr(lib, "fr_run_experiment")
         if self.has_engine:
             A.bind(lib, A.ENGINE_PROTOTYPES)
+
+    def pipeline_p2p_plan(self, stage: int, num_stages: int, m: int):
+        """[(group, is_send, peer, kind, micro_batch)] of one stage's 1F1B loop."""
+        cap = 4 * max(m, 1) + 4
+        buf = (A.P2POpC * cap)()
+        n = C.c_int64()
+        self._check(self.lib.fr_pipeline_p2p_plan(stage, num_stages, m, buf, cap, C.byref(n)))
+        return [(b.group, bool(b.is_send), b.peer, OpKind(b.kind), b.micro_batch)
+                for b in buf[:n.value]]
 
     # ----------------------------------------------------------- engine.hpp
     def run_experiment(self, cfg: PipelineConfig, tasks: Sequence[SideTaskSpec], seed: int,

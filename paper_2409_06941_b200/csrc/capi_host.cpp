@@ -182,6 +182,20 @@ int fr_default_stage_memory(int32_t p, double total, double w, double a, double*
   });
 }
 
+int fr_pipeline_p2p_plan(int32_t stage, int32_t p, int32_t m, fr_p2p_op* out, int64_t cap,
+                         int64_t* n_out) {
+  if (!n_out) return frcapi::fail(FR_ERR_ARGUMENT, "null count");
+  return frcapi::guard([&]() -> int {
+    const auto plan = pipeline_p2p_plan(stage, p, m);
+    *n_out = static_cast<int64_t>(plan.size());
+    if (*n_out > cap) return frcapi::fail(FR_ERR_CAPACITY, "p2p plan needs up to 4*m entries");
+    for (std::size_t i = 0; i < plan.size(); ++i)
+      out[i] = fr_p2p_op{plan[i].group, plan[i].is_send ? 1 : 0, plan[i].peer,
+                         static_cast<int32_t>(plan[i].kind), plan[i].micro_batch};
+    return FR_OK;
+  });
+}
+
 int fr_side_task_validate(const fr_side_task_spec* spec, const char* path) {
   return frcapi::guard([&]() -> int {
     spec_in(spec).validate(path ? path : "");
@@ -339,6 +353,13 @@ int fr_manager_queue_at(const fr_manager* m, int32_t w, int32_t i, char* buf, in
   const std::string& id = ws->task_queue[static_cast<std::size_t>(i)];
   if (static_cast<int32_t>(id.size()) + 1 > cap) return frcapi::fail(FR_ERR_CAPACITY, "id buffer");
   std::memcpy(buf, id.c_str(), id.size() + 1);
+  return FR_OK;
+}
+
+int fr_manager_push_task(fr_manager* m, int32_t w, const char* id) {
+  WorkerState* ws = worker_of(m, w);
+  if (!ws || !id) return frcapi::fail(FR_ERR_NOT_FOUND, "no such worker / null id");
+  ws->task_queue.push_back(id_in(id));
   return FR_OK;
 }
 

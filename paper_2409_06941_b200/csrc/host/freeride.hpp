@@ -110,6 +110,18 @@ double bubble_rate(int num_stages, const OpEvent* ops, std::size_t n_ops, const 
 std::vector<double> default_stage_memory(int num_stages, double gpu_memory_total,
                                          double weight_mem, double activation_mem);
 
+// Point-to-point plan of one stage's 1F1B loop for a real multi-GPU pipeline
+// (fr_p2p_op in freeride.h): group g precedes op g and pairs op g-1's send
+// with op g's receive.
+struct P2POp {
+  int group;
+  bool is_send;
+  int peer;
+  OpKind kind;  // FP: activation, BP: gradient
+  int micro_batch;
+};
+std::vector<P2POp> pipeline_p2p_plan(int stage, int num_stages, int num_micro_batches);
+
 // ----------------------------------------------------------------- task.hpp
 enum class SideTaskState { Submitted = 0, Created = 1, Paused = 2, Running = 3, Stopped = 4 };
 enum class TransitionKind {

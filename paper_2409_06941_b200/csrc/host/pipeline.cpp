@@ -290,3 +290,32 @@ std::vector<double> default_stage_memory(int p, double total, double w, double a
 }
 
 }  // namespace freeride
+
+namespace freeride {
+
+// 1F1B point-to-point plan of one stage (see freeride.h fr_p2p_op): group g
+// (0..2m) precedes op g; it sends op g-1's output (FP -> stage+1 activation,
+// BP -> stage-1 gradient) and receives op g's input (FP <- stage-1, BP <-
+// stage+1).  Send first, then recv, inside one group.
+std::vector<P2POp> pipeline_p2p_plan(int stage, int p, int m) {
+  if (p < 1 || m < 1 || stage < 0 || stage >= p)
+    throw ValidationError("stage", "need 0 <= stage < num_stages and m >= 1");
+  const auto order = stage_issue_order(stage, p, m);
+  std::vector<P2POp> plan;
+  const int n = static_cast<int>(order.size());
+  for (int g = 0; g <= n; ++g) {
+    if (g > 0) {
+      const auto [k, mb] = order[g - 1];
+      if (k == OpKind::FP && stage + 1 < p) plan.push_back({g, true, stage + 1, OpKind::FP, mb});
+      if (k == OpKind::BP && stage > 0) plan.push_back({g, true, stage - 1, OpKind::BP, mb});
+    }
+    if (g < n) {
+      const auto [k, mb] = order[g];
+      if (k == OpKind::FP && stage > 0) plan.push_back({g, false, stage - 1, OpKind::FP, mb});
+      if (k == OpKind::BP && stage + 1 < p) plan.push_back({g, false, stage + 1, OpKind::BP, mb});
+    }
+  }
+  return plan;
+}
+
+}  // namespace freeride

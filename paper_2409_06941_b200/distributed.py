@@ -1,0 +1,80 @@
+"""Multi-GPU plumbing: one process per GPU (torch.distributed), one pipeline
+stage and one side-task worker per GPU.
+
+* Side tasks shard as replicas: no collective on their data path.
+* Alg. 1 placement is the only cross-rank decision: every rank all-gathers
+  the workers' (GPUMem, task count), rebuilds the same WorkerStates and runs
+  the product's deterministic `select_worker` -- identical answer on every
+  rank, no broadcast needed; only the chosen rank submits the task to its
+  local harness.
+* The pipeline's exchange (activations forward, gradients backward) follows
+  `pipeline_p2p_plan`: at each op boundary the stage posts op g-1's send and
+  op g's receive as one group (NCCL group / batch_isend_irecv), which keeps
+  1F1B deadlock-free (tests/test_p2p_plan.py).
+"""
+from __future__ import annotations
+
+from typing import Callable, List, Optional, Sequence, Tuple
+
+import torch
+import torch.distributed as dist
+
+from .bubblesim import BubbleSim, OpKind, TaskProfile
+
+
+def gather_workers(gpu_mem: float, task_count: int, group=None) -> List[Tuple[float, int]]:
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, (float(gpu_mem), int(task_count)), group=group)
+    return out
+
+
+def select_worker_global(api: BubbleSim, task_memory: float,
+                         workers: Sequence[Tuple[float, int]]) -> Optional[int]:
+    """Alg. 1 (manager.cpp:5-19 semantics) over gathered worker states."""
+    ws = api.workers([m for m, _ in workers])
+    for w, (_, count) in enumerate(workers):
+        for i in range(count):
+            ws.push_task(w, f"~{w}.{i}")
+    return api.select_worker(task_memory, ws)
+
+
+def submit_collective(api: BubbleSim, profile: TaskProfile, local_gpu_mem: float,
+                      local_task_count: int, group=None) -> Optional[int]:
+    """Collective Alg. 1: returns the chosen rank (same on all ranks) or None."""
+    return select_worker_global(api, profile.est_memory,
+                                gather_workers(local_gpu_mem, local_task_count, group))
+
+
+def run_p2p_plan(api: BubbleSim, m: int, compute: Callable[[OpKind, int, Optional[torch.Tensor]], torch.Tensor],
+                 make_buffer: Callable[[], torch.Tensor], group=None) -> List[Tuple[OpKind, int]]:
+    """Executes this rank's stage of a 1F1B pipeline with the product's P2P
+    plan: for each op g (issue order) post group g (send op g-1's output,
+    receive op g's input) and wait, then run `compute(kind, mb, input)`.
+    Returns the executed op order."""
+    rank, p = dist.get_rank(group), dist.get_world_size(group)
+    plan = api.pipeline_p2p_plan(rank, p, m)
+    order = api.stage_issue_order(rank, p, m)
+    outputs = {}
+    done = []
+    for g in range(len(order) + 1):
+        ops, recv_buf = [], None
+        for (grp, is_send, peer, kind, mb) in plan:
+            if grp != g:
+                continue
+            if is_send:
+                ops.append(dist.P2POp(dist.isend, outputs.pop((kind, mb)), peer, group))
+            else:
+                recv_buf = make_buffer()
+                ops.append(dist.P2POp(dist.irecv, recv_buf, peer, group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        if g < len(order):
+            kind, mb = order[g]
+            out = compute(kind, mb, recv_buf)
+            sends_out = (kind == OpKind.FP and rank + 1 < p) or (kind == OpKind.BP and rank > 0)
+            if sends_out:
+                outputs[(kind, mb)] = out
+            done.append((kind, mb))
+    assert not outputs, "every produced tensor must have been sent"
+    return done
