@@ -45,7 +45,8 @@ sys.path.insert(0, ROOT)
 
 STAGES = 4
 MICRO_BATCHES = 4
-SHAPE = dict(layers=6, hidden=2048, tokens=8192, ffn_mult=4)
+SHAPE = dict(layers=6, hidden=2048, tokens=8192, ffn_mult=4)        # nanoGPT-1.2B / 4 stages
+SHAPE_36B = dict(layers=9, hidden=2880, tokens=8192, ffn_mult=4)    # nanoGPT-3.6B / 4 stages
 FRAMES = dict(sw=3840, sh=2160, dw=1920, dh=1080)
 BATCH = 64
 IMAGES_PER_STEP = 8
@@ -252,6 +253,40 @@ def ours(args):
                             "fill_image": runs["image"][s]["with"]["used_s"] / runs["image"][s]["with"]["bubble_s"],
                             "breakdown_image": runs["image"][s]["with"]["breakdown"]}
                            for s, p in enumerate(stage_prof)]
+    # configs[3]: mixed side tasks over a 3.6B-shaped pipeline, placed by Alg. 1
+    mixed = None
+    if not args.no_mixed:
+        from paper_2409_06941_b200 import api as host_api
+        a = host_api()
+        probe = gpu.Harness(num_stages=STAGES, num_micro_batches=MICRO_BATCHES, stage=0,
+                            profile_epochs=0, profile_reps=1, **SHAPE_36B)
+        avail = [probe.profile()["available_memory"]]
+        probe.close()
+        specs = [("pagerank", lambda: gpu.PageRankTask(**PR)), ("sgd", lambda: gpu.SgdTask(**SGD)),
+                 ("image", lambda: gpu.ImageTask(batch=BATCH, images_per_step=IMAGES_PER_STEP, **FRAMES)),
+                 ("pagerank2", lambda: gpu.PageRankTask(**PR))]
+        from paper_2409_06941_b200.bubblesim import TaskProfile
+        mem = {"pagerank": 0.3, "pagerank2": 0.3, "sgd": 1.6, "image": 2.2}
+        wstates = a.workers([avail[0]] * STAGES)   # replica: every stage sees its own GPU's memory
+        placement = {}
+        for name, _ in specs:
+            o = a.submit_task(TaskProfile(name, 1e-4, 1e-4, mem[name], 32), wstates)
+            placement[name] = o.worker_id if o.assigned else None
+        mixed = {"placement": placement, "stages": []}
+        for name, make in specs:
+            s = placement[name]
+            if s is None:
+                continue
+            h = gpu.Harness(num_stages=STAGES, num_micro_batches=MICRO_BATCHES, stage=s, **SHAPE_36B)
+            r = harvest(h, name, make(), K, W)
+            h.close()
+            mixed["stages"].append({"stage": s, "task": name, "units_per_bubble_s": r["with"]["work_units"] / r["base"]["bubble_s"],
+                                    "unit": "px" if name == "image" else "edges",
+                                    "dT": (r["with"]["makespan_s"] - r["base"]["makespan_s"]) / r["base"]["makespan_s"],
+                                    "fill": r["with"]["used_s"] / r["with"]["bubble_s"]})
+        mixed["dT_max"] = max(x["dT"] for x in mixed["stages"])
+        mixed["fill_mean"] = statistics.fmean(x["fill"] for x in mixed["stages"])
+    local_res["mixed"] = mixed
     csr = None
     if rank == 0 and not args.no_cpu:
         g = gpu.PageRankGraph(scale=PR["scale"], edge_factor=PR["edge_factor"], seed=PR["seed"])
@@ -340,6 +375,10 @@ def emit(args, results, ws, names, csr):
         "roofline": image_roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": results[0]["clocks"],
         "gpu_launches": launches, "workloads": workloads, "stages": results[0]["stages"],
     }
+    if results[0].get("mixed"):
+        workloads["mixed"] = dict(results[0]["mixed"],
+                                  config="configs[3]: PageRank + SGD + Image + PageRank on a "
+                                         "nanoGPT-3.6B-shaped 4-stage pipeline, placed by Alg. 1")
     print(json.dumps(line), flush=True)
 
 
@@ -376,6 +415,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-mixed", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

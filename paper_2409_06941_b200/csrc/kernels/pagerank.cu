@@ -173,16 +173,20 @@ __global__ void __launch_bounds__(kPrThreads) pr_binned_kernel(PrArgs a) {
     e = a.offsets[row] + sub;
     e1 = a.offsets[row + 1];
   }
+  // Predicated 4-wide chunks: all four col_idx loads, then all four gathers,
+  // are in flight together even for rows shorter than 4 x lanes (the common
+  // case), i.e. two dependent L2 round trips per chunk, not two per edge.
   double s0 = 0.0, s1 = 0.0;
-  for (; e + 3 * lanes < e1; e += 4 * lanes) {
-    const int32_t u0 = __ldg(&a.col[e]), u1 = __ldg(&a.col[e + lanes]);
-    const int32_t u2 = __ldg(&a.col[e + 2 * lanes]), u3 = __ldg(&a.col[e + 3 * lanes]);
-    const float c0 = __ldg(&a.c_in[u0]), c1 = __ldg(&a.c_in[u1]);
-    const float c2 = __ldg(&a.c_in[u2]), c3 = __ldg(&a.c_in[u3]);
-    s0 += static_cast<double>(c0) + static_cast<double>(c1);
-    s1 += static_cast<double>(c2) + static_cast<double>(c3);
+  for (; e < e1; e += 4 * lanes) {
+    int32_t u[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) u[j] = e + j * lanes < e1 ? __ldg(&a.col[e + j * lanes]) : -1;
+    float c[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) c[j] = u[j] >= 0 ? __ldg(&a.c_in[u[j]]) : 0.0f;
+    s0 += static_cast<double>(c[0]) + static_cast<double>(c[1]);
+    s1 += static_cast<double>(c[2]) + static_cast<double>(c[3]);
   }
-  for (; e < e1; e += lanes) s0 += __ldg(&a.c_in[__ldg(&a.col[e])]);
   double s = s0 + s1;
   for (int o = lanes >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if (sub == 0 && row >= 0) {

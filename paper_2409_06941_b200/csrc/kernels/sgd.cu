@@ -17,6 +17,7 @@
 // 268 B/edge algorithmic.  Each lane carries two edges per iteration to keep
 // enough 64 B requests in flight.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "freeride_gpu.h"
@@ -25,6 +26,7 @@
 namespace {
 
 constexpr int kSgdThreads = 256;
+constexpr int kSgdDefaultMinBlocks = 1;
 constexpr uint64_t kSgdPermMul = 2654435761ull;
 
 __device__ __forceinline__ int32_t sgd_vertex(uint64_t h, int32_t V) {
@@ -90,8 +92,9 @@ __device__ __forceinline__ void deltas(const float4& a, const float4& b, float e
 __device__ __forceinline__ void apply(float4* p, const float4& d) { atomicAdd(p, d); }
 
 // Each lane group handles edges g, g + G, g + 2G, ... two at a time.
-template <int K>
-__global__ void __launch_bounds__(kSgdThreads) sgd_step_kernel(
+// MINB: CTAs per SM the register allocation must allow (occupancy vs ILP).
+template <int K, int MINB>
+__global__ void __launch_bounds__(kSgdThreads, MINB) sgd_step_kernel(
     const int32_t* __restrict__ us, const int32_t* __restrict__ vs, const float* __restrict__ rs,
     float* __restrict__ L, int64_t e0, int64_t e1, float eta, float lam) {
   constexpr int LN = Row<K>::kLanes;
@@ -190,7 +193,16 @@ template <int K>
 void launch_step(fr_sgd_problem* p, int64_t a, int64_t b, float eta, float lam, cudaStream_t s) {
   const int64_t groups = (b - a + 1) / 2;
   const int grid = grid_for(groups * Row<K>::kLanes, kSgdThreads, 8);
-  sgd_step_kernel<K><<<grid, kSgdThreads, 0, s>>>(p->u, p->v, p->r, p->L, a, b, eta, lam);
+  static const int minb = [] {
+    const char* e = std::getenv("FR_SGD_MINB");  // tuning hook
+    return e ? std::atoi(e) : kSgdDefaultMinBlocks;
+  }();
+  if (minb >= 8)
+    sgd_step_kernel<K, 8><<<grid, kSgdThreads, 0, s>>>(p->u, p->v, p->r, p->L, a, b, eta, lam);
+  else if (minb >= 6)
+    sgd_step_kernel<K, 6><<<grid, kSgdThreads, 0, s>>>(p->u, p->v, p->r, p->L, a, b, eta, lam);
+  else
+    sgd_step_kernel<K, 1><<<grid, kSgdThreads, 0, s>>>(p->u, p->v, p->r, p->L, a, b, eta, lam);
 }
 
 template <int K>
