@@ -349,8 +349,8 @@ def emit(args, results, ws, names, csr):
         "pagerank": {"config": "configs[0]: RMAT scale 20 (edge factor 16, seed 1), pull, d=0.85, 1 iteration/step",
                      "value": rate("pagerank"), "unit": "edges/bubble-s", "dT": dT("pagerank"),
                      "fill": fill("pagerank"),
-                     "roofline": roof("pagerank", "pr_binned_kernel (1 iteration/launch, in-pipeline); "
-                                      "working set L2-resident, bound is L2 gathers", bound="l2"),
+                     "roofline": roof("pagerank", "pr_pull_kernel (1 iteration/launch, in-pipeline); "
+                                      "working set L2-resident: latency-bound gathers, not HBM"),
                      "cpu_baseline": cpu_pagerank(args.cpu_seconds / 2, csr) if csr is not None else None},
         "sgd": {"config": "configs[2]: Orkut shape V=3,072,441 E=117,185,083 k=16, 2^20 edges/step",
                 "value": rate("sgd"), "unit": "edges/bubble-s", "dT": dT("sgd"), "fill": fill("sgd"),

@@ -6,22 +6,26 @@
 //
 // Graph build (once, on the GPU): RMAT edges with the oracle's counter-based
 // generator, self-loops dropped, (dst,src) keys radix-sorted and de-duplicated
-// (CUB), offsets by histogram + scan, out-degrees by atomics.
+// (CUB), offsets by histogram + scan, out-degrees by atomics.  That original
+// CSR is what the parity tests compare; the step reads a relabelled copy:
 //
-// Step kernel, binned CSR-vector: at graph build the rows are bucketed by
-// in-degree into lane-group sizes g in {1..32} (~4 edges per lane); a warp
-// serves 32/g rows of one bucket with no shared memory and no barriers, each
-// lane keeping 4 independent L2 gathers in flight and accumulating in fp64,
-// then an xor-shuffle reduction inside the g-lane group and a fused r'/c'
-// epilogue.  Rows with more than kHubEdges in-edges (RMAT hubs, up to ~40k)
-// get a whole CTA and are scheduled first.  (An earlier smem-staged
-// "CSR-stream" variant lost ~2x to barrier and shared-atomic stalls on RMAT's
-// skewed rows -- see DESIGN.md.)  At RMAT scale 20 the working set (~85 MB)
-// is L2-resident on B200 (126 MB): the step is bound by L2 gather bandwidth
-// (one 32 B sector per 4 B rank), not by HBM.
+//  * columns (the c[] index space) are renumbered by out-degree descending,
+//    so the sources of most in-edges sit in a short prefix of c[] (RMAT-20:
+//    the top 48 Ki vertices feed ~78 % of all gathers).  Each CTA stages that
+//    prefix in shared memory once per iteration; a warp gather from shared
+//    memory costs its bank-conflict degree (~3) instead of one L1 wavefront
+//    per distinct line (~32), which is what bounds a divergent L2 gather;
+//  * rows are ordered by in-degree bucket (split rows, then lane-group sizes
+//    g = 32..1, then the rows with no in-edges), so a work item is 32/g
+//    consecutive rows whose offsets load coalesced, and the zero-in-degree
+//    tail (r' = (1-d)/V forever) is written only by the first two iterations.
+//
+// r is kept in original vertex order (the scattered r' store goes through
+// the row's original id), c in column order.
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -30,7 +34,6 @@
 
 namespace {
 
-constexpr int kPrThreads = 256;
 constexpr uint32_t kRmatA = 2448131358u, kRmatAB = 3264175144u, kRmatABC = 4080218931u;
 constexpr uint64_t kRmatPermMul = 0x9E3779B97F4A7C15ull;
 
@@ -84,115 +87,246 @@ __global__ void split_keys_kernel(const uint64_t* __restrict__ keys, int64_t n,
   }
 }
 
-__global__ void inv_deg_kernel(const int32_t* __restrict__ outdeg, int32_t V,
-                               float* __restrict__ inv) {
+// Column order: out-degree descending, then original id.
+__global__ void col_keys_kernel(const int32_t* __restrict__ outdeg, int32_t V,
+                                uint64_t* __restrict__ keys) {
   for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x)
-    inv[v] = outdeg[v] > 0 ? 1.0f / static_cast<float>(outdeg[v]) : 0.0f;
+    keys[v] = (static_cast<uint64_t>(0x7FFFFFFF - outdeg[v]) << 32) | static_cast<uint32_t>(v);
 }
 
-__global__ void pr_reset_kernel(const float* __restrict__ inv, int32_t V, float* __restrict__ r,
-                                float* __restrict__ c) {
-  const float r0 = static_cast<float>(1.0 / static_cast<double>(V));
-  for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
-    r[v] = r0;
-    c[v] = r0 * inv[v];
+__global__ void col_perm_kernel(const uint64_t* __restrict__ sorted, int32_t V,
+                                int32_t* __restrict__ colid) {
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < V; i += gridDim.x * blockDim.x)
+    colid[static_cast<uint32_t>(sorted[i])] = i;
+}
+
+// In-degree bucket: 7 = split (> kSplitEdges), 6..1 = g = 32..1 lanes per
+// row (smallest power of two with 4g >= deg), 0 = no in-edges.
+__host__ __device__ __forceinline__ int row_bucket(int32_t d, int32_t split_edges) {
+  if (d > split_edges) return 7;
+  if (d == 0) return 0;
+  int k = 0;
+  while (k < 5 && (4 << k) < d) ++k;
+  return k + 1;
+}
+
+// Row order: bucket descending, then column id (keeps c' stores of a warp close).
+__global__ void row_keys_kernel(const int32_t* __restrict__ indeg,
+                                const int32_t* __restrict__ colid, int32_t V, int32_t split_edges,
+                                uint64_t* __restrict__ keys) {
+  for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x)
+    keys[v] = (static_cast<uint64_t>(7 - row_bucket(indeg[v], split_edges)) << 40) |
+              (static_cast<uint64_t>(static_cast<uint32_t>(colid[v])) << 8) |
+              0u;  // low byte unused
+}
+
+// Per row i (vertex v): rowc = column id, rowr = original id, rinv, in-degree
+__global__ void row_perm_kernel(const uint64_t* __restrict__ sorted, int32_t V,
+                                const int32_t* __restrict__ colperm_inv,  // column id -> original
+                                const int32_t* __restrict__ outdeg,
+                                const int32_t* __restrict__ indeg, int32_t* __restrict__ rowof,
+                                int32_t* __restrict__ rowc, int32_t* __restrict__ rowr,
+                                float* __restrict__ rinv, int32_t* __restrict__ rindeg) {
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < V; i += gridDim.x * blockDim.x) {
+    const int32_t c = static_cast<int32_t>((sorted[i] >> 8) & 0xFFFFFFFFu);
+    const int32_t v = colperm_inv[c];
+    rowof[v] = i;
+    rowc[i] = c;
+    rowr[i] = v;
+    rinv[i] = outdeg[v] > 0 ? 1.0f / static_cast<float>(outdeg[v]) : 0.0f;
+    rindeg[i] = indeg[v];
   }
 }
 
+__global__ void col_inv_kernel(const uint64_t* __restrict__ sorted, int32_t V,
+                               int32_t* __restrict__ colperm_inv) {
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < V; i += gridDim.x * blockDim.x)
+    colperm_inv[i] = static_cast<int32_t>(static_cast<uint32_t>(sorted[i]));
+}
+
+// (dst << 32 | src) in original ids -> (row of dst << 32 | column of src)
+__global__ void relabel_edges_kernel(const uint64_t* __restrict__ keys, int64_t E,
+                                     const int32_t* __restrict__ rowof,
+                                     const int32_t* __restrict__ colid,
+                                     uint64_t* __restrict__ out) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < E;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t k = keys[e];
+    out[e] = (static_cast<uint64_t>(rowof[k >> 32]) << 32) |
+             static_cast<uint32_t>(colid[k & 0xFFFFFFFFu]);
+  }
+}
+
+__global__ void low_word_kernel(const uint64_t* __restrict__ keys, int64_t n,
+                                int32_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = static_cast<int32_t>(keys[i] & 0xFFFFFFFFu);
+}
+
+// r = 1/V (original order); c[0][col] = r * inv (written through the rows),
+// c[1] = 0 (rewritten by the first iteration).
+__global__ void pr_reset_kernel(const int32_t* __restrict__ rowc, const float* __restrict__ rinv,
+                                int32_t V, float* __restrict__ r, float* __restrict__ c0,
+                                float* __restrict__ c1) {
+  const float r0 = static_cast<float>(1.0 / static_cast<double>(V));
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < V; i += gridDim.x * blockDim.x) {
+    r[i] = r0;
+    c0[rowc[i]] = r0 * rinv[i];
+    c1[i] = 0.0f;
+  }
+}
+
+constexpr int kPrThreads = 1024;     // persistent: one CTA per SM
+constexpr int kPrWarps = kPrThreads / 32;
+constexpr int kSplitEdges = 256;     // default: rows with more in-edges are split into chunks
+constexpr int kDefaultHot = 49152;   // c[] prefix staged in shared memory (192 KB)
+constexpr int kMaxCtas = 256;        // split-row chunk lists per CTA (grid = SM count)
+constexpr int kMaxSlots = 256;       // split rows per CTA (shared-memory accumulators)
+
 struct PrArgs {
-  const int32_t* offsets;
-  const int32_t* col;
-  const float* inv;
-  const int32_t* blk;  // work list: hub (row,-1) / item (start, g | count<<8) pairs
-  const int32_t* rows; // binned row list (pr_binned_kernel)
-  int32_t n_hub;
+  const int32_t* off;    // relabelled incoming CSR (row order)
+  const int32_t* col;    // column ids
+  const float* rinv;     // per row: 1 / out-degree (0 if dangling)
+  const int32_t* rowc;   // per row: column id (c' store)
+  const int32_t* rowr;   // per row: original id (r' store)
+  const int4* chunks;    // {row, e_begin, e_end, slot | chunks of the row << 8}, grouped by CTA
   const float* c_in;
   float* r_out;
   float* c_out;
-  int32_t n_blk;
-  double base;
-  double damp;
+  int32_t bstart[8];     // first row of bucket b (7 = split .. 1 = g 1), bstart[0] = tail
+  int32_t istart[8];     // first item of bucket b = 6..1 (items of b-1 follow), istart[0] = total
+  int32_t hot, V, do_tail;
+  double base, damp;
+  int32_t cta_chunk[kMaxCtas + 1];  // CTA b owns chunks [cta_chunk[b], cta_chunk[b+1])
 };
 
-__device__ __forceinline__ double block_sum(double x, double* red) {
+// N predicated gathers per lane, `stride` apart: hot sources from shared
+// memory, the rest from L2.  The N values are summed in fp32 (N <= 8 terms,
+// relative error <= N * 2^-24), the caller accumulates these partials in fp64.
+template <int N>
+__device__ __forceinline__ double gather(const PrArgs& a, const float* hot, int32_t e, int32_t e1,
+                                         int stride) {
+  int32_t u[N];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  if (l == 0) red[w] = x;
-  __syncthreads();
-  double t = 0.0;
-  if (threadIdx.x < kPrThreads / 32) t = red[threadIdx.x];
-  if (w == 0) {
+  for (int j = 0; j < N; ++j) u[j] = e + j * stride < e1 ? __ldg(&a.col[e + j * stride]) : -1;
+  float s = 0.0f;
 #pragma unroll
-    for (int o = 4; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-  }
-  return t;  // valid in thread 0
+  for (int j = 0; j < N; ++j) s += u[j] < 0 ? 0.0f : (u[j] < a.hot ? hot[u[j]] : __ldg(&a.c_in[u[j]]));
+  return static_cast<double>(s);
 }
 
-constexpr int kHubEdges = 2048;
+// A bucket item as seen by one lane: its row, edge range and the row's
+// output metadata, all loaded up front (one round trip).
+struct Item {
+  int32_t e, e1, rr, rc;
+  float inv;
+  int lanes;
+  bool emit;
+};
 
-// Binned CSR-vector pull: no shared memory, no barriers on the common path.
-// Block b < n_hub: one hub row for the whole CTA.  Otherwise each warp takes
-// one work item: 32/g rows of one degree bucket, g lanes per row striding the
-// row's in-edges (coalesced col_idx within the group, 4 independent L2
-// gathers in flight per lane), fp64 partials, xor-shuffle reduction inside
-// the g-lane group, fused r'/c' epilogue by the group's first lane.
-__global__ void __launch_bounds__(kPrThreads) pr_binned_kernel(PrArgs a) {
-  __shared__ double red[kPrThreads / 32];
-  const int tid = threadIdx.x;
-  if (static_cast<int32_t>(blockIdx.x) < a.n_hub) {
-    const int32_t r0 = a.blk[2 * blockIdx.x];
-    const int32_t e0 = a.offsets[r0], e1 = a.offsets[r0 + 1];
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    int32_t i = e0 + tid;
-    for (; i + 3 * kPrThreads < e1; i += 4 * kPrThreads) {
-      const int32_t u0 = __ldg(&a.col[i]), u1 = __ldg(&a.col[i + kPrThreads]);
-      const int32_t u2 = __ldg(&a.col[i + 2 * kPrThreads]), u3 = __ldg(&a.col[i + 3 * kPrThreads]);
-      s0 += __ldg(&a.c_in[u0]);
-      s1 += __ldg(&a.c_in[u1]);
-      s2 += __ldg(&a.c_in[u2]);
-      s3 += __ldg(&a.c_in[u3]);
-    }
-    for (; i < e1; i += kPrThreads) s0 += __ldg(&a.c_in[__ldg(&a.col[i])]);
-    const double s = block_sum((s0 + s1) + (s2 + s3), red);
-    if (tid == 0) {
-      const float rv = static_cast<float>(a.base + a.damp * s);
-      a.r_out[r0] = rv;
-      a.c_out[r0] = rv * a.inv[r0];
-    }
-    return;
-  }
-  const int32_t item = a.n_hub + (static_cast<int32_t>(blockIdx.x) - a.n_hub) * (kPrThreads / 32) + (tid >> 5);
-  if (item >= a.n_blk) return;
-  const int32_t start = a.blk[2 * item], code = a.blk[2 * item + 1];
-  const int lanes = code & 0xFF, count = code >> 8;
-  const int lane = tid & 31, grp = lane / lanes, sub = lane % lanes;
-  int32_t row = -1, e = 0, e1 = 0;
-  if (grp < count) {
-    row = a.rows[start + grp];
-    e = a.offsets[row] + sub;
-    e1 = a.offsets[row + 1];
-  }
-  // Predicated 4-wide chunks: all four col_idx loads, then all four gathers,
-  // are in flight together even for rows shorter than 4 x lanes (the common
-  // case), i.e. two dependent L2 round trips per chunk, not two per edge.
-  double s0 = 0.0, s1 = 0.0;
-  for (; e < e1; e += 4 * lanes) {
-    int32_t u[4];
+__device__ __forceinline__ Item prep(const PrArgs& a, int it, bool valid, int lane) {
+  int b = 6;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) u[j] = e + j * lanes < e1 ? __ldg(&a.col[e + j * lanes]) : -1;
-    float c[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) c[j] = u[j] >= 0 ? __ldg(&a.c_in[u[j]]) : 0.0f;
-    s0 += static_cast<double>(c[0]) + static_cast<double>(c[1]);
-    s1 += static_cast<double>(c[2]) + static_cast<double>(c[3]);
+  for (int k = 6; k > 1; --k)
+    if (it >= a.istart[k - 1]) b = k - 1;
+  Item x;
+  x.lanes = 1 << (b - 1);
+  const int sub = lane & (x.lanes - 1);
+  const int32_t row = a.bstart[b] + (it - a.istart[b]) * (32 >> (b - 1)) + (lane >> (b - 1));
+  const bool live = valid && row < a.bstart[b - 1];
+  x.e = x.e1 = 0;
+  x.rr = x.rc = 0;
+  x.inv = 0.0f;
+  x.emit = live && sub == 0;
+  if (live) {
+    x.e = __ldg(&a.off[row]) + sub;
+    x.e1 = __ldg(&a.off[row + 1]);
+    if (sub == 0) {
+      x.rr = __ldg(&a.rowr[row]);
+      x.rc = __ldg(&a.rowc[row]);
+      x.inv = __ldg(&a.rinv[row]);
+    }
   }
-  double s = s0 + s1;
+  return x;
+}
+
+__device__ __forceinline__ void store(const PrArgs& a, int32_t rr, int32_t rc, float inv, double s) {
+  const float rv = static_cast<float>(a.base + a.damp * s);
+  a.r_out[rr] = rv;
+  a.c_out[rc] = rv * inv;
+}
+
+__device__ __forceinline__ double group_sum(double s, int lanes) {
   for (int o = lanes >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (sub == 0 && row >= 0) {
-    const float rv = static_cast<float>(a.base + a.damp * s);
-    a.r_out[row] = rv;
-    a.c_out[row] = rv * a.inv[row];
+  return s;
+}
+
+// One pull iteration.  Persistent CTAs (one per SM, 32 warps) copy the hot
+// prefix of c[] into shared memory, then
+//  (1) split rows: each CTA owns whole split rows (LPT-balanced at graph
+//      build), its warps take their 256-edge chunks (8 gathers in flight per
+//      lane) and meet in shared-memory fp64 accumulators; the warp finishing
+//      a row's last chunk stores r'/c' (CTA-scope fences only: no global
+//      memory barrier, no L1 invalidation);
+//  (2) bucket items (32/g consecutive rows, g lanes per row), two items per
+//      warp interleaved so both items' loads are in flight together, in a
+//      static round-robin over all warps (items are ordered heavy first and
+//      carry ~64..256 edges each);
+//  (3) the zero-in-degree tail, when asked.
+__global__ void __launch_bounds__(kPrThreads, 1) pr_pull_kernel(PrArgs a) {
+  extern __shared__ float4 hot4[];
+  __shared__ double sacc[kMaxSlots];
+  __shared__ int scnt[kMaxSlots];
+  const float* hot = reinterpret_cast<const float*>(hot4);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  {
+    const float4* src = reinterpret_cast<const float4*>(a.c_in);
+    for (int i = tid; i < (a.hot >> 2); i += kPrThreads) hot4[i] = __ldg(&src[i]);
+    if (tid < kMaxSlots) {
+      sacc[tid] = 0.0;
+      scnt[tid] = 0;
+    }
+  }
+  __syncthreads();
+  for (int c = a.cta_chunk[blockIdx.x] + warp; c < a.cta_chunk[blockIdx.x + 1]; c += kPrWarps) {
+    const int4 ch = __ldg(&a.chunks[c]);
+    double s = 0.0;
+    for (int32_t e = ch.y + lane; e < ch.z; e += 256) s += gather<8>(a, hot, e, ch.z, 32);
+    s = group_sum(s, 32);
+    if (lane == 0) {
+      const int slot = ch.w & 0xFF, need = ch.w >> 8;
+      atomicAdd(&sacc[slot], s);
+      __threadfence_block();
+      if (atomicAdd(&scnt[slot], 1) + 1 == need) {
+        __threadfence_block();
+        const double tot = *static_cast<volatile double*>(&sacc[slot]);
+        store(a, __ldg(&a.rowr[ch.x]), __ldg(&a.rowc[ch.x]), __ldg(&a.rinv[ch.x]), tot);
+      }
+    }
+  }
+  const int nw = gridDim.x * kPrWarps, gw = blockIdx.x * kPrWarps + warp, n = a.istart[0];
+  // software-pipelined: the next pair's offsets and output metadata load
+  // while this pair gathers
+  Item x = prep(a, gw, gw < n, lane), y = prep(a, gw + nw, gw + nw < n, lane);
+  for (int it = gw; it < n; it += 2 * nw) {
+    const int nx = it + 2 * nw;
+    const Item px = prep(a, nx, nx < n, lane), py = prep(a, nx + nw, nx + nw < n, lane);
+    double sx = 0.0, sy = 0.0;
+    for (int32_t ex = x.e, ey = y.e; ex < x.e1 || ey < y.e1; ex += 4 * x.lanes, ey += 4 * y.lanes) {
+      sx += gather<4>(a, hot, ex, x.e1, x.lanes);
+      sy += gather<4>(a, hot, ey, y.e1, y.lanes);
+    }
+    sx = group_sum(sx, x.lanes);
+    sy = group_sum(sy, y.lanes);
+    if (x.emit) store(a, x.rr, x.rc, x.inv, sx);
+    if (y.emit) store(a, y.rr, y.rc, y.inv, sy);
+    x = px;
+    y = py;
+  }
+  if (a.do_tail) {
+    for (int32_t i = a.bstart[0] + blockIdx.x * kPrThreads + tid; i < a.V; i += gridDim.x * kPrThreads)
+      store(a, __ldg(&a.rowr[i]), __ldg(&a.rowc[i]), __ldg(&a.rinv[i]), 0.0);
   }
 }
 
@@ -204,19 +338,43 @@ int grid_for(int64_t work, int threads, int per_sm) {
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(sms) * per_sm)));
 }
 
+int split_edges() {
+  static const int v = [] {
+    const char* e = std::getenv("FR_PR_SPLIT");  // tuning hook, 32..256
+    return e ? std::min(256, std::max(32, std::atoi(e))) : kSplitEdges;
+  }();
+  return v;
+}
+
+int hot_vertices(int32_t V) {
+  static const int want = [] {
+    const char* e = std::getenv("FR_PR_HOT");  // tuning hook
+    return e ? std::max(0, std::atoi(e)) : kDefaultHot;
+  }();
+  return std::min(want, V) & ~3;
+}
+
 }  // namespace
 
+// Device view of a graph.  The original CSR (offsets/col/outdeg) is what the
+// parity tests compare with the oracle; the step kernel reads the relabelled
+// copy (xoff/xcol + per-row rowc/rowr/rinv) and the split-row chunk list.
 struct fr_pr_graph {
   int32_t V = 0;
   int64_t E = 0;
-  int32_t* offsets = nullptr;  // V + 1
+  int32_t* offsets = nullptr;  // V + 1, original ids
   int32_t* col = nullptr;      // E
   int32_t* outdeg = nullptr;   // V
-  float* inv = nullptr;        // V
-  int32_t* blk = nullptr;      // work list: n_blk (a, b) pairs, then the binned row list
-  int32_t n_blk = 0;           // hubs + warp items
-  int32_t n_hub = 0;           // leading hub rows (one CTA each)
-  int64_t blk_len = 0;         // int32 entries in blk
+  int32_t* xoff = nullptr;     // V + 1, row order
+  int32_t* xcol = nullptr;     // E, column ids
+  int32_t* rowc = nullptr;     // V
+  int32_t* rowr = nullptr;     // V
+  float* rinv = nullptr;       // V
+  int4* chunks = nullptr;      // n_chunk, grouped by CTA
+  int32_t n_chunk = 0, n_split = 0;
+  int32_t cta_chunk[kMaxCtas + 1] = {};
+  int32_t bstart[8] = {};      // see PrArgs
+  int32_t istart[8] = {};
   int sms = 148;
 };
 
@@ -226,82 +384,85 @@ struct fr_pr_state {
   float* c[2] = {nullptr, nullptr};
   int cur = 0;
   int64_t iterations = 0;
+  int tail_pending = 2;        // launches that still write the zero-in-degree tail
+  float tail_damping = -1.0f;  // damping the tail was written with
 };
 
 namespace {
 
 void free_graph(fr_pr_graph* g) {
   for (void* p : {static_cast<void*>(g->offsets), static_cast<void*>(g->col),
-                  static_cast<void*>(g->outdeg), static_cast<void*>(g->inv),
-                  static_cast<void*>(g->blk)})
+                  static_cast<void*>(g->outdeg), static_cast<void*>(g->xoff),
+                  static_cast<void*>(g->xcol), static_cast<void*>(g->rowc),
+                  static_cast<void*>(g->rowr), static_cast<void*>(g->rinv),
+                  static_cast<void*>(g->chunks)})
     if (p) cudaFree(p);
   delete g;
 }
 
-// Binned work list for pr_binned_kernel.  Rows with more than kHubEdges
-// in-edges are hubs (one CTA each, listed first so they start in the first
-// wave).  Every other row gets g lanes, g = the smallest power of two >=
-// ceil(deg / 4) (so each lane gathers ~4 edges), 1 <= g <= 32; rows are
-// bucketed by g and each warp item serves 32/g rows of one bucket.  Items are
-// ordered by descending g (heavier work first).
-// blk layout: n_blk pairs (a, b) then the bucketed row list:
-//   hub  : (row, -1)
-//   item : (start in row list, g | count << 8)
-int build_bins(fr_pr_graph* g, cudaStream_t s) {
+// Bucket boundaries, item counts and the split-row chunk list (host, once).
+int build_work(fr_pr_graph* g, cudaStream_t s) {
   std::vector<int32_t> off(static_cast<size_t>(g->V) + 1);
-  FR_CUDA_TRY(cudaMemcpyAsync(off.data(), g->offsets, off.size() * sizeof(int32_t),
+  FR_CUDA_TRY(cudaMemcpyAsync(off.data(), g->xoff, off.size() * sizeof(int32_t),
                               cudaMemcpyDeviceToHost, s));
   FR_CUDA_TRY(cudaStreamSynchronize(s));
-  std::vector<int32_t> hubs, bucket[6];  // bucket k: g = 1 << k
-  for (int32_t r = 0; r < g->V; ++r) {
-    const int32_t d = off[r + 1] - off[r];
-    if (d > kHubEdges) {
-      hubs.push_back(r);
-      continue;
-    }
-    int k = 0;
-    while (k < 5 && (4 << k) < d) ++k;
-    bucket[k].push_back(r);
+  int32_t count[8] = {};
+  const int split = split_edges();
+  for (int32_t r = 0; r < g->V; ++r) ++count[row_bucket(off[r + 1] - off[r], split)];
+  // rows are sorted by bucket descending: bucket 7 first
+  int32_t at = 0;
+  for (int b = 7; b >= 0; --b) {
+    g->bstart[b] = at;
+    at += count[b];
   }
-  std::sort(hubs.begin(), hubs.end(), [&](int32_t x, int32_t y) {
+  int32_t items = 0;
+  for (int b = 6; b >= 1; --b) {
+    g->istart[b] = items;
+    const int per = 32 >> (b - 1);
+    items += (count[b] + per - 1) / per;
+  }
+  g->istart[7] = 0;
+  g->istart[0] = items;
+  // split rows -> CTAs, longest first onto the least-loaded CTA (LPT), at
+  // most kMaxSlots rows per CTA; each CTA's chunks are contiguous.
+  const int ctas = std::min(g->sms, kMaxCtas);
+  if (count[7] > ctas * kMaxSlots)
+    return frcapi::fail(FR_ERR_UNSUPPORTED, "too many split rows for the per-CTA accumulators");
+  std::vector<int32_t> order(count[7]);
+  for (int32_t r = 0; r < count[7]; ++r) order[r] = r;
+  std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) {
     return off[x + 1] - off[x] > off[y + 1] - off[y];
   });
-  std::vector<int32_t> pairs, rows;
-  for (int32_t h : hubs) {
-    pairs.push_back(h);
-    pairs.push_back(-1);
+  std::vector<int64_t> load(ctas, 0);
+  std::vector<std::vector<int32_t>> owned(ctas);
+  for (int32_t r : order) {
+    int best = -1;
+    for (int c = 0; c < ctas; ++c)
+      if (static_cast<int>(owned[c].size()) < kMaxSlots && (best < 0 || load[c] < load[best])) best = c;
+    owned[best].push_back(r);
+    load[best] += off[r + 1] - off[r];
   }
-  for (int k = 5; k >= 0; --k) {
-    const int32_t lanes = 1 << k, per = 32 / lanes;
-    for (size_t i = 0; i < bucket[k].size(); i += per) {
-      const int32_t cnt = static_cast<int32_t>(std::min<size_t>(per, bucket[k].size() - i));
-      pairs.push_back(static_cast<int32_t>(rows.size() + i));
-      pairs.push_back(lanes | (cnt << 8));
+  std::vector<int4> chunks;
+  for (int c = 0; c < ctas; ++c) {
+    g->cta_chunk[c] = static_cast<int32_t>(chunks.size());
+    for (size_t slot = 0; slot < owned[c].size(); ++slot) {
+      const int32_t r = owned[c][slot];
+      const int32_t n = (off[r + 1] - off[r] + split - 1) / split;
+      for (int32_t e = off[r]; e < off[r + 1]; e += split)
+        chunks.push_back(make_int4(r, e, std::min(e + split, off[r + 1]),
+                                   static_cast<int32_t>(slot) | (n << 8)));
     }
-    rows.insert(rows.end(), bucket[k].begin(), bucket[k].end());
   }
-  // item starts index the row list, which follows the pairs
-  const int32_t n = static_cast<int32_t>(pairs.size() / 2);
-  std::vector<int32_t> blk(pairs);
-  blk.insert(blk.end(), rows.begin(), rows.end());
-  g->n_blk = n;
-  g->n_hub = static_cast<int32_t>(hubs.size());
-  g->blk_len = static_cast<int64_t>(blk.size());
-  FR_CUDA_TRY(cudaMalloc(&g->blk, blk.size() * sizeof(int32_t)));
-  FR_CUDA_TRY(cudaMemcpyAsync(g->blk, blk.data(), blk.size() * sizeof(int32_t),
-                              cudaMemcpyHostToDevice, s));
-  FR_CUDA_TRY(cudaStreamSynchronize(s));
+  for (int c = ctas; c <= kMaxCtas; ++c) g->cta_chunk[c] = static_cast<int32_t>(chunks.size());
+  g->n_split = count[7];
+  g->n_chunk = static_cast<int32_t>(chunks.size());
+  FR_CUDA_TRY(cudaMalloc(&g->chunks, std::max<size_t>(1, chunks.size()) * sizeof(int4)));
+  if (!chunks.empty()) {
+    FR_CUDA_TRY(cudaMemcpyAsync(g->chunks, chunks.data(), chunks.size() * sizeof(int4),
+                                cudaMemcpyHostToDevice, s));
+    FR_CUDA_TRY(cudaStreamSynchronize(s));
+  }
   return FR_OK;
-}
-
-int finish_graph(fr_pr_graph* g, cudaStream_t s) {
-  FR_CUDA_TRY(cudaMalloc(&g->inv, sizeof(float) * static_cast<size_t>(g->V)));
-  inv_deg_kernel<<<grid_for(g->V, 256, 8), 256, 0, s>>>(g->outdeg, g->V, g->inv);
-  FR_CUDA_LAUNCHED("inv_deg");
-  int dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&g->sms, cudaDevAttrMultiProcessorCount, dev);
-  return build_bins(g, s);
 }
 
 }  // namespace
@@ -317,31 +478,41 @@ int fr_pr_graph_rmat(int32_t scale, int32_t edge_factor, uint64_t seed, void* st
   const int64_t m = static_cast<int64_t>(edge_factor) << scale;
   auto* g = new fr_pr_graph;
   g->V = 1 << scale;
+  const size_t V = static_cast<size_t>(g->V);
   int32_t *src = nullptr, *dst = nullptr, *indeg = nullptr, *d_sel = nullptr;
-  uint64_t *keys = nullptr, *sorted = nullptr;
+  int32_t *colid = nullptr, *colinv = nullptr, *rowof = nullptr, *rindeg = nullptr;
+  uint64_t *keys = nullptr, *sorted = nullptr, *vkeys = nullptr;
   void* tmp = nullptr;
-  size_t tmp_bytes = 0, need = 0;
+  size_t tmp_bytes = 0;
   int rc = FR_OK;
   auto step = [&](cudaError_t e, const char* what) {
     if (rc == FR_OK && e != cudaSuccess) rc = frcapi::cuda_status(e, what);
     return rc == FR_OK;
   };
+  auto temp = [&](size_t need) {  // grow the CUB scratch
+    if (rc != FR_OK || need <= tmp_bytes) return;
+    if (tmp) cudaFree(tmp);
+    tmp = nullptr;
+    tmp_bytes = 0;
+    if (step(cudaMalloc(&tmp, need), "cub temp")) tmp_bytes = need;
+  };
+  const int gv = grid_for(g->V, 256, 8), gm = grid_for(m, 256, 16);
   step(cudaMalloc(&src, m * sizeof(int32_t)), "rmat src");
   step(cudaMalloc(&dst, m * sizeof(int32_t)), "rmat dst");
   step(cudaMalloc(&keys, m * sizeof(uint64_t)), "keys");
   step(cudaMalloc(&sorted, m * sizeof(uint64_t)), "sorted");
   step(cudaMalloc(&d_sel, sizeof(int32_t)), "count");
   if (rc == FR_OK) {
-    rmat_kernel<<<grid_for(m, 256, 16), 256, 0, s>>>(scale, m, seed, src, dst);
-    edge_keys_kernel<<<grid_for(m, 256, 16), 256, 0, s>>>(src, dst, m, keys);
+    rmat_kernel<<<gm, 256, 0, s>>>(scale, m, seed, src, dst);
+    edge_keys_kernel<<<gm, 256, 0, s>>>(src, dst, m, keys);
     step(cudaGetLastError(), "rmat / keys");
   }
+  size_t need = 0;
   if (rc == FR_OK) {
     cub::DeviceRadixSort::SortKeys(nullptr, need, keys, sorted, static_cast<int>(m), 0, 64, s);
-    tmp_bytes = need;
+    temp(need);
     cub::DeviceSelect::Unique(nullptr, need, sorted, keys, d_sel, static_cast<int>(m), s);
-    tmp_bytes = std::max(tmp_bytes, need);
-    step(cudaMalloc(&tmp, tmp_bytes), "cub temp");
+    temp(need);
   }
   int32_t n_unique = 0;
   if (rc == FR_OK) {
@@ -356,31 +527,71 @@ int fr_pr_graph_rmat(int32_t scale, int32_t edge_factor, uint64_t seed, void* st
     if (n_unique > 0)
       step(cudaMemcpy(&last, keys + n_unique - 1, sizeof(uint64_t), cudaMemcpyDeviceToHost), "last key");
     g->E = (n_unique > 0 && last == ~0ull) ? n_unique - 1 : n_unique;
-    step(cudaMalloc(&g->col, std::max<int64_t>(1, g->E) * sizeof(int32_t)), "col");
-    step(cudaMalloc(&g->offsets, (static_cast<size_t>(g->V) + 1) * sizeof(int32_t)), "offsets");
-    step(cudaMalloc(&g->outdeg, static_cast<size_t>(g->V) * sizeof(int32_t)), "outdeg");
-    step(cudaMalloc(&indeg, static_cast<size_t>(g->V) * sizeof(int32_t)), "indeg");
+    const size_t Eb = std::max<int64_t>(1, g->E) * sizeof(int32_t);
+    step(cudaMalloc(&g->col, Eb), "col");
+    step(cudaMalloc(&g->xcol, Eb), "xcol");
+    step(cudaMalloc(&g->offsets, (V + 1) * sizeof(int32_t)), "offsets");
+    step(cudaMalloc(&g->xoff, (V + 1) * sizeof(int32_t)), "xoff");
+    step(cudaMalloc(&g->outdeg, V * sizeof(int32_t)), "outdeg");
+    step(cudaMalloc(&g->rowc, V * sizeof(int32_t)), "rowc");
+    step(cudaMalloc(&g->rowr, V * sizeof(int32_t)), "rowr");
+    step(cudaMalloc(&g->rinv, V * sizeof(float)), "rinv");
+    step(cudaMalloc(&indeg, V * sizeof(int32_t)), "indeg");
+    step(cudaMalloc(&colid, V * sizeof(int32_t)), "colid");
+    step(cudaMalloc(&colinv, V * sizeof(int32_t)), "colinv");
+    step(cudaMalloc(&rowof, V * sizeof(int32_t)), "rowof");
+    step(cudaMalloc(&rindeg, V * sizeof(int32_t)), "rindeg");
+    step(cudaMalloc(&vkeys, 2 * V * sizeof(uint64_t)), "vertex keys");
   }
   if (rc == FR_OK) {
-    step(cudaMemsetAsync(indeg, 0, static_cast<size_t>(g->V) * sizeof(int32_t), s), "memset");
-    step(cudaMemsetAsync(g->outdeg, 0, static_cast<size_t>(g->V) * sizeof(int32_t), s), "memset");
+    step(cudaMemsetAsync(indeg, 0, V * sizeof(int32_t), s), "memset");
+    step(cudaMemsetAsync(g->outdeg, 0, V * sizeof(int32_t), s), "memset");
     step(cudaMemsetAsync(g->offsets, 0, sizeof(int32_t), s), "memset");
+    step(cudaMemsetAsync(g->xoff, 0, sizeof(int32_t), s), "memset");
     if (g->E > 0) split_keys_kernel<<<grid_for(g->E, 256, 16), 256, 0, s>>>(keys, g->E, g->col, indeg, g->outdeg);
     step(cudaGetLastError(), "split keys");
-    size_t sb = 0;
-    cub::DeviceScan::InclusiveSum(nullptr, sb, indeg, g->offsets + 1, g->V, s);
-    if (sb > tmp_bytes) {
-      cudaFree(tmp);
-      tmp = nullptr;
-      step(cudaMalloc(&tmp, sb), "scan temp");
-      tmp_bytes = sb;
-    }
+    cub::DeviceScan::InclusiveSum(nullptr, need, indeg, g->offsets + 1, g->V, s);
+    temp(need);
     step(cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, indeg, g->offsets + 1, g->V, s), "scan");
   }
+  // column order, then row order, then the relabelled CSR
+  if (rc == FR_OK) {
+    cub::DeviceRadixSort::SortKeys(nullptr, need, vkeys, vkeys + V, g->V, 0, 64, s);
+    temp(need);
+    col_keys_kernel<<<gv, 256, 0, s>>>(g->outdeg, g->V, vkeys);
+    step(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, vkeys, vkeys + V, g->V, 0, 63, s), "column sort");
+    col_perm_kernel<<<gv, 256, 0, s>>>(vkeys + V, g->V, colid);
+    col_inv_kernel<<<gv, 256, 0, s>>>(vkeys + V, g->V, colinv);
+    row_keys_kernel<<<gv, 256, 0, s>>>(indeg, colid, g->V, split_edges(), vkeys);
+    step(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, vkeys, vkeys + V, g->V, 8, 43, s), "row sort");
+    row_perm_kernel<<<gv, 256, 0, s>>>(vkeys + V, g->V, colinv, g->outdeg, indeg, rowof, g->rowc,
+                                       g->rowr, g->rinv, rindeg);
+    step(cudaGetLastError(), "relabel");
+    if (g->E > 0) {
+      relabel_edges_kernel<<<grid_for(g->E, 256, 16), 256, 0, s>>>(keys, g->E, rowof, colid, sorted);
+      step(cudaGetLastError(), "relabel edges");
+      cub::DeviceRadixSort::SortKeys(nullptr, need, sorted, keys, static_cast<int>(g->E), 0, 32 + scale, s);
+      temp(need);
+      step(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, sorted, keys, static_cast<int>(g->E), 0,
+                                          32 + scale, s), "relabelled edge sort");
+      low_word_kernel<<<grid_for(g->E, 256, 16), 256, 0, s>>>(keys, g->E, g->xcol);
+      step(cudaGetLastError(), "xcol");
+    }
+    cub::DeviceScan::InclusiveSum(nullptr, need, rindeg, g->xoff + 1, g->V, s);
+    temp(need);
+    step(cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, rindeg, g->xoff + 1, g->V, s), "xscan");
+  }
   for (void* p : {static_cast<void*>(src), static_cast<void*>(dst), static_cast<void*>(keys),
-                  static_cast<void*>(sorted), static_cast<void*>(indeg), static_cast<void*>(d_sel), tmp})
+                  static_cast<void*>(sorted), static_cast<void*>(indeg), static_cast<void*>(d_sel),
+                  static_cast<void*>(colid), static_cast<void*>(colinv), static_cast<void*>(rowof),
+                  static_cast<void*>(rindeg), static_cast<void*>(vkeys), tmp})
     if (p) cudaFreeAsync(p, s);
-  if (rc == FR_OK) rc = finish_graph(g, s);
+  if (rc == FR_OK) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g->sms, cudaDevAttrMultiProcessorCount, dev);
+    rc = build_work(g, s);
+  }
   if (rc != FR_OK) {
     free_graph(g);
     return rc;
@@ -398,13 +609,14 @@ int fr_pr_graph_info(const fr_pr_graph* g, int32_t* V, int64_t* E, int32_t* n_bl
   if (!g) return frcapi::fail(FR_ERR_ARGUMENT, "null graph");
   if (V) *V = g->V;
   if (E) *E = g->E;
-  if (n_blocks) *n_blocks = g->n_blk;
+  if (n_blocks) *n_blocks = g->n_chunk + g->istart[0];
   return FR_OK;
 }
 
 int fr_pr_graph_csr(const fr_pr_graph* g, const int32_t** offsets, const int32_t** col_idx,
                     const int32_t** outdeg) {
   if (!g) return frcapi::fail(FR_ERR_ARGUMENT, "null graph");
+  if (!g->offsets) return frcapi::fail(FR_ERR_UNSUPPORTED, "graph holds only the relabelled CSR");
   if (offsets) *offsets = g->offsets;
   if (col_idx) *col_idx = g->col;
   if (outdeg) *outdeg = g->outdeg;
@@ -415,12 +627,13 @@ int fr_pr_state_create(const fr_pr_graph* g, fr_pr_state** out) {
   if (!g || !out) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
   auto* st = new fr_pr_state;
   st->g = g;
-  const size_t b = sizeof(float) * static_cast<size_t>(std::max(1, g->V));
+  const size_t b = sizeof(float) * static_cast<size_t>(std::max(4, g->V));
   cudaError_t e = cudaMalloc(&st->r, b);
   if (e == cudaSuccess) e = cudaMalloc(&st->c[0], b);
   if (e == cudaSuccess) e = cudaMalloc(&st->c[1], b);
   if (e != cudaSuccess) {
-    for (float* p : {st->r, st->c[0], st->c[1]})
+    for (void* p : {static_cast<void*>(st->r), static_cast<void*>(st->c[0]),
+                    static_cast<void*>(st->c[1])})
       if (p) cudaFree(p);
     delete st;
     return frcapi::cuda_status(e, "pagerank state");
@@ -431,7 +644,8 @@ int fr_pr_state_create(const fr_pr_graph* g, fr_pr_state** out) {
 
 int fr_pr_state_destroy(fr_pr_state* st) {
   if (!st) return FR_OK;
-  for (float* p : {st->r, st->c[0], st->c[1]})
+  for (void* p : {static_cast<void*>(st->r), static_cast<void*>(st->c[0]),
+                  static_cast<void*>(st->c[1])})
     if (p) cudaFree(p);
   delete st;
   return FR_OK;
@@ -439,10 +653,14 @@ int fr_pr_state_destroy(fr_pr_state* st) {
 
 int fr_pr_reset(fr_pr_state* st, void* stream) {
   if (!st) return frcapi::fail(FR_ERR_ARGUMENT, "null state");
+  auto s = static_cast<cudaStream_t>(stream);
+  const fr_pr_graph* g = st->g;
   st->cur = 0;
   st->iterations = 0;
-  pr_reset_kernel<<<grid_for(st->g->V, 256, 8), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      st->g->inv, st->g->V, st->r, st->c[0]);
+  st->tail_pending = 2;
+  st->tail_damping = -1.0f;
+  pr_reset_kernel<<<grid_for(g->V, 256, 8), 256, 0, s>>>(g->rowc, g->rinv, g->V, st->r, st->c[0],
+                                                         st->c[1]);
   FR_CUDA_LAUNCHED("pr_reset");
   return FR_OK;
 }
@@ -453,23 +671,37 @@ int fr_pr_step(fr_pr_state* st, int32_t iters, float damping, void* stream) {
   const fr_pr_graph* g = st->g;
   auto s = static_cast<cudaStream_t>(stream);
   PrArgs a{};
-  a.offsets = g->offsets;
-  a.col = g->col;
-  a.inv = g->inv;
-  a.blk = g->blk;
-  a.n_blk = g->n_blk;
-  a.n_hub = g->n_hub;
-  a.rows = g->blk + 2 * static_cast<int64_t>(g->n_blk);
+  a.off = g->xoff;
+  a.col = g->xcol;
+  a.rinv = g->rinv;
+  a.rowc = g->rowc;
+  a.rowr = g->rowr;
+  a.chunks = g->chunks;
   a.r_out = st->r;
+  std::memcpy(a.cta_chunk, g->cta_chunk, sizeof(a.cta_chunk));
+  std::memcpy(a.bstart, g->bstart, sizeof(a.bstart));
+  std::memcpy(a.istart, g->istart, sizeof(a.istart));
+  a.hot = hot_vertices(g->V);
+  a.V = g->V;
   a.damp = static_cast<double>(damping);
   a.base = (1.0 - static_cast<double>(damping)) / static_cast<double>(g->V);
-  const int warps = kPrThreads / 32;
-  const int grid = g->n_hub + (g->n_blk - g->n_hub + warps - 1) / warps;
-  if (grid == 0) return FR_OK;
+  const size_t smem = static_cast<size_t>(a.hot) * sizeof(float);
+  static int smem_set = -1;  // per process; the attribute is per function
+  if (static_cast<int>(smem) > smem_set) {
+    FR_CUDA_TRY(cudaFuncSetAttribute(pr_pull_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+    smem_set = static_cast<int>(smem);
+  }
+  if (st->tail_damping != damping) {  // the tail's constant changed
+    st->tail_damping = damping;
+    st->tail_pending = 2;
+  }
   for (int i = 0; i < iters; ++i) {
     a.c_in = st->c[st->cur];
     a.c_out = st->c[st->cur ^ 1];
-    pr_binned_kernel<<<grid, kPrThreads, 0, s>>>(a);
+    a.do_tail = st->tail_pending > 0;
+    pr_pull_kernel<<<std::min(g->sms, kMaxCtas), kPrThreads, smem, s>>>(a);
+    if (st->tail_pending > 0) --st->tail_pending;
     st->cur ^= 1;
     st->iterations++;
   }
@@ -497,41 +729,47 @@ namespace {
 
 struct PrTask {
   fr_pagerank_task_config cfg{};
-  int32_t V = 0, n_blk = 0, n_hub = 0;
-  int64_t blk_len = 0;
-  int64_t E = 0;
-  int32_t *h_off = nullptr, *h_col = nullptr, *h_outdeg = nullptr, *h_blk = nullptr;
-  float* h_inv = nullptr;
+  fr_pr_graph shape;  // sizes, buckets and counts of the built graph (no device pointers)
+  int32_t *h_xoff = nullptr, *h_xcol = nullptr, *h_rowc = nullptr, *h_rowr = nullptr;
+  float* h_rinv = nullptr;
+  int4* h_chunks = nullptr;
   fr_pr_graph g;  // device view (owned through the task, freed with cudaFreeAsync)
   fr_pr_state st;
   bool on_gpu = false;
   cudaStream_t last = nullptr;
 };
 
+// The task keeps only what the step reads (not the original-order CSR).
 int pr_task_create(void* u) {
   auto* t = static_cast<PrTask*>(u);
-  if (t->h_off) return FR_OK;
+  if (t->h_xoff) return FR_OK;
   cudaStream_t s = nullptr;
   FR_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
   fr_pr_graph* g = nullptr;
   int rc = fr_pr_graph_rmat(t->cfg.scale, t->cfg.edge_factor, t->cfg.seed, s, &g);
   if (rc == FR_OK) {
-    t->V = g->V;
-    t->E = g->E;
-    t->n_blk = g->n_blk;
+    fr_pr_graph& sh = t->shape;
+    sh.V = g->V;
+    sh.E = g->E;
+    sh.n_chunk = g->n_chunk;
+    sh.n_split = g->n_split;
+    std::memcpy(sh.bstart, g->bstart, sizeof(sh.bstart));
+    std::memcpy(sh.istart, g->istart, sizeof(sh.istart));
+    std::memcpy(sh.cta_chunk, g->cta_chunk, sizeof(sh.cta_chunk));
+    sh.sms = g->sms;
     auto pin = [&](void** p, size_t bytes, const void* dev) {
       if (rc != FR_OK) return;
-      cudaError_t e = cudaMallocHost(p, std::max<size_t>(bytes, 4));
+      cudaError_t e = cudaMallocHost(p, std::max<size_t>(bytes, 16));
       if (e == cudaSuccess && bytes) e = cudaMemcpy(*p, dev, bytes, cudaMemcpyDeviceToHost);
       if (e != cudaSuccess) rc = frcapi::cuda_status(e, "pagerank host copy");
     };
-    pin(reinterpret_cast<void**>(&t->h_off), (size_t(t->V) + 1) * 4, g->offsets);
-    pin(reinterpret_cast<void**>(&t->h_col), size_t(t->E) * 4, g->col);
-    pin(reinterpret_cast<void**>(&t->h_outdeg), size_t(t->V) * 4, g->outdeg);
-    pin(reinterpret_cast<void**>(&t->h_inv), size_t(t->V) * 4, g->inv);
-    t->n_hub = g->n_hub;
-    t->blk_len = g->blk_len;
-    pin(reinterpret_cast<void**>(&t->h_blk), size_t(t->blk_len) * 4, g->blk);
+    const size_t V = static_cast<size_t>(g->V);
+    pin(reinterpret_cast<void**>(&t->h_xoff), (V + 1) * 4, g->xoff);
+    pin(reinterpret_cast<void**>(&t->h_xcol), size_t(g->E) * 4, g->xcol);
+    pin(reinterpret_cast<void**>(&t->h_rowc), V * 4, g->rowc);
+    pin(reinterpret_cast<void**>(&t->h_rowr), V * 4, g->rowr);
+    pin(reinterpret_cast<void**>(&t->h_rinv), V * 4, g->rinv);
+    pin(reinterpret_cast<void**>(&t->h_chunks), size_t(g->n_chunk) * sizeof(int4), g->chunks);
     fr_pr_graph_destroy(g);
   }
   cudaStreamDestroy(s);
@@ -543,27 +781,23 @@ int pr_task_init(void* u, void* stream) {
   auto s = static_cast<cudaStream_t>(stream);
   t->last = s;
   fr_pr_graph& g = t->g;
-  g.V = t->V;
-  g.E = t->E;
-  g.n_blk = t->n_blk;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&g.sms, cudaDevAttrMultiProcessorCount, dev);
+  g = t->shape;
+  const size_t V = static_cast<size_t>(g.V);
   auto up = [&](void** d, const void* h, size_t bytes) -> cudaError_t {
-    cudaError_t e = cudaMallocAsync(d, std::max<size_t>(bytes, 4), s);
+    cudaError_t e = cudaMallocAsync(d, std::max<size_t>(bytes, 16), s);
     if (e == cudaSuccess && bytes) e = cudaMemcpyAsync(*d, h, bytes, cudaMemcpyHostToDevice, s);
     return e;
   };
-  FR_CUDA_TRY(up(reinterpret_cast<void**>(&g.offsets), t->h_off, (size_t(t->V) + 1) * 4));
-  FR_CUDA_TRY(up(reinterpret_cast<void**>(&g.col), t->h_col, size_t(t->E) * 4));
-  FR_CUDA_TRY(up(reinterpret_cast<void**>(&g.outdeg), t->h_outdeg, size_t(t->V) * 4));
-  FR_CUDA_TRY(up(reinterpret_cast<void**>(&g.inv), t->h_inv, size_t(t->V) * 4));
-  g.n_hub = t->n_hub;
-  g.blk_len = t->blk_len;
-  FR_CUDA_TRY(up(reinterpret_cast<void**>(&g.blk), t->h_blk, size_t(t->blk_len) * 4));
+  FR_CUDA_TRY(up(reinterpret_cast<void**>(&g.xoff), t->h_xoff, (V + 1) * 4));
+  FR_CUDA_TRY(up(reinterpret_cast<void**>(&g.xcol), t->h_xcol, size_t(g.E) * 4));
+  FR_CUDA_TRY(up(reinterpret_cast<void**>(&g.rowc), t->h_rowc, V * 4));
+  FR_CUDA_TRY(up(reinterpret_cast<void**>(&g.rowr), t->h_rowr, V * 4));
+  FR_CUDA_TRY(up(reinterpret_cast<void**>(&g.rinv), t->h_rinv, V * 4));
+  FR_CUDA_TRY(up(reinterpret_cast<void**>(&g.chunks), t->h_chunks, size_t(g.n_chunk) * sizeof(int4)));
+  t->st = fr_pr_state{};
   t->st.g = &g;
   for (float** p : {&t->st.r, &t->st.c[0], &t->st.c[1]})
-    FR_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(p), size_t(t->V) * 4, s));
+    FR_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(p), std::max<size_t>(V, 4) * 4, s));
   t->on_gpu = true;
   return fr_pr_reset(&t->st, s);
 }
@@ -577,13 +811,14 @@ int pr_task_step(void* u, void* stream) {
 int pr_task_stop(void* u) {
   auto* t = static_cast<PrTask*>(u);
   if (!t->on_gpu) return FR_OK;
-  for (void* p : {static_cast<void*>(t->g.offsets), static_cast<void*>(t->g.col),
-                  static_cast<void*>(t->g.outdeg), static_cast<void*>(t->g.inv),
-                  static_cast<void*>(t->g.blk), static_cast<void*>(t->st.r),
-                  static_cast<void*>(t->st.c[0]), static_cast<void*>(t->st.c[1])})
+  for (void* p : {static_cast<void*>(t->g.xoff), static_cast<void*>(t->g.xcol),
+                  static_cast<void*>(t->g.rowc), static_cast<void*>(t->g.rowr),
+                  static_cast<void*>(t->g.rinv), static_cast<void*>(t->g.chunks),
+                  static_cast<void*>(t->st.r), static_cast<void*>(t->st.c[0]),
+                  static_cast<void*>(t->st.c[1])})
     if (p) FR_CUDA_TRY(cudaFreeAsync(p, t->last));
   t->g = fr_pr_graph{};
-  t->st = fr_pr_state{};
+  t->st.r = nullptr;
   t->on_gpu = false;
   return FR_OK;
 }
@@ -599,9 +834,9 @@ void pr_task_destroy(void* u) {
   if (t->last) cudaStreamSynchronize(t->last);
   pr_task_stop(t);
   if (t->last) cudaStreamSynchronize(t->last);
-  for (void* p : {static_cast<void*>(t->h_off), static_cast<void*>(t->h_col),
-                  static_cast<void*>(t->h_outdeg), static_cast<void*>(t->h_inv),
-                  static_cast<void*>(t->h_blk)})
+  for (void* p : {static_cast<void*>(t->h_xoff), static_cast<void*>(t->h_xcol),
+                  static_cast<void*>(t->h_rowc), static_cast<void*>(t->h_rowr),
+                  static_cast<void*>(t->h_rinv), static_cast<void*>(t->h_chunks)})
     if (p) cudaFreeHost(p);
   delete t;
 }
@@ -627,7 +862,7 @@ int fr_pagerank_task_create(const fr_pagerank_task_config* c, fr_side_task_vtabl
   vt->stop = pr_task_stop;
   vt->finished = pr_task_finished;
   vt->destroy = pr_task_destroy;
-  vt->work_units_per_step = static_cast<double>(t->E) * c->iters_per_step;  // edges
+  vt->work_units_per_step = static_cast<double>(t->shape.E) * c->iters_per_step;  // edges
   *user = t;
   return FR_OK;
 }
@@ -636,10 +871,12 @@ int fr_pagerank_task_info(void* user, int32_t* V, int64_t* E, double* memory_gib
                           const float** ranks, int64_t* iterations) {
   auto* t = static_cast<PrTask*>(user);
   if (!t) return frcapi::fail(FR_ERR_ARGUMENT, "null task");
-  if (V) *V = t->V;
-  if (E) *E = t->E;
+  const fr_pr_graph& g = t->shape;
+  if (V) *V = g.V;
+  if (E) *E = g.E;
+  // xoff + xcol + rowc/rowr/rinv + r + 2 c + chunk list
   if (memory_gib)
-    *memory_gib = (4.0 * (t->V + 1) + 4.0 * t->E + 4.0 * t->V * 5 + 4.0 * t->blk_len) /
+    *memory_gib = (4.0 * (g.V + 1) + 4.0 * g.E + 4.0 * g.V * 6 + 16.0 * g.n_chunk) /
                   (1024.0 * 1024.0 * 1024.0);
   if (ranks) *ranks = t->on_gpu ? t->st.r : nullptr;
   if (iterations) *iterations = t->st.iterations;

@@ -81,3 +81,31 @@ def test_pagerank_task_in_bubbles(g, sidetask_oracle):
     want = sidetask_oracle.pr_run(off, col, outdeg, iters, 0.85)
     assert np.abs(ranks.double().cpu().numpy() - want).sum() <= 1e-6
     h.close()
+
+
+def test_damping_change_rewrites_constant_rows(g, sidetask_oracle, rmat20):
+    """The zero-in-degree rows' rank (1-d)/V is written only while it may
+    change: after a reset and after a damping change (two launches each)."""
+    graph, (off, col, outdeg) = rmat20
+    st = g.PageRankState(graph)
+    st.reset()
+    st.step(3, 0.85)
+    st.step(1, 0.6)
+    st.step(3, 0.6)
+    got = st.ranks().double().cpu().numpy()
+    want = sidetask_oracle.pr_run(off, col, outdeg, 3, 0.85)
+    want = sidetask_oracle.pr_run(off, col, outdeg, 4, 0.6, r0=want)
+    assert np.abs(got - want).sum() <= 1e-6
+
+
+def test_reset_restarts(g, sidetask_oracle):
+    graph = g.PageRankGraph(scale=16, edge_factor=16, seed=11)
+    src, dst = sidetask_oracle.rmat_edges(16, 16, seed=11)
+    off, col, outdeg = sidetask_oracle.build_pull_csr(1 << 16, src, dst)
+    st = g.PageRankState(graph)
+    st.reset()
+    st.step(5, 0.85)
+    st.reset()
+    st.step(2, 0.85)
+    want = sidetask_oracle.pr_run(off, col, outdeg, 2, 0.85)
+    assert np.abs(st.ranks().double().cpu().numpy() - want).sum() <= 1e-6
