@@ -11,7 +11,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libfreeride.so")
+# FR_LIB: load another build of the library (A/B experiments only)
+LIB_PATH = os.environ.get("FR_LIB") or os.path.join(_HERE, "_lib", "libfreeride.so")
 REPO_ROOT = os.path.dirname(_HERE)
 
 _lock = threading.Lock()

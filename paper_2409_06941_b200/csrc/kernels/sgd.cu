@@ -105,15 +105,31 @@ __global__ void __launch_bounds__(kSgdThreads, MINB) sgd_step_kernel(
   // Warp-uniform trip count (the group shuffles need every lane present);
   // lanes whose edge is past the end ride along predicated off.
   const int64_t warp_first = group - lane / LN;
-  for (int64_t ew = e0 + warp_first; ew < e1; ew += 2 * G) {
+  // Software-pipelined: the next pair's (u, v, r) load while this pair's
+  // latent rows are in flight.
+  int64_t ew = e0 + warp_first;
+  int32_t u0 = 0, v0 = 0, u1 = 0, v1 = 0;
+  float r0 = 0.0f, r1 = 0.0f;
+  auto fetch = [&](int64_t base, int32_t& a0, int32_t& b0, float& q0, int32_t& a1, int32_t& b1,
+                   float& q1) {
+    const int64_t e = base + lane / LN, f = e + G;
+    const bool one = e < e1, two = f < e1;
+    a0 = one ? __ldg(&us[e]) : 0;
+    b0 = one ? __ldg(&vs[e]) : 0;
+    q0 = one ? __ldg(&rs[e]) : 0.0f;
+    a1 = two ? __ldg(&us[f]) : a0;
+    b1 = two ? __ldg(&vs[f]) : b0;
+    q1 = two ? __ldg(&rs[f]) : 0.0f;
+  };
+  if (ew < e1) fetch(ew, u0, v0, r0, u1, v1, r1);
+  for (; ew < e1; ew += 2 * G) {
     const int64_t e = ew + lane / LN, f = e + G;
     const bool one = e < e1, two = f < e1;
-    const int32_t u0 = one ? __ldg(&us[e]) : 0, v0 = one ? __ldg(&vs[e]) : 0;
-    const float r0 = one ? __ldg(&rs[e]) : 0.0f;
-    const int32_t u1 = two ? __ldg(&us[f]) : u0, v1 = two ? __ldg(&vs[f]) : v0;
-    const float r1 = two ? __ldg(&rs[f]) : 0.0f;
     const float4 a0 = L4[static_cast<int64_t>(u0) * LN + sub], b0 = L4[static_cast<int64_t>(v0) * LN + sub];
     const float4 a1 = L4[static_cast<int64_t>(u1) * LN + sub], b1 = L4[static_cast<int64_t>(v1) * LN + sub];
+    int32_t nu0 = 0, nv0 = 0, nu1 = 0, nv1 = 0;
+    float nr0 = 0.0f, nr1 = 0.0f;
+    if (ew + 2 * G < e1) fetch(ew + 2 * G, nu0, nv0, nr0, nu1, nv1, nr1);
     const float err0 = r0 - group_sum<K>(dot4(a0, b0));
     const float err1 = r1 - group_sum<K>(dot4(a1, b1));
     float4 da, db;
@@ -127,6 +143,7 @@ __global__ void __launch_bounds__(kSgdThreads, MINB) sgd_step_kernel(
       apply(&L4[static_cast<int64_t>(u1) * LN + sub], da);
       apply(&L4[static_cast<int64_t>(v1) * LN + sub], db);
     }
+    u0 = nu0; v0 = nv0; r0 = nr0; u1 = nu1; v1 = nv1; r1 = nr1;
   }
 }
 
