@@ -12,8 +12,10 @@ collective on the data path) -> scaling "weak".
 Headline workload (BASELINE.json configs[1]): the image resize + watermark
 side task (64 synthetic 4K RGB frames -> 1080p, RGBA watermark, 8 frames per
 RunNextStep).  The same run also measures configs[0] (PageRank, RMAT-20,
-one pull iteration per step) and configs[2] (Graph-SGD, Orkut shape, rank
-16, 2^20 edges per step) under "workloads".
+one pull iteration per step), configs[2] (Graph-SGD, Orkut shape, rank
+16, 2^20 edges per step), configs[3] (mixed, 3.6B-shaped stages) and the
+image task through the imperative interface (device-preempted workload)
+under "workloads".
 
 A bench *step* is one training iteration (epoch) of all 4 stages with the
 side task harvesting its bubbles.  Per stage and workload: the bubble
@@ -201,7 +203,7 @@ def ours(args):
     from paper_2409_06941_b200 import gpu
     gpu.glib()
     K, W = args.steps, args.warmup
-    names = ["image", "pagerank", "sgd"] + ([] if args.no_e2e else ["image_e2e"])
+    names = ["image", "image_imperative", "pagerank", "sgd"] + ([] if args.no_e2e else ["image_e2e"])
     runs = {n: [] for n in names}
     stage_prof = []
     if dist:
@@ -214,6 +216,8 @@ def ours(args):
             for n in names:
                 if n == "image":
                     task = gpu.ImageTask(batch=BATCH, images_per_step=IMAGES_PER_STEP, **FRAMES)
+                elif n == "image_imperative":
+                    task = gpu.ImageTask(batch=BATCH, images_per_step=IMAGES_PER_STEP, imperative=True, **FRAMES)
                 elif n == "image_e2e":
                     task = gpu.ImageTask(batch=BATCH, images_per_step=E2E_IMAGES_PER_STEP, host_io=True, **FRAMES)
                 elif n == "pagerank":
@@ -234,6 +238,7 @@ def ours(args):
                     used=sum(r["with"]["used_s"] for r in rs),
                     bubble_with=sum(r["with"]["bubble_s"] for r in rs),
                     overrun=sum(r["with"]["overrun_s"] for r in rs),
+                    pauses=sum(r["with"]["pauses"] for r in rs),
                     steps=sum(r["with"]["steps_completed"] for r in rs),
                     launches=sum(r["side"] for r in rs),
                     mean_step_s=statistics.fmean(d for r in rs for d in r["durs"]) if any(r["durs"] for r in rs) else None,
@@ -357,6 +362,17 @@ def emit(args, results, ws, names, csr):
                 "roofline": roof("sgd", "sgd_step_kernel<16> (2^20 edges/launch, in-pipeline)"),
                 "cpu_baseline": cpu_sgd(args.cpu_seconds / 2) if not args.no_cpu else None},
     }
+    imp = results[0]["image_imperative"]
+    workloads["image_imperative"] = {
+        "config": "configs[1] through the imperative interface (RunGpuWorkload): one preemptible K5 "
+                  "workload per bubble over the 64-frame batch, paused on the device per output row",
+        "value": rate("image_imperative"), "unit": UNIT, "dT": dT("image_imperative"),
+        "fill": fill("image_imperative"),
+        "overrun_per_pause_us": sum(r["image_imperative"]["overrun"] for r in results)
+        / max(1, sum(r["image_imperative"]["pauses"] for r in results)) * 1e6,
+        "alg_GBps_in_bubbles": imp["units"] / OUT_PX * (FRAMES["sw"] * FRAMES["sh"] * 3 + OUT_PX * 3)
+        / max(1e-12, imp["used"] + imp["overrun"]) / 1e9,
+        "workload_launches": imp["launches"]}
     launches = sum(r[n]["launches"] for r in results for n in names) + sum(r["gap_kernels"] for r in results)
     line = {
         "metric": METRIC, "value": rate("image"), "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": W,

@@ -32,6 +32,17 @@ int fr_memcpy(void* dst, const void* src, int64_t bytes);
 /* diagnostics: spin `cycles` SM clocks on one warp, write {cycles, ns} */
 int fr_clock_probe(uint64_t* out_cycles_ns, int64_t cycles, void* stream);
 
+/* Device-side preemption for the imperative interface: the workload stops
+ * taking new work items once *stop_word >= token.  The harness's gap kernel
+ * raises stop_word (device memory, gpu-scope) at the instant the next op's
+ * dependency arrives, i.e. the bubble end, so the pause reaches the GPU
+ * without a host round trip and lands within one work item. */
+typedef struct fr_preempt {
+  const uint32_t* stop_word; /* device pointer, read with ld.relaxed.gpu */
+  uint32_t token;
+  uint32_t reserved;
+} fr_preempt;
+
 /* ------------------------------------------- K5: image resize + watermark */
 /* Plan for one (src WxH -> dst WxH) shape.  Coefficients follow cv2's
  * INTER_LINEAR_EXACT (8-bit fixed point, half-pixel centres); the plan picks
@@ -56,6 +67,17 @@ int fr_img_prepare_watermark(const fr_img_plan* plan, const uint8_t* wm_rgba, vo
                              void* stream);
 int fr_img_resize_watermark_prepared(const fr_img_plan* plan, const uint8_t* src, uint8_t* dst,
                                      const void* prepared, int32_t n, void* stream);
+/* Preemptible K5 over a resident batch of n frames (fast 2x path only):
+ * takes up to max_rows output rows, row (base + t) mod (n * dh) for the
+ * t-th row taken, base = counters[0] -- so a launch may loop over the batch
+ * and the next launch resumes at the first row this one did not take.
+ * counters: 8 x uint32 of zeroed device memory owned by the caller (the
+ * cursor, scheduler state, and counters[2..3] = rows completed, uint64).
+ * Stops taking rows once *preempt->stop_word >= preempt->token (preempt may
+ * be null); every row taken is completed before the launch ends. */
+int fr_img_resize_watermark_preemptible(const fr_img_plan* plan, const uint8_t* src, uint8_t* dst,
+                                        const void* prepared, int32_t n, uint32_t* counters,
+                                        int64_t max_rows, const fr_preempt* preempt, void* stream);
 /* synthetic inputs (same counter-based arithmetic as oracle/sidetasks.c) */
 int fr_img_generate(uint8_t* dst, int32_t n, int32_t w, int32_t h, int32_t channels,
                     uint64_t seed, int32_t first_index, void* stream);
@@ -122,6 +144,17 @@ typedef struct fr_side_task_vtable {
   int (*finished)(void* user, int64_t steps_completed, int32_t* done);
   void (*destroy)(void* user);
   double work_units_per_step; /* px, edges, ... reported per completed step */
+  /* Imperative interface (PAPER.md:484-499 RunGpuWorkload; task.hpp:93
+   * imperative_run): interface_kind = FR_IMPERATIVE makes
+   * the worker call run_gpu_workload from StartSideTask until the pause
+   * instead of gated RunNextStep calls.  run_gpu_workload enqueues one
+   * preemptible launch on `stream` (it returns when the work is done or the
+   * preempt word fires, keeping its progress for the next call); work_done
+   * reports cumulative completed work units (may synchronise `stream`). */
+  int32_t interface_kind;     /* enum fr_interface: FR_ITERATIVE = 0, FR_IMPERATIVE = 1 */
+  int32_t reserved;
+  int (*run_gpu_workload)(void* user, void* stream, const fr_preempt* preempt);
+  int (*work_done)(void* user, void* stream, double* units);
 } fr_side_task_vtable;
 
 /* Built-in side tasks (kernels above) behind the vtable. */
@@ -130,7 +163,9 @@ typedef struct fr_image_task_config {
   int32_t batch;                /* images resident (device) or staged (host mode) */
   int32_t images_per_step;      /* one RunNextStep = this many images */
   int32_t host_io;              /* 1: inputs in pinned host memory, H2D/D2H per step */
-  int32_t reserved;
+  int32_t interface_kind;       /* FR_ITERATIVE: steps of images_per_step frames;
+                                   FR_IMPERATIVE: one preemptible workload over the
+                                   whole batch, paused on the device per output row */
   uint64_t seed;
   int64_t total_steps;          /* <= 0: unbounded */
 } fr_image_task_config;

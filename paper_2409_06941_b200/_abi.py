@@ -439,6 +439,7 @@ GPU_PROTOTYPES = {
     "fr_img_prepared_bytes": (C.c_int, [vp, P(i64)]),
     "fr_img_prepare_watermark": (C.c_int, [vp, vp, vp, vp]),
     "fr_img_resize_watermark_prepared": (C.c_int, [vp, vp, vp, vp, i32, vp]),
+    "fr_img_resize_watermark_preemptible": (C.c_int, [vp, vp, vp, vp, i32, vp, i64, vp, vp]),
     "fr_img_generate": (C.c_int, [vp, i32, i32, i32, i32, u64, i32, vp]),
     "fr_img_generate_watermark": (C.c_int, [vp, i32, i32, u64, vp]),
 }
@@ -455,13 +456,21 @@ class SideTaskVTableC(Struct):
         ("finished", C.CFUNCTYPE(C.c_int, vp, C.c_int64, P(i32))),
         ("destroy", C.CFUNCTYPE(None, vp)),
         ("work_units_per_step", C.c_double),
+        ("interface_kind", i32),
+        ("reserved", i32),
+        ("run_gpu_workload", C.CFUNCTYPE(C.c_int, vp, vp, vp)),
+        ("work_done", C.CFUNCTYPE(C.c_int, vp, vp, P(C.c_double))),
     ]
+
+
+class PreemptC(Struct):
+    _fields_ = [("stop_word", vp), ("token", C.c_uint32), ("reserved", C.c_uint32)]
 
 
 class ImageTaskConfigC(Struct):
     _fields_ = [
         ("sw", i32), ("sh", i32), ("dw", i32), ("dh", i32),
-        ("batch", i32), ("images_per_step", i32), ("host_io", i32), ("reserved", i32),
+        ("batch", i32), ("images_per_step", i32), ("host_io", i32), ("interface_kind", i32),
         ("seed", u64), ("total_steps", i64),
     ]
 

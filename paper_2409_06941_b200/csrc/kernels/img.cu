@@ -71,11 +71,21 @@ __global__ void img_prepare_wm_kernel(const uint8_t* __restrict__ wm, uint4* __r
 // tail of the previous GEMM), and with a static split the CTAs that could
 // not become resident would run their whole share as a serial tail.  The
 // last CTA to exit re-arms the counters for the next launch on the stream.
-template <int S>
+//
+// PREEMPT (imperative interface): before taking a row the elected thread
+// reads the stop word (gpu scope); once it reaches `token` no further row is
+// taken, the rows already in the smem ring finish, and the CTA exits.  Rows
+// are taken from a per-launch count t (counters[4]) as row (base + t) mod
+// rows, base = counters[0], at most `budget` per launch, so one launch can
+// loop over the batch several times; the last CTA out advances base by the
+// rows taken, so the next launch resumes at the first untaken row, and adds
+// them to counters[2..3] (every taken row is completed before exit).
+template <int S, bool PREEMPT>
 __global__ void __launch_bounds__(kImgThreads, kImgCtasPerSm)
     img_resize2x_wm_tma(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
                         const uint4* __restrict__ wmp, int dw, int dh, uint32_t rows,
-                        uint32_t* __restrict__ counters) {
+                        uint32_t* __restrict__ counters, const uint32_t* __restrict__ stop_word,
+                        uint32_t token, uint32_t budget) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint32_t row_of[S], y_of[S];
   const uint32_t src_row = 6u * static_cast<uint32_t>(dw);  // one source row, RGB
@@ -108,18 +118,28 @@ __global__ void __launch_bounds__(kImgThreads, kImgCtasPerSm)
                   src + (static_cast<uint64_t>(img) * 2 * dh + 2 * y) * src_row, 2u * src_row,
                   &full[s], pol_stream);
   };
+  const uint32_t base = PREEMPT ? counters[0] : 0u;  // advanced only after this launch
+  auto take = [&]() -> uint32_t {
+    if (!PREEMPT) return atomicAdd(&counters[0], 1u);
+    if (frk::ld_relaxed_gpu(stop_word) >= token) return rows;  // paused: no new row
+    const uint32_t t = atomicAdd(&counters[4], 1u);
+    if (t >= budget) return rows;
+    const uint32_t r = base + t;  // base < rows, t < budget < 2^31
+    return r % rows;
+  };
   if (tid == 0)
-    for (int s = 0; s < S; ++s) grab(s, atomicAdd(&counters[0], 1u));
+    for (int s = 0; s < S; ++s) grab(s, take());
   __syncthreads();
 
-  for (uint32_t k = 0;; ++k) {
+  uint32_t k = 0;
+  for (;; ++k) {
     const int s = static_cast<int>(k % S);
     const uint32_t row = row_of[s];  // written >= S-1 barriers ago (or before the first)
     if (row >= rows) break;          // rows are grabbed in increasing order: all done
     const uint32_t y = y_of[s];
     // the elected thread's next row: the atomic's round trip overlaps this
     // row's compute instead of delaying the refill after the barrier
-    const uint32_t next_row = tid == 0 ? atomicAdd(&counters[0], 1u) : 0u;
+    const uint32_t next_row = tid == 0 ? take() : 0u;
     uint8_t* st = smem + s * stage_bytes;
     const uint8_t* ra = st;
     const uint8_t* rb = st + src_row;
@@ -192,9 +212,16 @@ __global__ void __launch_bounds__(kImgThreads, kImgCtasPerSm)
   }
   if (tid == 0) {
     frk::bulk_wait<0>();
+    if (PREEMPT) atomicAdd(reinterpret_cast<unsigned long long*>(counters + 2), k);
     __threadfence();
     if (atomicAdd(&counters[1], 1u) == gridDim.x - 1) {  // last CTA out re-arms
-      counters[0] = 0;
+      if (PREEMPT) {
+        const uint32_t taken = min(atomicAdd(&counters[4], 0u), budget);
+        counters[0] = static_cast<uint32_t>((static_cast<uint64_t>(base) + taken) % rows);
+        counters[4] = 0;
+      } else {
+        counters[0] = 0;
+      }
       counters[1] = 0;
     }
   }
@@ -330,12 +357,14 @@ int fr_img_plan_create(int32_t sw, int32_t sh, int32_t dw, int32_t dh, fr_img_pl
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     if (plan->smem <= optin) {
-      e = cudaFuncSetAttribute(img_resize2x_wm_tma<kImgStages>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, plan->smem);
-      if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(img_resize2x_wm_tma<kImgStages>,
-                                 cudaFuncAttributePreferredSharedMemoryCarveout,
-                                 cudaSharedmemCarveoutMaxShared);
+      for (const void* fn : {reinterpret_cast<const void*>(img_resize2x_wm_tma<kImgStages, false>),
+                             reinterpret_cast<const void*>(img_resize2x_wm_tma<kImgStages, true>)}) {
+        if (e == cudaSuccess)
+          e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, plan->smem);
+        if (e == cudaSuccess)
+          e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                   cudaSharedmemCarveoutMaxShared);
+      }
       if (e != cudaSuccess) {
         delete plan;
         return frcapi::cuda_status(e, "cudaFuncSetAttribute(img_resize2x_wm_tma)");
@@ -414,9 +443,9 @@ int fr_img_resize_watermark_prepared(const fr_img_plan* plan, const uint8_t* src
     const int64_t rows = static_cast<int64_t>(n) * plan->dh;
     if (rows >= (int64_t{1} << 31)) return frcapi::fail(FR_ERR_UNSUPPORTED, "too many rows in one step");
     const int grid = static_cast<int>(std::min<int64_t>(rows, int64_t(plan->sms) * kImgCtasPerSm));
-    img_resize2x_wm_tma<kImgStages><<<grid, kImgThreads, plan->smem, s>>>(
+    img_resize2x_wm_tma<kImgStages, false><<<grid, kImgThreads, plan->smem, s>>>(
         src, dst, static_cast<const uint4*>(prepared), plan->dw, plan->dh, static_cast<uint32_t>(rows),
-        plan->d_ctr);
+        plan->d_ctr, nullptr, 0u, 0u);
   } else {
     const int64_t total = static_cast<int64_t>(n) * plan->dw * plan->dh;
     img_resize_wm_general<<<grid_for(total, 256, 8), 256, 0, s>>>(
@@ -424,6 +453,34 @@ int fr_img_resize_watermark_prepared(const fr_img_plan* plan, const uint8_t* src
         plan->dh, total);
   }
   FR_CUDA_LAUNCHED("img_resize_watermark");
+  return FR_OK;
+}
+
+int fr_img_resize_watermark_preemptible(const fr_img_plan* plan, const uint8_t* src, uint8_t* dst,
+                                        const void* prepared, int32_t n, uint32_t* counters,
+                                        int64_t max_rows, const fr_preempt* preempt, void* stream) {
+  if (!plan || !counters || (n > 0 && (!src || !dst || !prepared)))
+    return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  if (plan->path != FR_IMG_PATH_TMA_2X)
+    return frcapi::fail(FR_ERR_UNSUPPORTED, "preemptible path needs the exact-2x TMA plan");
+  if (n < 0) return frcapi::fail(FR_ERR_VALIDATION, "n must be >= 0", "n");
+  if (n == 0) return FR_OK;
+  if (!aligned16(src) || !aligned16(dst) || !aligned16(prepared) ||
+      (reinterpret_cast<uintptr_t>(counters) & 7u))
+    return frcapi::fail(FR_ERR_UNSUPPORTED, "TMA path needs 16-byte aligned buffers");
+  const int64_t rows = static_cast<int64_t>(n) * plan->dh;
+  if (rows >= (int64_t{1} << 31)) return frcapi::fail(FR_ERR_UNSUPPORTED, "too many rows in one launch");
+  if (max_rows < 0 || max_rows >= (int64_t{1} << 31))
+    return frcapi::fail(FR_ERR_VALIDATION, "max_rows in [0, 2^31)", "max_rows");
+  if (max_rows == 0) return FR_OK;
+  const int grid = static_cast<int>(std::min<int64_t>(max_rows, int64_t(plan->sms) * kImgCtasPerSm));
+  // no preempt: a stop word that never fires (counters[5] stays 0 < token)
+  const uint32_t* word = preempt && preempt->stop_word ? preempt->stop_word : counters + 5;
+  const uint32_t token = preempt && preempt->stop_word ? preempt->token : 0xFFFFFFFFu;
+  img_resize2x_wm_tma<kImgStages, true><<<grid, kImgThreads, plan->smem, static_cast<cudaStream_t>(stream)>>>(
+      src, dst, static_cast<const uint4*>(prepared), plan->dw, plan->dh, static_cast<uint32_t>(rows),
+      counters, word, token, static_cast<uint32_t>(max_rows));
+  FR_CUDA_LAUNCHED("img_resize_watermark_preemptible");
   return FR_OK;
 }
 

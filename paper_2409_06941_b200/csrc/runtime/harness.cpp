@@ -15,7 +15,13 @@
 //    queued back to back without idling the GPU between them;
 //  * a pause takes effect when the in-flight steps drain (last_paused is the
 //    drain time) and framework_enforce (limits.cpp:21-26) judges it after the
-//    grace period.
+//    grace period;
+//  * imperative tasks (vtable interface_kind = FR_IMPERATIVE, imperative_run
+//    task.cpp:102-106) run one preemptible GPU workload from StartSideTask on;
+//    the pause is delivered on the device: the gap kernel that observes the
+//    next op's dependency raises the bubble-end word the workload polls
+//    between work items, so it lands within one work item (SPEC.md:170 allows
+//    one kernel) without waiting for the host to see BubbleEnded.
 // Everything is timed on the device (globaltimer / CUDA events).
 #include <cuda_runtime.h>
 
@@ -74,6 +80,7 @@ struct Task {
   SideTaskRuntime rt;
   TaskProfile prof;
   bool initializing = false;
+  bool imperative() const { return vt.interface_kind == FR_IMPERATIVE; }
   cudaEvent_t init_a = nullptr, init_b = nullptr;
   bool init_recorded = false;
   ~Task() {
@@ -320,6 +327,7 @@ double elapsed_s(cudaEvent_t a, cudaEvent_t b) {
 void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
   pool_used = 0;
   std::memset(ring, 0, sizeof(RingSlot) * kRingSlots);
+  ck(cudaMemset(&ctl->end_seq, 0, sizeof(ctl->end_seq)), "end_seq reset");
   calibrate();
   ck(cudaDeviceSynchronize(), "pre-run sync");
   const int nops = static_cast<int>(ops.size());
@@ -370,6 +378,7 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
             a.slot_end = slot++;
             a.code_start = ring_code(kEvBubbleStart, id);
             a.code_end = ring_code(kEvBubbleEnd, id);
+            a.end_token = id + 1;  // bubble ids grow monotonically through the run
           }
           a.span_ns = span;
           if (g < nops) {
@@ -413,6 +422,15 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
   const int depth = std::max(1, cfg.max_inflight_steps);
 
   auto task_of = [&](const std::string& id) -> Task& { return *tasks.at(id); };
+  // imperative work is counted by the workload itself (rows, pixels, ...)
+  std::map<Task*, double> work_before;
+  for (auto& kv : tasks)
+    if (kv.second->imperative() && kv.second->vt.work_done && with_tasks) {
+      double u = 0;
+      hook(kv.second->vt.work_done(kv.second->user, side, &u), "work_done");
+      work_before[kv.second.get()] = u;
+    }
+  std::uint32_t cur_token = 0;  // bubble-end token the running imperative workload stops at
   auto stop_task = [&](Task& t, Tick now) {
     apply_transition(t.rt, TransitionKind::StopSideTask, now);
     hook(t.vt.stop ? t.vt.stop(t.user) : FR_OK, "stop");
@@ -427,17 +445,17 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
       Task* st = steps[inflight.front()].task;
       inflight.pop_front();
       ++completed;
-      units += st->vt.work_units_per_step;  // the completing step's own task
-      st->rt.steps_completed++;  // counted at step end (task.hpp:55)
+      if (!st->imperative()) units += st->vt.work_units_per_step;  // the completing step's own task
+      st->rt.steps_completed++;  // counted at step end (task.hpp:55); imperative: kernels
       // Re-anchor the projection: the next queued step started when this one
       // ended (~now), so drift from mis-estimated step times cannot build up.
-      if (!inflight.empty()) {
+      if (!inflight.empty() && !st->imperative()) {
         const double est = gate_est(*st);
         proj_end_dev = std::max<std::int64_t>(
             proj_end_dev, dev_now() + static_cast<std::int64_t>(std::llround(est / kTick)) *
                                           static_cast<std::int64_t>(inflight.size()));
       }
-      if (running) {
+      if (running && !running->imperative()) {
         int32_t done = 0;
         if (running->vt.finished) hook(running->vt.finished(running->user, running->rt.steps_completed, &done), "finished");
         if (done) stop_task(*running, dev_now());
@@ -496,6 +514,7 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
         bubble_end_dev = t_dev + pb.duration;  // StartSideTask carries the bubble end
         proj_end_dev = 0;
         gate_closed = false;
+        cur_token = id + 1;
       }
     }
   };
@@ -546,8 +565,25 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
       drain_completions();
       finish_init();
       finish_pause();
-      // 3. dispatch: the program-directed gate at the projected start time
-      while (running && !pause_pending && !gate_closed &&
+      // 3a. imperative: one preemptible workload at a time (each loops over
+      // its input until the device-side stop; a queued second launch would
+      // only run -- and exit -- after the next op has taken the SMs)
+      while (running && running->imperative() && !pause_pending &&
+             running->rt.state == SideTaskState::Running && inflight.empty()) {
+        const std::int64_t h0 = host_ns();
+        imperative_run(running->rt, h0 + clock_off, 0);  // RUNNING precondition (task.cpp:102)
+        fr_preempt pre{&ctl->end_seq, cur_token, 0};
+        StepRec r{ev(), ev(), running};
+        ck(cudaEventRecord(r.a, side), "record");
+        hook(running->vt.run_gpu_workload(running->user, side, &pre), "run_gpu_workload");
+        ck(cudaEventRecord(r.b, side), "record");
+        steps.push_back(r);
+        inflight.push_back(steps.size() - 1);
+        ++launched;
+        dispatch_ns += static_cast<double>(host_ns() - h0);
+      }
+      // 3b. iterative dispatch: the program-directed gate at the projected start time
+      while (running && !running->imperative() && !pause_pending && !gate_closed &&
              running->rt.state == SideTaskState::Running &&
              static_cast<int>(inflight.size()) < depth) {
         const std::int64_t h0 = host_ns();
@@ -589,6 +625,11 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
   ck(cudaStreamSynchronize(side), "side sync");
   drain_completions();
   finish_init();
+  for (auto& [t, before] : work_before) {
+    double u = before;
+    hook(t->vt.work_done(t->user, side, &u), "work_done");
+    units += u - before;
+  }
 
   // ---- device-timed accounting
   op_se.clear();
@@ -756,7 +797,7 @@ int fr_harness_stage_bubbles(const fr_harness* h, fr_bubble* out, int32_t cap, i
 int fr_harness_submit(fr_harness* h, const char* task_id, const fr_side_task_vtable* vt,
                       void* user, double mem, int32_t profile_steps, fr_task_profile* prof_out,
                       int32_t* assigned) {
-  if (!h || !task_id || !vt || !vt->run_next_step || !vt->init)
+  if (!h || !task_id || !vt || !vt->init || (!vt->run_next_step && vt->interface_kind != FR_IMPERATIVE))
     return frcapi::fail(FR_ERR_ARGUMENT, "null argument / missing hook");
   if (h->tasks.count(task_id)) return frcapi::fail(FR_ERR_VALIDATION, "duplicate task id", "id");
   auto t = std::make_unique<Task>();
@@ -768,10 +809,14 @@ int fr_harness_submit(fr_harness* h, const char* task_id, const fr_side_task_vta
     t->rt.spec.memory_demand = mem;
     // profile_task (profiler.hpp:41): run the body standalone, time each
     // RunNextStep on the device, est = mean, max = worst (ns ticks).
+    const bool imperative = vt->interface_kind == FR_IMPERATIVE;
+    if (imperative && (!vt->run_gpu_workload || !vt->work_done))
+      throw HookError(FR_ERR_ARGUMENT, "imperative task without run_gpu_workload / work_done");
+    t->rt.spec.interface_kind = imperative ? TaskInterface::Imperative : TaskInterface::Iterative;
     hook(vt->create ? vt->create(user) : FR_OK, "create");
     hook(vt->init(user, h->side), "init");
-    const int n = std::max(1, profile_steps);
-    for (int i = 0; i < 2; ++i) hook(vt->run_next_step(user, h->side), "run_next_step");
+    const int n = imperative ? 0 : std::max(1, profile_steps);
+    for (int i = 0; i < (imperative ? 0 : 2); ++i) hook(vt->run_next_step(user, h->side), "run_next_step");
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs;
     for (int i = 0; i < n; ++i) {
       cudaEvent_t a = h->ev(), b = h->ev();
@@ -792,8 +837,10 @@ int fr_harness_submit(fr_harness* h, const char* task_id, const fr_side_task_vta
     TaskProfile p;
     p.task_id = task_id;
     p.profiled_steps = n;
-    p.est_per_step_duration = ticks_to_seconds(busy, kTick) / n;
-    p.max_per_step_duration = ticks_to_seconds(longest, kTick);
+    if (!imperative) {  // the profiler does not time imperative tasks
+      p.est_per_step_duration = ticks_to_seconds(busy, kTick) / n;
+      p.max_per_step_duration = ticks_to_seconds(longest, kTick);
+    }
     p.est_memory = mem;
     t->prof = p;
     const SubmitOutcome o = submit_task(p, h->workers);  // Alg. 1

@@ -7,6 +7,7 @@
 // training stream's host thread.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
 #include <new>
 
@@ -24,6 +25,8 @@ struct ImageTask {
   void* wmp = nullptr;  // prepared watermark (fr_img_prepare_watermark)
   uint8_t* h_src = nullptr;  // pinned host batch (host_io)
   uint8_t* h_dst = nullptr;
+  uint32_t* ctr = nullptr;   // imperative: preemptible row cursor + rows completed
+  uint64_t rows_base = 0;    // rows completed by earlier Init..Stop lifetimes
   int64_t cursor = 0;
   int64_t steps = 0;
   cudaStream_t last = nullptr;
@@ -38,8 +41,14 @@ int cu(cudaError_t e, const char* what) {
 
 int release(ImageTask* t, cudaStream_t s) {
   int rc = FR_OK;
+  if (t->ctr) {  // keep the completed-row count across Stop/Init
+    uint64_t done = 0;
+    if (cudaMemcpyAsync(&done, t->ctr + 2, sizeof(done), cudaMemcpyDeviceToHost, s) == cudaSuccess &&
+        cudaStreamSynchronize(s) == cudaSuccess)
+      t->rows_base += done;
+  }
   for (void** p : {reinterpret_cast<void**>(&t->src), reinterpret_cast<void**>(&t->dst),
-                   reinterpret_cast<void**>(&t->wm), &t->wmp})
+                   reinterpret_cast<void**>(&t->wm), &t->wmp, reinterpret_cast<void**>(&t->ctr)})
     if (*p) {
       if (rc == FR_OK) rc = cu(cudaFreeAsync(*p, s), "cudaFreeAsync");
       *p = nullptr;
@@ -67,6 +76,10 @@ int img_init(void* u, void* stream) {
   if (rc == FR_OK) rc = cu(cudaMallocAsync(&t->wmp, static_cast<std::size_t>(pbytes), s), "prepared wm");
   if (rc == FR_OK) rc = fr_img_generate_watermark(t->wm, c.dw, c.dh, c.seed ^ 0x77ull, s);
   if (rc == FR_OK) rc = fr_img_prepare_watermark(t->plan, t->wm, t->wmp, s);
+  if (rc == FR_OK && c.interface_kind == FR_IMPERATIVE) {
+    rc = cu(cudaMallocAsync(reinterpret_cast<void**>(&t->ctr), 8 * sizeof(uint32_t), s), "counters");
+    if (rc == FR_OK) rc = cu(cudaMemsetAsync(t->ctr, 0, 8 * sizeof(uint32_t), s), "counters");
+  }
   if (rc != FR_OK) return rc;
   if (!c.host_io) return fr_img_generate(t->src, c.batch, c.sw, c.sh, 3, c.seed, 0, s);
   if (!t->h_src) {  // host frames: generated once, kept across Stop/Init cycles
@@ -99,6 +112,33 @@ int img_step(void* u, void* stream) {
   if (rc != FR_OK) return rc;
   t->cursor = (i0 + n) % c.batch;
   t->steps++;
+  return FR_OK;
+}
+
+// Imperative: one preemptible launch of up to kWorkloadPasses passes over
+// the batch; it resumes at the first row the previous launch did not take
+// and stops taking rows when the stage's bubble-end word reaches the token.
+constexpr int64_t kWorkloadPasses = 4;
+
+int img_workload(void* u, void* stream, const fr_preempt* pre) {
+  auto* t = static_cast<ImageTask*>(u);
+  t->last = static_cast<cudaStream_t>(stream);
+  const int64_t rows = static_cast<int64_t>(t->cfg.batch) * t->cfg.dh;
+  return fr_img_resize_watermark_preemptible(t->plan, t->src, t->dst, t->wmp, t->cfg.batch, t->ctr,
+                                             std::min<int64_t>(kWorkloadPasses * rows, (int64_t{1} << 31) - 1),
+                                             pre, stream);
+}
+
+int img_work_done(void* u, void* stream, double* units) {
+  auto* t = static_cast<ImageTask*>(u);
+  uint64_t done = 0;
+  if (t->ctr) {
+    auto s = static_cast<cudaStream_t>(stream);
+    int rc = cu(cudaMemcpyAsync(&done, t->ctr + 2, sizeof(done), cudaMemcpyDeviceToHost, s), "rows done");
+    if (rc == FR_OK) rc = cu(cudaStreamSynchronize(s), "rows done");
+    if (rc != FR_OK) return rc;
+  }
+  *units = static_cast<double>(t->rows_base + done) * t->cfg.dw;  // output pixels
   return FR_OK;
 }
 
@@ -140,6 +180,10 @@ int fr_image_task_create(const fr_image_task_config* c, fr_side_task_vtable* vt,
   if (!c || !vt || !user) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
   if (c->batch < 1 || c->images_per_step < 1 || c->batch % c->images_per_step != 0)
     return frcapi::fail(FR_ERR_VALIDATION, "batch must be a positive multiple of images_per_step", "images_per_step");
+  if (c->interface_kind != FR_ITERATIVE && c->interface_kind != FR_IMPERATIVE)
+    return frcapi::fail(FR_ERR_VALIDATION, "interface_kind must be FR_ITERATIVE or FR_IMPERATIVE", "interface_kind");
+  if (c->interface_kind == FR_IMPERATIVE && c->host_io)
+    return frcapi::fail(FR_ERR_UNSUPPORTED, "the imperative image task keeps its batch resident (host_io = 0)");
   auto* t = new (std::nothrow) ImageTask;
   if (!t) return frcapi::fail(FR_ERR_INVARIANT, "out of host memory");
   t->cfg = *c;
@@ -151,6 +195,11 @@ int fr_image_task_create(const fr_image_task_config* c, fr_side_task_vtable* vt,
   vt->finished = img_finished;
   vt->destroy = img_destroy;
   vt->work_units_per_step = double(c->images_per_step) * c->dw * c->dh;  // output pixels
+  if (c->interface_kind == FR_IMPERATIVE) {
+    vt->interface_kind = FR_IMPERATIVE;
+    vt->run_gpu_workload = img_workload;
+    vt->work_done = img_work_done;
+  }
   *user = t;
   return FR_OK;
 }

@@ -45,6 +45,9 @@ __global__ void gap_kernel(GapArgs a) {
   }
   if (a.mode == 1) a.ctl->base_ns = target;
   a.ctl->last_ns = t;
+  // device-side pause of an imperative workload: its CTAs poll end_seq
+  // before taking each work item (fr_preempt), no host round trip
+  if (a.end_token) frk::st_relaxed_gpu(&a.ctl->end_seq, a.end_token);
   if (a.slot_end >= 0) publish(a.ring, a.ring_mask, a.slot_end, a.code_end, t);
 }
 

@@ -27,8 +27,10 @@ inline std::uint32_t ring_code(std::uint32_t kind, std::uint32_t bubble) {
 }
 
 struct TimelineCtl {
-  std::uint64_t base_ns;  // start of the current epoch (device clock)
+  std::uint64_t base_ns;   // start of the current epoch (device clock)
   std::uint64_t last_ns;
+  std::uint32_t end_seq;   // token of the last bubble that ended (imperative preemption)
+  std::uint32_t pad[3];
 };
 
 struct GapArgs {
@@ -42,6 +44,7 @@ struct GapArgs {
   std::int64_t ready_ns;     // dependency ready, relative to the epoch base
   std::int64_t span_ns;      // epoch span (epoch-end gaps)
   std::int32_t mode;         // 0: before an op, 1: epoch end, 2: first epoch begin
+  std::uint32_t end_token;   // > 0: raise ctl->end_seq to this at the bubble end
 };
 
 void configure_timeline_kernels();

@@ -100,6 +100,25 @@ class ImagePlan:
                                                       _stream(stream)))
         return dst
 
+    def run_preemptible(self, src, dst, prepared, counters, stop_word=None, token=0, max_rows=None,
+                        stream=None):
+        """Preemptible K5 (imperative interface): takes up to max_rows rows
+        (default: one pass) starting at row counters[0] (mod n*dh), stops
+        taking rows once stop_word[0] >= token; counters is a zeroed int32
+        tensor of 8 (counters[2:4] = rows completed, uint64)."""
+        n = src.shape[0]
+        if tuple(src.shape[1:]) != (self.sh, self.sw, 3) or tuple(dst.shape) != (n, self.dh, self.dw, 3):
+            raise ValueError("image shapes do not match the plan")
+        pre = None
+        if stop_word is not None:
+            pre = A.PreemptC(stop_word=stop_word.data_ptr(), token=token)
+        if max_rows is None:
+            max_rows = n * self.dh
+        check(glib().fr_img_resize_watermark_preemptible(
+            self._h, _ptr(src), _ptr(dst), _ptr(prepared), n, _ptr(counters), max_rows,
+            C.byref(pre) if pre is not None else None, _stream(stream)))
+        return dst
+
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value and _glib is not None:
@@ -118,10 +137,13 @@ class ImageTask:
     whose ownership passes to the Harness on submit."""
 
     def __init__(self, sw=3840, sh=2160, dw=1920, dh=1080, batch=64, images_per_step=8,
-                 host_io=False, seed=1, total_steps=0):
+                 host_io=False, seed=1, total_steps=0, imperative=False):
         self.cfg = A.ImageTaskConfigC(sw=sw, sh=sh, dw=dw, dh=dh, batch=batch,
                                       images_per_step=images_per_step, host_io=int(host_io),
-                                      seed=seed, total_steps=total_steps)
+                                      interface_kind=int(bool(imperative)), seed=seed,
+                                      total_steps=total_steps)
+        self.imperative = bool(imperative)
+        self.batch, self.dw, self.dh = batch, dw, dh
         self.vt = A.SideTaskVTableC()
         self.user = C.c_void_p()
         check(glib().fr_image_task_create(C.byref(self.cfg), C.byref(self.vt), C.byref(self.user)))
@@ -134,6 +156,18 @@ class ImageTask:
         self.bytes_per_step = images_per_step * (sw * sh * 3 + dw * dh * 3) + dw * dh * 8
         self.h2d_per_step = images_per_step * sw * sh * 3 if host_io else 0
         self.d2h_per_step = images_per_step * dw * dh * 3 if host_io else 0
+
+    def outputs(self):
+        """Copy of the task's resident output batch [batch, dh, dw, 3] (None
+        when the task holds no GPU state)."""
+        src, dst, wm, steps = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_int64()
+        check(glib().fr_image_task_buffers(self.user, C.byref(src), C.byref(dst), C.byref(wm),
+                                           C.byref(steps)))
+        if not dst.value:
+            return None
+        torch.cuda.synchronize()
+        return _dev_copy(dst.value, self.batch * self.dh * self.dw * 3, torch.uint8).view(
+            self.batch, self.dh, self.dw, 3)
 
 
 def _dev_copy(ptr: int, n: int, dtype) -> torch.Tensor:
