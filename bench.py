@@ -49,6 +49,7 @@ STAGES = 4
 MICRO_BATCHES = 4
 SHAPE = dict(layers=6, hidden=2048, tokens=8192, ffn_mult=4)        # nanoGPT-1.2B / 4 stages
 SHAPE_36B = dict(layers=9, hidden=2880, tokens=8192, ffn_mult=4)    # nanoGPT-3.6B / 4 stages
+LAYERS_6B, HIDDEN_6B = 32, 4096                                       # nanoGPT-6B (configs[4])
 FRAMES = dict(sw=3840, sh=2160, dw=1920, dh=1080)
 BATCH = 64
 IMAGES_PER_STEP = 8
@@ -292,6 +293,19 @@ def ours(args):
         mixed["dT_max"] = max(x["dT"] for x in mixed["stages"])
         mixed["fill_mean"] = statistics.fmean(x["fill"] for x in mixed["stages"])
     local_res["mixed"] = mixed
+    # configs[4] / SURVEY §8(e): with N > 1 GPUs, additionally a REAL N-stage
+    # pipeline (6B-shaped stages, rank s = stage s) whose activations and
+    # gradients travel through the peer-linked mailboxes (NVLink), one
+    # image side-task worker per GPU
+    linked = None
+    if dist and not args.no_linked:
+        from paper_2409_06941_b200 import distributed as D
+        shape = dict(layers=max(1, LAYERS_6B // ws), hidden=HIDDEN_6B, tokens=8192, ffn_mult=4)
+        linked = D.linked_harvest(
+            lambda: gpu.ImageTask(batch=BATCH, images_per_step=IMAGES_PER_STEP, **FRAMES),
+            shape, num_micro_batches=max(MICRO_BATCHES, ws), epochs=K, warmup=W, task_name="image")
+        linked["shape"] = shape
+    local_res["linked"] = linked
     csr = None
     if rank == 0 and not args.no_cpu:
         g = gpu.PageRankGraph(scale=PR["scale"], edge_factor=PR["edge_factor"], seed=PR["seed"])
@@ -391,6 +405,20 @@ def emit(args, results, ws, names, csr):
         "roofline": image_roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": results[0]["clocks"],
         "gpu_launches": launches, "workloads": workloads, "stages": results[0]["stages"],
     }
+    if results[0].get("linked"):
+        ls = [r["linked"] for r in results]
+        t_no = max(x["base"]["makespan_s"] for x in ls)
+        workloads["pipeline_linked"] = {
+            "config": f"configs[4]-style: real {ws}-stage 1F1B pipeline (m={max(MICRO_BATCHES, ws)}), "
+                      f"nanoGPT-6B-shaped stages {ls[0]['shape']}, activations/gradients through "
+                      "peer-linked mailboxes (copy engine over NVLink), image side task on every stage",
+            "value": sum(x["with"]["work_units"] for x in ls) / max(x["base"]["bubble_s"] for x in ls),
+            "unit": UNIT, "dT": (max(x["with"]["makespan_s"] for x in ls) - t_no) / t_no,
+            "fill": sum(x["with"]["used_s"] for x in ls) / sum(x["with"]["bubble_s"] for x in ls),
+            "bubble_rate": ls[0]["profile"]["bubble_rate"],
+            "stages": [{"stage": x["stage"], "dT": (x["with"]["makespan_s"] - x["base"]["makespan_s"])
+                        / x["base"]["makespan_s"], "fill": x["with"]["used_s"] / max(1e-12, x["with"]["bubble_s"])}
+                       for x in ls]}
     if results[0].get("mixed"):
         workloads["mixed"] = dict(results[0]["mixed"],
                                   config="configs[3]: PageRank + SGD + Image + PageRank on a "
@@ -432,6 +460,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-mixed", action="store_true")
+    ap.add_argument("--no-linked", action="store_true", help="skip the real N-stage pipeline (N > 1)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

@@ -230,7 +230,9 @@ typedef struct fr_harness_config {
   int64_t fp_ticks_override;  /* > 0: use instead of the measured op times */
   int64_t bp_ticks_override;
   int32_t profile_epochs;     /* dry-run epochs of the bubble profiler (0: from op times) */
-  int32_t reserved;
+  int32_t transport;          /* 0: replica (device-clock dependency waits, one GPU);
+                                 1: peer-linked pipeline (stage s on its own GPU, real
+                                 activation/gradient messages through neighbour mailboxes) */
 } fr_harness_config;
 
 /* All durations in ns ticks (tick_seconds = 1e-9). */
@@ -290,6 +292,23 @@ int fr_harness_run(fr_harness* h, int32_t epochs, int32_t with_tasks, fr_run_rep
 /* raw timelines of the last run, seconds from run start, (start, end) pairs */
 int fr_harness_timeline(const fr_harness* h, int32_t which /*0 ops,1 bubbles,2 steps*/,
                         double* start_end, int64_t cap, int64_t* n);
+/* Peer-linked pipeline (transport = 1), one harness per stage (normally one
+ * per GPU/process).  Each stage owns a mailbox (device memory: flags + one
+ * message slot per micro-batch and direction); a neighbour copies the op's
+ * output (tokens x hidden bf16) into it with the copy engine over NVLink /
+ * peer memory and raises the slot's flag; the stage's dependency wait spins
+ * on its own flag (replaces NCCL send/recv).  Link the
+ * neighbours' mailboxes (pointers valid in this process: same process, or
+ * opened with fr_ipc_open) before running; both stages must run the same
+ * epoch counts.  The bubble profiler does not dry-run at creation in this
+ * mode: run without tasks, then fr_harness_reprofile_bubbles. */
+int fr_harness_mailbox(const fr_harness* h, void** base, int64_t* bytes);
+int fr_harness_link(fr_harness* h, void* prev_mailbox /* null on stage 0 */,
+                    void* next_mailbox /* null on the last stage */);
+/* CUDA IPC for mailboxes across processes (64-byte cudaIpcMemHandle_t) */
+int fr_ipc_handle(void* dev_ptr, void* handle_out);
+int fr_ipc_open(const void* handle, void** dev_ptr);
+int fr_ipc_close(void* dev_ptr);
 /* this GPU's kernel launch count in the last run (side-task steps + stand-in) */
 int fr_harness_launches(const fr_harness* h, int64_t* side_steps, int64_t* training_ops);
 

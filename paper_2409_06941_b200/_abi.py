@@ -521,7 +521,7 @@ class HarnessConfigC(Struct):
         ("max_inflight_steps", i32), ("gate_estimate", i32),
         ("gpu_memory_total", dbl), ("weight_mem", dbl), ("activation_mem", dbl),
         ("fp_ticks_override", i64), ("bp_ticks_override", i64),
-        ("profile_epochs", i32), ("reserved", i32),
+        ("profile_epochs", i32), ("transport", i32),
     ]
 
 
@@ -558,4 +558,9 @@ GPU_PROTOTYPES.update({
     "fr_harness_reprofile_bubbles": (C.c_int, [vp]),
     "fr_harness_timeline": (C.c_int, [vp, i32, P(dbl), i64, P(i64)]),
     "fr_harness_launches": (C.c_int, [vp, P(i64), P(i64)]),
+    "fr_harness_mailbox": (C.c_int, [vp, P(vp), P(i64)]),
+    "fr_harness_link": (C.c_int, [vp, vp, vp]),
+    "fr_ipc_handle": (C.c_int, [vp, vp]),
+    "fr_ipc_open": (C.c_int, [vp, P(vp)]),
+    "fr_ipc_close": (C.c_int, [vp]),
 })

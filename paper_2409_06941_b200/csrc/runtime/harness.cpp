@@ -47,6 +47,14 @@
 using namespace freeride;
 using namespace freeride::rt;
 
+#define FR_CUDA_TRY_H(expr)                                                                  \
+  do {                                                                                       \
+    const cudaError_t fr_e_ = (expr);                                                        \
+    if (fr_e_ != cudaSuccess)                                                                \
+      return frcapi::fail(FR_ERR_CUDA_BASE + static_cast<int>(fr_e_),                        \
+                          std::string(#expr) + ": " + cudaGetErrorString(fr_e_));            \
+  } while (0)
+
 namespace {
 
 void ck(cudaError_t e, const char* what) {
@@ -95,6 +103,27 @@ struct StepRec {
   Task* task;
 };
 
+// Peer-linked pipeline mailbox (transport 1): one device allocation per
+// stage, written by its neighbours.  Flags (uint32, the global epoch + 1 of
+// the message) for dir 0 = FP input from stage s-1, dir 1 = BP input from
+// stage s+1, dir 2 = epoch-end token from stage s-1, one per micro-batch;
+// then the message slots of dirs 0 and 1.
+constexpr std::size_t kFlagArea = 4096;
+constexpr std::uint64_t kLinkTimeoutNs = 20'000'000'000ull;  // dependency-wait watchdog
+constexpr int kMaxMb = 256;
+
+struct Mailbox {
+  char* base = nullptr;
+  std::size_t msg_stride = 0;
+  int m = 0;
+  std::uint32_t* flag(int dir, int mb0) const {
+    return reinterpret_cast<std::uint32_t*>(base) + dir * kMaxMb + mb0;
+  }
+  void* slot(int dir, int mb0) const {
+    return base + kFlagArea + (static_cast<std::size_t>(dir) * m + mb0) * msg_stride;
+  }
+};
+
 }  // namespace
 
 struct fr_harness {
@@ -109,6 +138,11 @@ struct fr_harness {
   std::uint32_t* flag = nullptr;   // mapped
   std::uint64_t* stamp_dev = nullptr;
   std::uint32_t* flag_dev = nullptr;
+  // transport 1 (peer-linked pipeline)
+  Mailbox mbox, prev_mbox, next_mbox;
+  std::size_t mbox_bytes = 0, msg_bytes = 0;
+  bool linked = false;
+  std::uint32_t epoch_base = 0;    // global epochs run so far (message sequence numbers)
   std::int64_t clock_off = 0;      // device_ns = host_ns + clock_off
   double clock_err = 0;
   std::int64_t launch_lat = 5000;  // host launch -> device start, ns
@@ -150,6 +184,7 @@ struct fr_harness {
     if (stamp) cudaFreeHost(stamp);
     if (flag) cudaFreeHost(flag);
     if (ctl) cudaFree(ctl);
+    if (mbox.base) cudaFree(mbox.base);
     if (train) cudaStreamDestroy(train);
     if (side) cudaStreamDestroy(side);
   }
@@ -325,11 +360,16 @@ double elapsed_s(cudaEvent_t a, cudaEvent_t b) {
 }  // namespace
 
 void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
+  if (cfg.transport == 1 && !linked)
+    throw std::runtime_error("peer-linked harness: call fr_harness_link before running");
   pool_used = 0;
   std::memset(ring, 0, sizeof(RingSlot) * kRingSlots);
-  ck(cudaMemset(&ctl->end_seq, 0, sizeof(ctl->end_seq)), "end_seq reset");
+  ck(cudaMemset(&ctl->end_seq, 0, 2 * sizeof(std::uint32_t)), "end_seq / link_timeouts reset");
   calibrate();
-  ck(cudaDeviceSynchronize(), "pre-run sync");
+  // this harness's streams only: a device-wide sync would wait on a linked
+  // neighbour's dependency spin in the same process (deadlock)
+  ck(cudaStreamSynchronize(train), "pre-run sync");
+  ck(cudaStreamSynchronize(side), "pre-run sync");
   const int nops = static_cast<int>(ops.size());
   const int ngaps = nops + 1;
 
@@ -364,6 +404,62 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
       ck(cudaSetDevice(device), "cudaSetDevice");
       ck(cudaEventRecord(run_start, train), "record");
       std::int64_t slot = 0;
+      if (cfg.transport == 1) {
+        // Peer-linked 1F1B: wait on this stage's mailbox flag for the op's
+        // cross-stage input, run the op, copy its output into the
+        // neighbour's mailbox slot (copy engine over NVLink / peer memory,
+        // no SMs) and raise the neighbour's flag.  The epoch-end token runs
+        // down the chain from stage 0 (the last stage to finish an epoch).
+        const int p = cfg.num_stages, st = cfg.stage;
+        for (int e = 0; e < epochs; ++e) {
+          const std::uint32_t seq = epoch_base + static_cast<std::uint32_t>(e) + 1;
+          for (int g = 0; g < ngaps; ++g) {
+            LinkWaitArgs a{};
+            a.ctl = ctl;
+            a.ring = ring_dev;
+            a.ring_mask = kRingSlots - 1;
+            a.slot_start = a.slot_end = -1;
+            a.seq = seq;
+            a.mode = (e == 0 && g == 0) ? 2 : 0;
+            a.timeout_ns = kLinkTimeoutNs;
+            const int b = gap_bubble[static_cast<std::size_t>(g)];
+            if (b >= 0) {
+              const std::uint32_t id = static_cast<std::uint32_t>(e) * kBubbleIds + static_cast<std::uint32_t>(b);
+              a.slot_start = slot++;
+              a.slot_end = slot++;
+              a.code_start = ring_code(kEvBubbleStart, id);
+              a.code_end = ring_code(kEvBubbleEnd, id);
+              a.end_token = id + 1;
+            }
+            if (g < nops) {
+              const OpEvent& op = ops[static_cast<std::size_t>(g)];
+              const int mb0 = op.micro_batch - 1;
+              if (op.kind == OpKind::FP && st > 0) a.flag = mbox.flag(0, mb0);
+              if (op.kind == OpKind::BP && st < p - 1) a.flag = mbox.flag(1, mb0);
+              if (a.flag || b >= 0) launch_link_wait(a, train);
+              ck(cudaEventRecord(eev[e].op_start[g], train), "record");
+              op.kind == OpKind::FP ? standin->launch_fp(train) : standin->launch_bp(train);
+              ck(cudaEventRecord(eev[e].op_end[g], train), "record");
+              const Mailbox* to = nullptr;
+              int dir = 0;
+              if (op.kind == OpKind::FP && st < p - 1) to = &next_mbox, dir = 0;
+              if (op.kind == OpKind::BP && st > 0) to = &prev_mbox, dir = 1;
+              if (to) {
+                ck(cudaMemcpyAsync(to->slot(dir, mb0), standin->output(), msg_bytes,
+                                   cudaMemcpyDefault, train), "send");
+                launch_link_signal(to->flag(dir, mb0), seq, train);
+              }
+            } else {
+              if (st > 0) a.flag = mbox.flag(2, 0);
+              if (a.flag || b >= 0) launch_link_wait(a, train);
+              if (st < p - 1) launch_link_signal(next_mbox.flag(2, 0), seq, train);
+              ck(cudaEventRecord(eev[e].end, train), "record");
+            }
+          }
+        }
+        ck(cudaGetLastError(), "training enqueue");
+        return;
+      }
       for (int e = 0; e < epochs; ++e) {
         for (int g = 0; g < ngaps; ++g) {
           GapArgs a{};
@@ -625,6 +721,13 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
   ck(cudaStreamSynchronize(side), "side sync");
   drain_completions();
   finish_init();
+  if (cfg.transport == 1) {
+    std::uint32_t timeouts = 0;
+    ck(cudaMemcpy(&timeouts, &ctl->link_timeouts, sizeof(timeouts), cudaMemcpyDeviceToHost), "timeouts");
+    if (timeouts)
+      throw std::runtime_error("peer-linked pipeline: " + std::to_string(timeouts) +
+                               " dependency waits timed out (a neighbour stage never signalled)");
+  }
   for (auto& [t, before] : work_before) {
     double u = before;
     hook(t->vt.work_done(t->user, side, &u), "work_done");
@@ -713,6 +816,7 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
   rep->kills = kills;
   last_side_steps = launched;
   last_train_ops = static_cast<std::int64_t>(epochs) * nops;
+  epoch_base += static_cast<std::uint32_t>(epochs);
 }
 
 extern "C" {
@@ -721,8 +825,11 @@ int fr_harness_create(const fr_harness_config* cfg, fr_harness** out) {
   if (!cfg || !out) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
   if (cfg->stage < 0 || cfg->stage >= cfg->num_stages)
     return frcapi::fail(FR_ERR_VALIDATION, "stage must be in [0, num_stages)", "stage");
-  if (cfg->num_micro_batches < 1 || 2 * cfg->num_micro_batches + 1 >= static_cast<int>(kBubbleIds))
+  if (cfg->num_micro_batches < 1 || 2 * cfg->num_micro_batches + 1 >= static_cast<int>(kBubbleIds) ||
+      cfg->num_micro_batches > kMaxMb)
     return frcapi::fail(FR_ERR_VALIDATION, "num_micro_batches out of range", "num_micro_batches");
+  if (cfg->transport != 0 && cfg->transport != 1)
+    return frcapi::fail(FR_ERR_VALIDATION, "transport must be 0 (replica) or 1 (peer-linked)", "transport");
   auto h = std::make_unique<fr_harness>();
   return frcapi::guard([&]() -> int {
     h->cfg = *cfg;
@@ -755,7 +862,19 @@ int fr_harness_create(const fr_harness_config* cfg, fr_harness** out) {
     h->fp_tflops = h->standin->fp_flops() / (static_cast<double>(h->measure_op(true, 3)) * kTick) * 1e-12;
     h->bp_tflops = h->standin->bp_flops() / (static_cast<double>(h->measure_op(false, 3)) * kTick) * 1e-12;
     h->build_schedule_from(f, b);
-    h->profile_in_pipeline(cfg->profile_epochs);
+    if (cfg->transport == 1) {
+      // mailbox: flags, then FP-in and BP-in slots per micro-batch
+      h->msg_bytes = h->standin->message_bytes();
+      h->mbox.m = cfg->num_micro_batches;
+      h->mbox.msg_stride = (h->msg_bytes + 255) & ~static_cast<std::size_t>(255);
+      h->mbox_bytes = kFlagArea + 2 * static_cast<std::size_t>(h->mbox.m) * h->mbox.msg_stride;
+      ck(cudaMalloc(&h->mbox.base, h->mbox_bytes), "mailbox");
+      ck(cudaMemset(h->mbox.base, 0, kFlagArea), "mailbox flags");
+      h->prev_mbox = h->next_mbox = h->mbox;  // geometry; bases set by fr_harness_link
+      h->prev_mbox.base = h->next_mbox.base = nullptr;
+    } else {
+      h->profile_in_pipeline(cfg->profile_epochs);  // linked: dry-run after fr_harness_link
+    }
     h->workers.resize(1);
     h->workers[0].worker_id = 0;
     h->workers[0].gpu_mem = h->avail;
@@ -763,6 +882,48 @@ int fr_harness_create(const fr_harness_config* cfg, fr_harness** out) {
     *out = h.release();
     return FR_OK;
   });
+}
+
+int fr_harness_mailbox(const fr_harness* h, void** base, int64_t* bytes) {
+  if (!h || !base) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  if (h->cfg.transport != 1) return frcapi::fail(FR_ERR_UNSUPPORTED, "mailbox exists only with transport 1");
+  *base = h->mbox.base;
+  if (bytes) *bytes = static_cast<int64_t>(h->mbox_bytes);
+  return FR_OK;
+}
+
+int fr_harness_link(fr_harness* h, void* prev_mailbox, void* next_mailbox) {
+  if (!h) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  if (h->cfg.transport != 1) return frcapi::fail(FR_ERR_UNSUPPORTED, "link needs transport 1");
+  const int s = h->cfg.stage, p = h->cfg.num_stages;
+  if ((s > 0) != (prev_mailbox != nullptr) || (s < p - 1) != (next_mailbox != nullptr))
+    return frcapi::fail(FR_ERR_VALIDATION, "a stage links exactly its existing neighbours", "mailbox");
+  h->prev_mbox.base = static_cast<char*>(prev_mailbox);
+  h->next_mbox.base = static_cast<char*>(next_mailbox);
+  h->linked = true;
+  return FR_OK;
+}
+
+int fr_ipc_handle(void* dev_ptr, void* handle_out) {
+  if (!dev_ptr || !handle_out) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  cudaIpcMemHandle_t hd;
+  FR_CUDA_TRY_H(cudaIpcGetMemHandle(&hd, dev_ptr));
+  std::memcpy(handle_out, &hd, sizeof(hd));
+  return FR_OK;
+}
+
+int fr_ipc_open(const void* handle, void** dev_ptr) {
+  if (!handle || !dev_ptr) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  cudaIpcMemHandle_t hd;
+  std::memcpy(&hd, handle, sizeof(hd));
+  FR_CUDA_TRY_H(cudaIpcOpenMemHandle(dev_ptr, hd, cudaIpcMemLazyEnablePeerAccess));
+  return FR_OK;
+}
+
+int fr_ipc_close(void* dev_ptr) {
+  if (!dev_ptr) return FR_OK;
+  FR_CUDA_TRY_H(cudaIpcCloseMemHandle(dev_ptr));
+  return FR_OK;
 }
 
 int fr_harness_destroy(fr_harness* h) {

@@ -37,6 +37,12 @@ class StandIn {
   double bp_flops() const { return 2.0 * fp_flops(); }
   std::size_t weight_bytes() const;
   std::size_t activation_bytes() const;  // one micro-batch's stashed activations
+  // the activation / gradient a stage sends its neighbour per micro-batch:
+  // tokens x hidden bf16, taken from the op's output buffer
+  std::size_t message_bytes() const {
+    return static_cast<std::size_t>(shape_.tokens) * shape_.hidden * 2;
+  }
+  const void* output() const { return out_; }
 
  private:
   struct Gemm {

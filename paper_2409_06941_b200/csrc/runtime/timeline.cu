@@ -51,6 +51,40 @@ __global__ void gap_kernel(GapArgs a) {
   if (a.slot_end >= 0) publish(a.ring, a.ring_mask, a.slot_end, a.code_end, t);
 }
 
+__device__ __forceinline__ std::uint32_t ld_acquire_sys(const std::uint32_t* p) {
+  std::uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Single-thread kernel: BubbleStarted (the previous op on this stream is
+// done), spin until the neighbour's flag reaches seq, BubbleEnded.
+__global__ void link_wait_kernel(LinkWaitArgs a) {
+  const std::uint64_t now = frk::globaltimer_ns();
+  if (a.mode == 2) a.ctl->base_ns = now;
+  if (a.slot_start >= 0) publish(a.ring, a.ring_mask, a.slot_start, a.code_start, now);
+  if (a.flag) {
+    // a watchdog, not a protocol step: a neighbour that never signals (a
+    // dead process) must not wedge this GPU; the host reports the count
+    while (ld_acquire_sys(a.flag) < a.seq) {
+      __nanosleep(256);
+      if (frk::globaltimer_ns() - now > a.timeout_ns) {
+        atomicAdd(&a.ctl->link_timeouts, 1u);
+        break;
+      }
+    }
+  }
+  const std::uint64_t t = frk::globaltimer_ns();
+  a.ctl->last_ns = t;
+  if (a.end_token) frk::st_relaxed_gpu(&a.ctl->end_seq, a.end_token);
+  if (a.slot_end >= 0) publish(a.ring, a.ring_mask, a.slot_end, a.code_end, t);
+}
+
+__global__ void link_signal_kernel(std::uint32_t* flag, std::uint32_t v) {
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(v) : "memory");
+}
+
 __global__ void stamp_kernel(std::uint64_t* out, volatile std::uint32_t* flag, std::uint32_t val) {
   *reinterpret_cast<volatile std::uint64_t*>(out) = frk::globaltimer_ns();
   __threadfence_system();
@@ -80,10 +114,20 @@ void configure_timeline_kernels() {
                        cudaSharedmemCarveoutMaxShared);
   cudaFuncSetAttribute(stamp_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                        cudaSharedmemCarveoutMaxShared);
+  cudaFuncSetAttribute(link_wait_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       cudaSharedmemCarveoutMaxShared);
+  cudaFuncSetAttribute(link_signal_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       cudaSharedmemCarveoutMaxShared);
   done = true;
 }
 
 void launch_gap(const GapArgs& a, cudaStream_t s) { gap_kernel<<<1, 1, 0, s>>>(a); }
+
+void launch_link_wait(const LinkWaitArgs& a, cudaStream_t s) { link_wait_kernel<<<1, 1, 0, s>>>(a); }
+
+void launch_link_signal(std::uint32_t* flag, std::uint32_t v, cudaStream_t s) {
+  link_signal_kernel<<<1, 1, 0, s>>>(flag, v);
+}
 
 void launch_stamp(std::uint64_t* out, volatile std::uint32_t* flag, std::uint32_t val,
                   cudaStream_t s) {

@@ -30,7 +30,8 @@ struct TimelineCtl {
   std::uint64_t base_ns;   // start of the current epoch (device clock)
   std::uint64_t last_ns;
   std::uint32_t end_seq;   // token of the last bubble that ended (imperative preemption)
-  std::uint32_t pad[3];
+  std::uint32_t link_timeouts;  // linked waits that gave up (neighbour never signalled)
+  std::uint32_t pad[2];
 };
 
 struct GapArgs {
@@ -46,6 +47,29 @@ struct GapArgs {
   std::int32_t mode;         // 0: before an op, 1: epoch end, 2: first epoch begin
   std::uint32_t end_token;   // > 0: raise ctl->end_seq to this at the bubble end
 };
+
+// Peer-linked pipeline (transport 1): the wait for a cross-stage dependency
+// is a spin on this stage's own mailbox flag, which the neighbouring stage
+// raises (over NVLink / peer memory) after its copy of the activation or
+// gradient into this stage's mailbox slot has completed.
+struct LinkWaitArgs {
+  TimelineCtl* ctl;
+  RingSlot* ring;
+  std::uint32_t ring_mask;
+  std::int64_t slot_start;     // -1: no event
+  std::int64_t slot_end;
+  std::uint32_t code_start;
+  std::uint32_t code_end;
+  const std::uint32_t* flag;   // null: nothing to wait for
+  std::uint32_t seq;           // wait until *flag >= seq
+  std::uint32_t end_token;
+  std::int32_t mode;           // 2: first gap of the run (sets the epoch base)
+  std::uint64_t timeout_ns;    // give up (and count it) after this long
+};
+
+void launch_link_wait(const LinkWaitArgs& a, cudaStream_t s);
+// *flag = v (release, system scope) once the preceding stream work is done
+void launch_link_signal(std::uint32_t* flag, std::uint32_t v, cudaStream_t s);
 
 void configure_timeline_kernels();
 void launch_gap(const GapArgs& a, cudaStream_t s);

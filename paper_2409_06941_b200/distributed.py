@@ -78,3 +78,48 @@ def run_p2p_plan(api: BubbleSim, m: int, compute: Callable[[OpKind, int, Optiona
             done.append((kind, mb))
     assert not outputs, "every produced tensor must have been sent"
     return done
+
+
+def link_pipeline(h, group=None) -> List[int]:
+    """Peer-linked pipeline (transport="linked"): rank s is stage s.  Every
+    rank publishes its mailbox's CUDA IPC handle (all-gather over the process
+    group), opens its neighbours' mailboxes (NVLink peer mappings across GPUs,
+    plain device memory on a shared GPU) and links them.  Returns the opened
+    peer pointers (close them with gpu.ipc_close after the last run)."""
+    from . import gpu
+    rank, p = dist.get_rank(group), dist.get_world_size(group)
+    handles = [None] * p
+    dist.all_gather_object(handles, gpu.ipc_handle(h.mailbox()), group=group)
+    prev = gpu.ipc_open(handles[rank - 1]) if rank > 0 else None
+    nxt = gpu.ipc_open(handles[rank + 1]) if rank < p - 1 else None
+    h.link(prev, nxt)
+    return [x for x in (prev, nxt) if x]
+
+
+def linked_harvest(make_task, stage_shape: dict, num_micro_batches: int, epochs: int,
+                   warmup: int, group=None, task_name: str = "side") -> dict:
+    """One stage of a real p-stage pipeline (p = world size) with a side task
+    harvesting its bubbles: link, dry-run + bubble profiler, submit (Alg. 1
+    on this stage's worker), warm-up, ΔT baseline, harvest.  Every rank must
+    call it (the epochs run in lockstep through the mailboxes)."""
+    from . import gpu
+    rank, p = dist.get_rank(group), dist.get_world_size(group)
+    h = gpu.Harness(num_stages=p, num_micro_batches=num_micro_batches, stage=rank,
+                    transport="linked", **stage_shape)
+    opened = link_pipeline(h, group)
+    dist.barrier(group)
+    h.run(2, False)
+    h.reprofile_bubbles()
+    task = make_task()
+    ok, _ = h.submit(task_name, task, profile_steps=16)
+    if not ok:
+        raise RuntimeError(f"stage {rank}: side task rejected by Alg. 1")
+    h.run(max(1, warmup), True)
+    base = h.run(epochs, False)
+    r = h.run(epochs, True)
+    prof = h.profile()
+    dist.barrier(group)
+    h.close()
+    for x in opened:
+        gpu.ipc_close(x)
+    return {"stage": rank, "base": base, "with": r, "profile": prof}

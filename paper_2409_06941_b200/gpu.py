@@ -390,14 +390,18 @@ class Harness:
     def __init__(self, num_stages=4, num_micro_batches=4, stage=0, layers=6, hidden=2048,
                  tokens=8192, ffn_mult=4, profile_reps=5, max_inflight_steps=2, gate_estimate=0,
                  gpu_memory_total=178.0, weight_mem=-1.0, activation_mem=-1.0,
-                 fp_ticks=0, bp_ticks=0, profile_epochs=3):
+                 fp_ticks=0, bp_ticks=0, profile_epochs=3, transport="replica"):
+        """transport="replica": this GPU replays stage `stage` against the
+        device clock (one GPU); "linked": a real pipeline stage whose
+        neighbours are linked through mailboxes (see link())."""
+        tp = {"replica": 0, "linked": 1}[transport]
         self.cfg = A.HarnessConfigC(
             num_stages=num_stages, num_micro_batches=num_micro_batches, stage=stage, layers=layers,
             hidden=hidden, tokens=tokens, ffn_mult=ffn_mult, profile_reps=profile_reps,
             max_inflight_steps=max_inflight_steps, gate_estimate=gate_estimate,
             gpu_memory_total=gpu_memory_total, weight_mem=weight_mem,
             activation_mem=activation_mem, fp_ticks_override=fp_ticks, bp_ticks_override=bp_ticks,
-            profile_epochs=profile_epochs)
+            profile_epochs=profile_epochs if tp == 0 else 0, transport=tp)
         h = C.c_void_p()
         check(glib().fr_harness_create(C.byref(self.cfg), C.byref(h)))
         self._h = h
@@ -407,6 +411,18 @@ class Harness:
         p = A.HarnessProfileC()
         check(glib().fr_harness_get_profile(self._h, C.byref(p)))
         return p.as_dict()
+
+    def mailbox(self) -> int:
+        """Device pointer of this stage's mailbox (transport="linked")."""
+        p, n = C.c_void_p(), C.c_int64()
+        check(glib().fr_harness_mailbox(self._h, C.byref(p), C.byref(n)))
+        self.mailbox_bytes = n.value
+        return p.value
+
+    def link(self, prev_mailbox=None, next_mailbox=None):
+        """Neighbours' mailbox pointers valid in this process (same process,
+        or opened with ipc_open); None at the pipeline's ends."""
+        check(glib().fr_harness_link(self._h, prev_mailbox, next_mailbox))
 
     def stage_bubbles(self):
         out = (A.BubbleC * 1024)()
@@ -465,6 +481,23 @@ class Harness:
             self.close()
         except Exception:  # noqa: BLE001
             pass
+
+
+def ipc_handle(dev_ptr: int) -> bytes:
+    """64-byte CUDA IPC handle of a device allocation (e.g. a mailbox)."""
+    buf = C.create_string_buffer(64)
+    check(glib().fr_ipc_handle(dev_ptr, buf))
+    return buf.raw
+
+
+def ipc_open(handle: bytes) -> int:
+    p = C.c_void_p()
+    check(glib().fr_ipc_open(C.create_string_buffer(handle, 64), C.byref(p)))
+    return p.value
+
+
+def ipc_close(dev_ptr: int):
+    check(glib().fr_ipc_close(dev_ptr))
 
 
 def img_generate_watermark(w, h, seed=7, device="cuda", stream=None):
