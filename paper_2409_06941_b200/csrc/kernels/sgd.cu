@@ -27,6 +27,7 @@ namespace {
 
 constexpr int kSgdThreads = 256;
 constexpr int kSgdDefaultMinBlocks = 1;
+constexpr int kSgdDefaultEpi = 2;  // edges per lane group per iteration
 constexpr uint64_t kSgdPermMul = 2654435761ull;
 
 __device__ __forceinline__ int32_t sgd_vertex(uint64_t h, int32_t V) {
@@ -91,9 +92,11 @@ __device__ __forceinline__ void deltas(const float4& a, const float4& b, float e
 // every update lands; concurrent ones act like a small mini-batch on the hub.
 __device__ __forceinline__ void apply(float4* p, const float4& d) { atomicAdd(p, d); }
 
-// Each lane group handles edges g, g + G, g + 2G, ... two at a time.
+// Each lane group handles edges g, g + G, g + 2G, ..., EPI of them per
+// iteration (EPI x 2 latent-row loads in flight per lane), and the next
+// iteration's (u, v, r) load while this iteration's rows are in flight.
 // MINB: CTAs per SM the register allocation must allow (occupancy vs ILP).
-template <int K, int MINB>
+template <int K, int MINB, int EPI>
 __global__ void __launch_bounds__(kSgdThreads, MINB) sgd_step_kernel(
     const int32_t* __restrict__ us, const int32_t* __restrict__ vs, const float* __restrict__ rs,
     float* __restrict__ L, int64_t e0, int64_t e1, float eta, float lam) {
@@ -105,45 +108,47 @@ __global__ void __launch_bounds__(kSgdThreads, MINB) sgd_step_kernel(
   // Warp-uniform trip count (the group shuffles need every lane present);
   // lanes whose edge is past the end ride along predicated off.
   const int64_t warp_first = group - lane / LN;
-  // Software-pipelined: the next pair's (u, v, r) load while this pair's
-  // latent rows are in flight.
-  int64_t ew = e0 + warp_first;
-  int32_t u0 = 0, v0 = 0, u1 = 0, v1 = 0;
-  float r0 = 0.0f, r1 = 0.0f;
-  auto fetch = [&](int64_t base, int32_t& a0, int32_t& b0, float& q0, int32_t& a1, int32_t& b1,
-                   float& q1) {
-    const int64_t e = base + lane / LN, f = e + G;
-    const bool one = e < e1, two = f < e1;
-    a0 = one ? __ldg(&us[e]) : 0;
-    b0 = one ? __ldg(&vs[e]) : 0;
-    q0 = one ? __ldg(&rs[e]) : 0.0f;
-    a1 = two ? __ldg(&us[f]) : a0;
-    b1 = two ? __ldg(&vs[f]) : b0;
-    q1 = two ? __ldg(&rs[f]) : 0.0f;
+  auto fetch = [&](int64_t base, int32_t* a, int32_t* b, float* q) {
+#pragma unroll
+    for (int j = 0; j < EPI; ++j) {
+      const int64_t e = base + lane / LN + j * G;
+      const bool ok = e < e1;
+      a[j] = ok ? __ldg(&us[e]) : (j ? a[0] : 0);
+      b[j] = ok ? __ldg(&vs[e]) : (j ? b[0] : 0);
+      q[j] = ok ? __ldg(&rs[e]) : 0.0f;
+    }
   };
-  if (ew < e1) fetch(ew, u0, v0, r0, u1, v1, r1);
-  for (; ew < e1; ew += 2 * G) {
-    const int64_t e = ew + lane / LN, f = e + G;
-    const bool one = e < e1, two = f < e1;
-    const float4 a0 = L4[static_cast<int64_t>(u0) * LN + sub], b0 = L4[static_cast<int64_t>(v0) * LN + sub];
-    const float4 a1 = L4[static_cast<int64_t>(u1) * LN + sub], b1 = L4[static_cast<int64_t>(v1) * LN + sub];
-    int32_t nu0 = 0, nv0 = 0, nu1 = 0, nv1 = 0;
-    float nr0 = 0.0f, nr1 = 0.0f;
-    if (ew + 2 * G < e1) fetch(ew + 2 * G, nu0, nv0, nr0, nu1, nv1, nr1);
-    const float err0 = r0 - group_sum<K>(dot4(a0, b0));
-    const float err1 = r1 - group_sum<K>(dot4(a1, b1));
-    float4 da, db;
-    if (one) {
-      deltas(a0, b0, err0, eta, lam, da, db);
-      apply(&L4[static_cast<int64_t>(u0) * LN + sub], da);
-      apply(&L4[static_cast<int64_t>(v0) * LN + sub], db);
+  int32_t u[EPI], v[EPI];
+  float r[EPI];
+  int64_t ew = e0 + warp_first;
+  if (ew < e1) fetch(ew, u, v, r);
+  for (; ew < e1; ew += EPI * G) {
+    float4 a[EPI], b[EPI];
+#pragma unroll
+    for (int j = 0; j < EPI; ++j) {
+      a[j] = L4[static_cast<int64_t>(u[j]) * LN + sub];
+      b[j] = L4[static_cast<int64_t>(v[j]) * LN + sub];
     }
-    if (two) {
-      deltas(a1, b1, err1, eta, lam, da, db);
-      apply(&L4[static_cast<int64_t>(u1) * LN + sub], da);
-      apply(&L4[static_cast<int64_t>(v1) * LN + sub], db);
+    int32_t nu[EPI], nv[EPI];
+    float nr[EPI];
+    if (ew + EPI * G < e1) {
+      fetch(ew + EPI * G, nu, nv, nr);
+    } else {
+#pragma unroll
+      for (int j = 0; j < EPI; ++j) nu[j] = nv[j] = 0, nr[j] = 0.0f;
     }
-    u0 = nu0; v0 = nv0; r0 = nr0; u1 = nu1; v1 = nv1; r1 = nr1;
+#pragma unroll
+    for (int j = 0; j < EPI; ++j) {
+      const float err = r[j] - group_sum<K>(dot4(a[j], b[j]));
+      if (ew + lane / LN + j * G < e1) {
+        float4 da, db;
+        deltas(a[j], b[j], err, eta, lam, da, db);
+        apply(&L4[static_cast<int64_t>(u[j]) * LN + sub], da);
+        apply(&L4[static_cast<int64_t>(v[j]) * LN + sub], db);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < EPI; ++j) u[j] = nu[j], v[j] = nv[j], r[j] = nr[j];
   }
 }
 
@@ -206,20 +211,38 @@ struct fr_sgd_problem {
 
 namespace {
 
+template <int K, int MINB, int EPI>
+void launch_step_v(fr_sgd_problem* p, int64_t a, int64_t b, float eta, float lam, cudaStream_t s) {
+  // persistent-style grid: exactly the resident CTAs (no second partial wave)
+  static const int per_sm = [] {
+    int n = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sgd_step_kernel<K, MINB, EPI>, kSgdThreads, 0);
+    return std::max(1, n);
+  }();
+  const int64_t groups = (b - a + EPI - 1) / EPI;
+  const int grid = static_cast<int>(std::max<int64_t>(
+      1, std::min<int64_t>((groups * Row<K>::kLanes + kSgdThreads - 1) / kSgdThreads,
+                           int64_t(p->sms) * per_sm)));
+  sgd_step_kernel<K, MINB, EPI><<<grid, kSgdThreads, 0, s>>>(p->u, p->v, p->r, p->L, a, b, eta, lam);
+}
+
 template <int K>
 void launch_step(fr_sgd_problem* p, int64_t a, int64_t b, float eta, float lam, cudaStream_t s) {
-  const int64_t groups = (b - a + 1) / 2;
-  const int grid = grid_for(groups * Row<K>::kLanes, kSgdThreads, 8);
   static const int minb = [] {
-    const char* e = std::getenv("FR_SGD_MINB");  // tuning hook
+    const char* e = std::getenv("FR_SGD_MINB");  // tuning hooks
     return e ? std::atoi(e) : kSgdDefaultMinBlocks;
   }();
-  if (minb >= 8)
-    sgd_step_kernel<K, 8><<<grid, kSgdThreads, 0, s>>>(p->u, p->v, p->r, p->L, a, b, eta, lam);
-  else if (minb >= 6)
-    sgd_step_kernel<K, 6><<<grid, kSgdThreads, 0, s>>>(p->u, p->v, p->r, p->L, a, b, eta, lam);
-  else
-    sgd_step_kernel<K, 1><<<grid, kSgdThreads, 0, s>>>(p->u, p->v, p->r, p->L, a, b, eta, lam);
+  static const int epi = [] {
+    const char* e = std::getenv("FR_SGD_EPI");
+    return e ? std::atoi(e) : kSgdDefaultEpi;
+  }();
+  if (epi >= 4) {
+    if (minb >= 4) launch_step_v<K, 4, 4>(p, a, b, eta, lam, s);
+    else launch_step_v<K, 1, 4>(p, a, b, eta, lam, s);
+  } else {
+    if (minb >= 6) launch_step_v<K, 6, 2>(p, a, b, eta, lam, s);
+    else launch_step_v<K, 1, 2>(p, a, b, eta, lam, s);
+  }
 }
 
 template <int K>
