@@ -155,6 +155,12 @@ typedef struct fr_side_task_vtable {
   int32_t reserved;
   int (*run_gpu_workload)(void* user, void* stream, const fr_preempt* preempt);
   int (*work_done)(void* user, void* stream, double* units);
+  /* Framework-enforced kill (limits.hpp:34 framework_enforce, check_memory
+   * :20): optional.  Called from the worker thread when the task is killed;
+   * must make its in-flight GPU work end promptly (e.g. raise a word its
+   * kernels poll) without synchronising.  The worker then drains the task's
+   * stream, calls stop and releases the task's memory pool. */
+  int (*cancel)(void* user);
 } fr_side_task_vtable;
 
 /* Built-in side tasks (kernels above) behind the vtable. */
@@ -175,6 +181,26 @@ int fr_image_task_memory(const fr_image_task_config* cfg, double* gib);
 /* device pointers of the last processed batch slot (for checking) */
 int fr_image_task_buffers(void* user, const uint8_t** src, uint8_t** dst, const uint8_t** wm,
                           int64_t* steps_done);
+
+/* Synthetic side task: the reference's SideTaskSpec (task.hpp:33-50) made
+ * real -- each RunNextStep is a spin kernel occupying every SM for step_ns,
+ * InitSideTask allocates memory_demand_gib, and the Fig. 9 misbehaviours
+ * (task.hpp:26-31) are reproducible: MemoryLeak allocates leak_gib_per_step
+ * more each step; a task whose steps run far longer than profiled
+ * (step_ns >> profile_step_ns) overruns its bubbles like IgnoresPause.
+ * cooperative = 1: the step kernel polls the task's cancel word, so a kill
+ * ends it within ~1 us. */
+typedef struct fr_synthetic_task_config {
+  int64_t step_ns;
+  int64_t profile_step_ns;      /* step length while being profiled (<= 0: step_ns) */
+  double memory_demand_gib;
+  double leak_gib_per_step;
+  int64_t total_steps;          /* <= 0: unbounded */
+  int32_t cooperative;
+  int32_t reserved;
+} fr_synthetic_task_config;
+int fr_synthetic_task_create(const fr_synthetic_task_config* cfg, fr_side_task_vtable* vt,
+                             void** user);
 
 typedef struct fr_pagerank_task_config {
   int32_t scale;          /* RMAT scale: V = 2^scale */
@@ -233,6 +259,12 @@ typedef struct fr_harness_config {
   int32_t transport;          /* 0: replica (device-clock dependency waits, one GPU);
                                  1: peer-linked pipeline (stage s on its own GPU, real
                                  activation/gradient messages through neighbour mailboxes) */
+  /* limits (limits.hpp:9-15): every task allocates from its own CUDA memory
+   * pool; limit = profiled est_memory + headroom, checked (check_memory,
+   * strict) after InitSideTask and every RunNextStep -> OOM kill; a pause not
+   * observed within grace_ns -> pause-timeout kill (framework_enforce). */
+  double memory_headroom_gib;
+  int64_t grace_ns;           /* <= 0: 100 ms (LimitConfig::grace_period = 100 ticks of 1 ms) */
 } fr_harness_config;
 
 /* All durations in ns ticks (tick_seconds = 1e-9). */
@@ -264,7 +296,9 @@ typedef struct fr_run_report {
   double max_step_overrun_s;    /* worst step tail past its bubble end */
   fr_stage_breakdown breakdown; /* bubble_breakdown (metrics.hpp:64), ns ticks */
   int64_t pauses;
-  int64_t kills;                /* framework_enforce verdicts (limits.hpp:34) */
+  int64_t kills;                /* tasks killed in this run (both reasons) */
+  int64_t kills_oom;            /* check_memory OomKill (limits.hpp:20) */
+  int64_t kills_pause_timeout;  /* framework_enforce Kill (limits.hpp:34) */
 } fr_run_report;
 
 int fr_harness_create(const fr_harness_config* cfg, fr_harness** out);
@@ -289,6 +323,10 @@ int fr_harness_stop_task(fr_harness* h, const char* task_id);
 int fr_harness_reprofile(fr_harness* h, const char* task_id, fr_task_profile* out);
 /* Runs `epochs` epochs; with_tasks=0 is the ΔT baseline. Blocks. */
 int fr_harness_run(fr_harness* h, int32_t epochs, int32_t with_tasks, fr_run_report* out);
+/* a submitted task's state (enum fr_task_state), disposition (enum
+ * fr_disposition; FR_DISP_ACTIVE while alive) and bytes in its memory pool */
+int fr_harness_task_status(const fr_harness* h, const char* task_id, int32_t* state,
+                           int32_t* disposition, double* memory_used_gib);
 /* raw timelines of the last run, seconds from run start, (start, end) pairs */
 int fr_harness_timeline(const fr_harness* h, int32_t which /*0 ops,1 bubbles,2 steps*/,
                         double* start_end, int64_t cap, int64_t* n);

@@ -460,7 +460,14 @@ class SideTaskVTableC(Struct):
         ("reserved", i32),
         ("run_gpu_workload", C.CFUNCTYPE(C.c_int, vp, vp, vp)),
         ("work_done", C.CFUNCTYPE(C.c_int, vp, vp, P(C.c_double))),
+        ("cancel", C.CFUNCTYPE(C.c_int, vp)),
     ]
+
+
+class SyntheticTaskConfigC(Struct):
+    _fields_ = [("step_ns", i64), ("profile_step_ns", i64), ("memory_demand_gib", C.c_double),
+                ("leak_gib_per_step", C.c_double), ("total_steps", i64), ("cooperative", i32),
+                ("reserved", i32)]
 
 
 class PreemptC(Struct):
@@ -522,6 +529,7 @@ class HarnessConfigC(Struct):
         ("gpu_memory_total", dbl), ("weight_mem", dbl), ("activation_mem", dbl),
         ("fp_ticks_override", i64), ("bp_ticks_override", i64),
         ("profile_epochs", i32), ("transport", i32),
+        ("memory_headroom_gib", dbl), ("grace_ns", i64),
     ]
 
 
@@ -540,6 +548,7 @@ class RunReportC(Struct):
         ("work_units", dbl), ("steps_launched", i64), ("steps_completed", i64),
         ("dispatch_host_us", dbl), ("max_step_overrun_s", dbl),
         ("breakdown", StageBreakdownC), ("pauses", i64), ("kills", i64),
+        ("kills_oom", i64), ("kills_pause_timeout", i64),
     ]
 
 
@@ -548,6 +557,8 @@ GPU_PROTOTYPES.update({
     "fr_image_task_memory": (C.c_int, [P(ImageTaskConfigC), P(dbl)]),
     "fr_image_task_buffers": (C.c_int, [vp, P(vp), P(vp), P(vp), P(i64)]),
     "fr_harness_create": (C.c_int, [P(HarnessConfigC), P(vp)]),
+    "fr_synthetic_task_create": (C.c_int, [P(SyntheticTaskConfigC), P(SideTaskVTableC), P(vp)]),
+    "fr_harness_task_status": (C.c_int, [vp, C.c_char_p, P(i32), P(i32), P(dbl)]),
     "fr_harness_destroy": (C.c_int, [vp]),
     "fr_harness_get_profile": (C.c_int, [vp, P(HarnessProfileC)]),
     "fr_harness_stage_bubbles": (C.c_int, [vp, P(BubbleC), i32, P(i32)]),

@@ -31,6 +31,7 @@
 #include <cmath>
 #include <cstring>
 #include <deque>
+#include <functional>
 #include <map>
 #include <memory>
 #include <stdexcept>
@@ -80,6 +81,25 @@ constexpr double kTick = 1e-9;  // runtime ticks are nanoseconds
 constexpr std::uint32_t kRingSlots = 1u << 16;
 constexpr std::uint32_t kBubbleIds = 1024;  // bubble ids per epoch in a ring code
 constexpr Tick kGraceTicks = 100'000'000;  // LimitConfig::grace_period (0.1 s), ns ticks
+constexpr double kGiB = 1024.0 * 1024.0 * 1024.0;
+
+// Makes `pool` the device's current memory pool for the scope, so the
+// stream-ordered allocations a task's hooks make (cudaMallocAsync) are
+// accounted to the task.  Only the worker thread allocates while a run is in
+// flight (the training program is captured graphs + fixed buffers).
+struct PoolScope {
+  int dev;
+  cudaMemPool_t prev = nullptr;
+  bool active = false;
+  PoolScope(int d, cudaMemPool_t pool) : dev(d) {
+    if (pool && cudaDeviceGetMemPool(&prev, dev) == cudaSuccess &&
+        cudaDeviceSetMemPool(dev, pool) == cudaSuccess)
+      active = true;
+  }
+  ~PoolScope() {
+    if (active) cudaDeviceSetMemPool(dev, prev);
+  }
+};
 
 struct Task {
   std::string id;
@@ -91,10 +111,23 @@ struct Task {
   bool imperative() const { return vt.interface_kind == FR_IMPERATIVE; }
   cudaEvent_t init_a = nullptr, init_b = nullptr;
   bool init_recorded = false;
+  int device = 0;
+  cudaMemPool_t pool = nullptr;  // every allocation the task's hooks make
+  double mem_limit = 0.0;        // GiB: profiled est_memory + headroom (check_memory)
+  Disposition disp = Disposition::Active;
+  double used_gib() const {
+    std::size_t used = 0;
+    if (pool) cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+    return static_cast<double>(used) / kGiB;
+  }
   ~Task() {
     if (init_a) cudaEventDestroy(init_a);
     if (init_b) cudaEventDestroy(init_b);
-    if (vt.destroy && user) vt.destroy(user);
+    if (vt.destroy && user) {
+      PoolScope ps(device, pool);
+      vt.destroy(user);
+    }
+    if (pool) cudaMemPoolDestroy(pool);
   }
 };
 
@@ -529,10 +562,16 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
   std::uint32_t cur_token = 0;  // bubble-end token the running imperative workload stops at
   auto stop_task = [&](Task& t, Tick now) {
     apply_transition(t.rt, TransitionKind::StopSideTask, now);
-    hook(t.vt.stop ? t.vt.stop(t.user) : FR_OK, "stop");
+    {
+      PoolScope ps(device, t.pool);
+      hook(t.vt.stop ? t.vt.stop(t.user) : FR_OK, "stop");
+    }
+    t.disp = Disposition::Completed;
     if (ws.current_task && *ws.current_task == t.id) ws.current_task.reset();  // Appendix B rule 8
     if (running == &t) running = nullptr;
   };
+  std::int64_t kills_oom = 0, kills_timeout = 0;
+  std::function<void(Task&, Disposition)> kill;  // defined below (needs drain_completions)
   auto drain_completions = [&] {
     while (!inflight.empty()) {
       const cudaError_t q = cudaEventQuery(steps[inflight.front()].b);
@@ -557,6 +596,36 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
         if (done) stop_task(*running, dev_now());
       }
     }
+  };
+  // Framework-enforced kill (limits.cpp:13-26): cancel the task's in-flight
+  // work (its cancel hook), drain its stream, StopSideTask, release its pool.
+  kill = [&](Task& t, Disposition d) {
+    if (t.vt.cancel) hook(t.vt.cancel(t.user), "cancel");
+    ck(cudaStreamSynchronize(side), "kill drain");
+    drain_completions();
+    if (t.rt.state != SideTaskState::Stopped) {
+      apply_transition(t.rt, TransitionKind::StopSideTask, dev_now());
+      PoolScope ps(device, t.pool);
+      hook(t.vt.stop ? t.vt.stop(t.user) : FR_OK, "stop");
+    }
+    ck(cudaStreamSynchronize(side), "kill release");
+    if (t.pool) cudaMemPoolTrimTo(t.pool, 0);
+    t.disp = d;
+    t.initializing = false;
+    if (ws.current_task && *ws.current_task == t.id) ws.current_task.reset();  // Appendix B rule 8
+    ws.task_queue.erase(std::remove(ws.task_queue.begin(), ws.task_queue.end(), t.id), ws.task_queue.end());
+    if (running == &t) running = nullptr;
+    pause_pending = false;
+    gate_closed = false;
+    ++kills;
+    ++(d == Disposition::KilledOom ? kills_oom : kills_timeout);
+  };
+  auto oom = [&](Task& t) {  // check_memory (limits.cpp:13-15), strict exceedance
+    if (check_memory(t.used_gib(), t.mem_limit) == MemCheck::OomKill) {
+      kill(t, Disposition::KilledOom);
+      return true;
+    }
+    return false;
   };
   auto finish_pause = [&] {
     if (!pause_pending || !inflight.empty()) return;
@@ -599,10 +668,14 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
           ck(cudaEventCreate(&t.init_b), "init event");
         }
         ck(cudaEventRecord(t.init_a, side), "record");
-        hook(t.vt.init(t.user, side), "init");
+        {
+          PoolScope ps(device, t.pool);
+          hook(t.vt.init(t.user, side), "init");
+        }
         ck(cudaEventRecord(t.init_b, side), "record");
         t.initializing = true;
         t.init_recorded = true;
+        oom(t);
       } else if (act.kind == ManagerActionKind::IssueStart) {
         apply_transition(t.rt, TransitionKind::StartSideTask, t_dev);
         hook(t.vt.start ? t.vt.start(t.user) : FR_OK, "start");
@@ -671,12 +744,16 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
         fr_preempt pre{&ctl->end_seq, cur_token, 0};
         StepRec r{ev(), ev(), running};
         ck(cudaEventRecord(r.a, side), "record");
-        hook(running->vt.run_gpu_workload(running->user, side, &pre), "run_gpu_workload");
+        {
+          PoolScope ps(device, running->pool);
+          hook(running->vt.run_gpu_workload(running->user, side, &pre), "run_gpu_workload");
+        }
         ck(cudaEventRecord(r.b, side), "record");
         steps.push_back(r);
         inflight.push_back(steps.size() - 1);
         ++launched;
         dispatch_ns += static_cast<double>(host_ns() - h0);
+        if (oom(*r.task)) break;
       }
       // 3b. iterative dispatch: the program-directed gate at the projected start time
       while (running && !running->imperative() && !pause_pending && !gate_closed &&
@@ -694,7 +771,10 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
         }
         StepRec r{ev(), ev(), running};
         ck(cudaEventRecord(r.a, side), "record");
-        hook(running->vt.run_next_step(running->user, side), "run_next_step");
+        {
+          PoolScope ps(device, running->pool);
+          hook(running->vt.run_next_step(running->user, side), "run_next_step");
+        }
         ck(cudaEventRecord(r.b, side), "record");
         apply_transition(running->rt, TransitionKind::RunNextStep, start);
         steps.push_back(r);
@@ -702,15 +782,17 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
         proj_end_dev = d.step_end;
         ++launched;
         dispatch_ns += static_cast<double>(host_ns() - h0);
+        if (oom(*r.task)) break;
       }
       // framework-enforced limit: a pause not observed within the grace
-      // period gets a Kill verdict (limits.cpp:21-26); kernels cannot be
-      // revoked, so the verdict is counted and reported.
+      // period is a Kill (limits.cpp:21-26): the task's cancel hook stops its
+      // in-flight kernels (cooperative ones exit at once), then it is stopped
+      // and its memory pool released.
       if (pause_pending && !kill_judged && running &&
-          framework_enforce(running->rt.last_paused, pause_issued_dev, dev_now(), kGraceTicks) ==
-              Enforce::Kill) {
-        ++kills;
+          framework_enforce(running->rt.last_paused, pause_issued_dev, dev_now(),
+                            cfg.grace_ns > 0 ? cfg.grace_ns : kGraceTicks) == Enforce::Kill) {
         kill_judged = true;
+        kill(*running, Disposition::KilledPauseTimeout);
       }
       if (next_slot >= n_events && inflight.empty() && !pause_pending) break;
     }
@@ -814,6 +896,8 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
   rep->breakdown = fr_stage_breakdown{0, 0, bd[0].used_by_side_tasks, bd[0].runtime_overhead, bd[0].idle_oom, bd[0].idle_insufficient_time};
   rep->pauses = pauses;
   rep->kills = kills;
+  rep->kills_oom = kills_oom;
+  rep->kills_pause_timeout = kills_timeout;
   last_side_steps = launched;
   last_train_ops = static_cast<std::int64_t>(epochs) * nops;
   epoch_base += static_cast<std::uint32_t>(epochs);
@@ -974,6 +1058,15 @@ int fr_harness_submit(fr_harness* h, const char* task_id, const fr_side_task_vta
     if (imperative && (!vt->run_gpu_workload || !vt->work_done))
       throw HookError(FR_ERR_ARGUMENT, "imperative task without run_gpu_workload / work_done");
     t->rt.spec.interface_kind = imperative ? TaskInterface::Imperative : TaskInterface::Iterative;
+    t->device = h->device;
+    cudaMemPoolProps pp{};
+    pp.allocType = cudaMemAllocationTypePinned;
+    pp.location.type = cudaMemLocationTypeDevice;
+    pp.location.id = h->device;
+    ck(cudaMemPoolCreate(&t->pool, &pp), "task memory pool");
+    std::uint64_t keep = UINT64_MAX;  // cache freed memory inside the pool (no device sync on reuse)
+    cudaMemPoolSetAttribute(t->pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    PoolScope ps(h->device, t->pool);
     hook(vt->create ? vt->create(user) : FR_OK, "create");
     hook(vt->init(user, h->side), "init");
     const int n = imperative ? 0 : std::max(1, profile_steps);
@@ -995,6 +1088,14 @@ int fr_harness_submit(fr_harness* h, const char* task_id, const fr_side_task_vta
     }
     h->pool_used = 0;
     hook(vt->stop ? vt->stop(user) : FR_OK, "stop");  // profiling instance torn down
+    ck(cudaStreamSynchronize(h->side), "profile sync");
+    // GPU memory consumption (§4.3): the pool's high-water mark
+    // while the task was initialised and stepped standalone
+    std::size_t high = 0;
+    cudaMemPoolGetAttribute(t->pool, cudaMemPoolAttrUsedMemHigh, &high);
+    std::uint64_t zero = 0;
+    cudaMemPoolSetAttribute(t->pool, cudaMemPoolAttrUsedMemHigh, &zero);
+    cudaMemPoolTrimTo(t->pool, 0);
     TaskProfile p;
     p.task_id = task_id;
     p.profiled_steps = n;
@@ -1002,8 +1103,9 @@ int fr_harness_submit(fr_harness* h, const char* task_id, const fr_side_task_vta
       p.est_per_step_duration = ticks_to_seconds(busy, kTick) / n;
       p.max_per_step_duration = ticks_to_seconds(longest, kTick);
     }
-    p.est_memory = mem;
+    p.est_memory = std::max(mem, static_cast<double>(high) / kGiB);
     t->prof = p;
+    t->mem_limit = p.est_memory + std::max(0.0, h->cfg.memory_headroom_gib);
     const SubmitOutcome o = submit_task(p, h->workers);  // Alg. 1
     if (assigned) *assigned = o.assigned;
     if (prof_out) frcapi::profile_out(p, prof_out);
@@ -1013,6 +1115,7 @@ int fr_harness_submit(fr_harness* h, const char* task_id, const fr_side_task_vta
       h->tasks[task_id] = std::move(t);
     } else {
       t->user = nullptr;  // rejected: ownership stays with the caller
+      t->disp = Disposition::Rejected;
     }
     return FR_OK;
   });
@@ -1046,6 +1149,7 @@ int fr_harness_stop_task(fr_harness* h, const char* task_id) {
   return frcapi::guard([&]() -> int {
     if (t.rt.state != SideTaskState::Stopped) {
       apply_transition(t.rt, TransitionKind::StopSideTask, 0);  // {CREATED,PAUSED,RUNNING} -> STOPPED
+      PoolScope ps(h->device, t.pool);
       if (t.rt.memory_allocated == 0.0 && t.vt.stop) hook(t.vt.stop(t.user), "stop");
     }
     WorkerState& ws = h->workers[0];
@@ -1075,6 +1179,18 @@ int fr_harness_reprofile(fr_harness* h, const char* task_id, fr_task_profile* ou
   t.prof.est_per_step_duration = ticks_to_seconds(busy, kTick) / n;
   t.prof.max_per_step_duration = ticks_to_seconds(longest, kTick);
   if (out) frcapi::profile_out(t.prof, out);
+  return FR_OK;
+}
+
+int fr_harness_task_status(const fr_harness* h, const char* task_id, int32_t* state,
+                           int32_t* disposition, double* memory_used_gib) {
+  if (!h || !task_id) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  auto it = h->tasks.find(task_id);
+  if (it == h->tasks.end()) return frcapi::fail(FR_ERR_NOT_FOUND, "unknown task");
+  const Task& t = *it->second;
+  if (state) *state = static_cast<int32_t>(t.rt.state);
+  if (disposition) *disposition = static_cast<int32_t>(t.disp);
+  if (memory_used_gib) *memory_used_gib = t.used_gib();
   return FR_OK;
 }
 

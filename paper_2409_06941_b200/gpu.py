@@ -178,6 +178,27 @@ def _dev_copy(ptr: int, n: int, dtype) -> torch.Tensor:
     return out
 
 
+class SyntheticTask:
+    """The reference's synthetic SideTaskSpec made real (fr_synthetic_task_create):
+    steps are spin kernels on every SM, Init allocates memory_demand_gib,
+    leak_gib_per_step reproduces MemoryLeak, step_ns >> profile_step_ns a task
+    that overruns its bubbles (Fig. 9 scenarios)."""
+
+    def __init__(self, step_ns=200_000, profile_step_ns=0, memory_demand_gib=0.25,
+                 leak_gib_per_step=0.0, total_steps=0, cooperative=True):
+        self.cfg = A.SyntheticTaskConfigC(step_ns=step_ns, profile_step_ns=profile_step_ns,
+                                          memory_demand_gib=memory_demand_gib,
+                                          leak_gib_per_step=leak_gib_per_step,
+                                          total_steps=total_steps, cooperative=int(cooperative))
+        self.vt = A.SideTaskVTableC()
+        self.user = C.c_void_p()
+        check(glib().fr_synthetic_task_create(C.byref(self.cfg), C.byref(self.vt), C.byref(self.user)))
+        self.memory_gib = memory_demand_gib
+        self.units_per_step = 1.0
+        self.bytes_per_step = 0
+        self.h2d_per_step = self.d2h_per_step = 0
+
+
 class PageRankGraph:
     """fr_pr_graph: RMAT graph as an incoming CSR on the device."""
 
@@ -390,7 +411,8 @@ class Harness:
     def __init__(self, num_stages=4, num_micro_batches=4, stage=0, layers=6, hidden=2048,
                  tokens=8192, ffn_mult=4, profile_reps=5, max_inflight_steps=2, gate_estimate=0,
                  gpu_memory_total=178.0, weight_mem=-1.0, activation_mem=-1.0,
-                 fp_ticks=0, bp_ticks=0, profile_epochs=3, transport="replica"):
+                 fp_ticks=0, bp_ticks=0, profile_epochs=3, transport="replica",
+                 memory_headroom_gib=0.0, grace_ns=0):
         """transport="replica": this GPU replays stage `stage` against the
         device clock (one GPU); "linked": a real pipeline stage whose
         neighbours are linked through mailboxes (see link())."""
@@ -401,7 +423,8 @@ class Harness:
             max_inflight_steps=max_inflight_steps, gate_estimate=gate_estimate,
             gpu_memory_total=gpu_memory_total, weight_mem=weight_mem,
             activation_mem=activation_mem, fp_ticks_override=fp_ticks, bp_ticks_override=bp_ticks,
-            profile_epochs=profile_epochs if tp == 0 else 0, transport=tp)
+            profile_epochs=profile_epochs if tp == 0 else 0, transport=tp,
+            memory_headroom_gib=memory_headroom_gib, grace_ns=grace_ns)
         h = C.c_void_p()
         check(glib().fr_harness_create(C.byref(self.cfg), C.byref(h)))
         self._h = h
@@ -423,6 +446,17 @@ class Harness:
         """Neighbours' mailbox pointers valid in this process (same process,
         or opened with ipc_open); None at the pipeline's ends."""
         check(glib().fr_harness_link(self._h, prev_mailbox, next_mailbox))
+
+    DISPOSITIONS = ("rejected", "completed", "killed_oom", "killed_pause_timeout",
+                    "killed_init_timeout", "active")
+    STATES = ("submitted", "created", "paused", "running", "stopped")
+
+    def task_status(self, task_id: str) -> dict:
+        st, disp, gib = C.c_int32(), C.c_int32(), C.c_double()
+        check(glib().fr_harness_task_status(self._h, task_id.encode(), C.byref(st), C.byref(disp),
+                                            C.byref(gib)))
+        return {"state": self.STATES[st.value], "disposition": self.DISPOSITIONS[disp.value],
+                "memory_used_gib": gib.value}
 
     def stage_bubbles(self):
         out = (A.BubbleC * 1024)()
