@@ -457,6 +457,15 @@ int fr_run_trace_transitions(const fr_run_trace* t, int32_t which, fr_transition
 int fr_run_trace_activities(const fr_run_trace* t, fr_activity_record* out, int64_t cap);
 int fr_run_trace_kills(const fr_run_trace* t, fr_kill_record* out, int64_t cap);
 int fr_run_trace_dispositions(const fr_run_trace* t, fr_disposition_record* out, int64_t cap);
+/* replay_check (engine.hpp:100-104): re-validates the module invariants over
+ * the finished trace; violations joined by '\n' into buf (cap bytes,
+ * NUL-terminated, truncated to fit), *n_violations = their count (0 = sound). */
+int fr_run_trace_check(const fr_run_trace* t, char* buf, int64_t cap, int32_t* n_violations);
+/* write_trace_file / read_trace_file (trace.hpp:19-20): the JSONL stream --
+ * meta line (config, seed, profiles), records in timeline order,
+ * dispositions, end line; byte-stable for identical runs. */
+int fr_run_trace_write_jsonl(const fr_run_trace* t, const char* path);
+int fr_run_trace_read_jsonl(const char* path, fr_run_trace** out);
 
 /* time_increase  metrics.hpp:25 */
 int fr_time_increase(double t_no_seconds, double t_with_seconds, double* out);

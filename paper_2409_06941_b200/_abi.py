@@ -382,6 +382,9 @@ ENGINE_PROTOTYPES = {
     "fr_manager_push_task": (C.c_int, [vp, i32, cp]),
     "fr_run_experiment": (C.c_int, [P(ExperimentConfigC), i32, u64, P(vp)]),
     "fr_run_trace_destroy": (None, [vp]),
+    "fr_run_trace_check": (C.c_int, [vp, C.c_char_p, i64, P(i32)]),
+    "fr_run_trace_write_jsonl": (C.c_int, [vp, C.c_char_p]),
+    "fr_run_trace_read_jsonl": (C.c_int, [C.c_char_p, P(vp)]),
     "fr_run_trace_get_counts": (C.c_int, [vp, P(RunTraceCountsC)]),
     "fr_run_trace_ops": (C.c_int, [vp, P(OpEventC), i64]),
     "fr_run_trace_bubbles": (C.c_int, [vp, P(BubbleC), i64]),

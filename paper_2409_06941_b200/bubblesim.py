@@ -452,12 +452,15 @@ class BubbleSim:
     def run_experiment(self, cfg: PipelineConfig, tasks: Sequence[SideTaskSpec], seed: int,
                        with_tasks: bool = True, check_overhead: int = 1, rpc_latency: int = 0,
                        step_jitter: float = 0.0, profile_steps: int = 32, gate_max: bool = False,
-                       limits: LimitConfig = LimitConfig()) -> dict:  # engine.hpp:97-98
+                       limits: LimitConfig = LimitConfig(), check: bool = False,
+                       trace_path: Optional[str] = None) -> dict:  # engine.hpp:97-98
         """RunTrace as plain tuples: ops (stage, kind, mb, epoch, start, end);
         bubbles (stage, epoch, start, duration, avail, btype); submits/assigns/
         rejects (t, task, worker); rpcs/transitions (t, task, kind, worker);
         activities (start, end, task, worker, kind, clipped); kills
-        (t, task, worker, reason); dispositions (task, disposition, steps, worker)."""
+        (t, task, worker, reason); dispositions (task, disposition, steps, worker).
+        check: also run replay_check (engine.hpp:104) -> out["violations"];
+        trace_path: also write the JSONL trace stream (trace.hpp:19)."""
         if not self.has_engine:
             raise FreeRideError("library has no engine (the reference declares run_experiment only)")
         c = _Cfg(cfg)
@@ -498,7 +501,26 @@ class BubbleSim:
                                     d.worker if d.has_worker else None)
                                    for d in get(self.lib.fr_run_trace_dispositions, A.DispositionRecordC,
                                                 n.dispositions)]
+            if check:
+                out["violations"] = self._trace_check(h)
+            if trace_path is not None:
+                self._check(self.lib.fr_run_trace_write_jsonl(h, trace_path.encode()))
             return out
+        finally:
+            self.lib.fr_run_trace_destroy(h)
+
+    def _trace_check(self, h) -> List[str]:
+        n = C.c_int32()
+        buf = C.create_string_buffer(1 << 16)
+        self._check(self.lib.fr_run_trace_check(h, buf, len(buf), C.byref(n)))
+        return [x for x in buf.value.decode().split("\n") if x][: n.value] if n.value else []
+
+    def replay_check_file(self, path: str) -> List[str]:
+        """read_trace_file + replay_check (trace.hpp:20, engine.hpp:104)."""
+        h = C.c_void_p()
+        self._check(self.lib.fr_run_trace_read_jsonl(path.encode(), C.byref(h)))
+        try:
+            return self._trace_check(h)
         finally:
             self.lib.fr_run_trace_destroy(h)
 

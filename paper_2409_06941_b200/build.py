@@ -21,6 +21,7 @@ CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 OBJ = os.path.join(os.path.dirname(HERE), "build", "obj")
 OUT = os.path.join(HERE, "_lib", "libfreeride.so")
+SIM = os.path.join(HERE, "_lib", "freeride-sim")  # the CLI (csrc/tools, host objects only)
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 
@@ -33,7 +34,8 @@ NVCCFLAGS = ["-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC",
 
 
 def _sources():
-    cpp = sorted(glob.glob(os.path.join(CSRC, "**", "*.cpp"), recursive=True))
+    cpp = sorted(p for p in glob.glob(os.path.join(CSRC, "**", "*.cpp"), recursive=True)
+                 if os.sep + "tools" + os.sep not in p)
     cu = sorted(glob.glob(os.path.join(CSRC, "**", "*.cu"), recursive=True))
     return cpp, cu
 
@@ -93,6 +95,16 @@ def build(verbose: bool = False, jobs: int = 0) -> str:
               f"-L{CUDA}/lib64", "-lcublasLt", "-Xlinker", f"-rpath={CUDA}/lib64",
               "-Xcompiler", "-pthread"])
         shutil.move(tmp, OUT)
+    # the CLI: its own main + the pure-C++ host objects (no CUDA)
+    tool = os.path.join(CSRC, "tools", "freeride_sim.cpp")
+    tool_o = _obj_for(tool)
+    cxx = os.environ.get("CXX", "g++")
+    if _stale(tool, tool_o, hm):
+        _run([cxx, *CXXFLAGS, *INC, "-c", tool, "-o", tool_o])
+    host_objs = [_obj_for(s) for s in cpp if os.sep + "host" + os.sep in s]
+    if not os.path.exists(SIM) or any(os.path.getmtime(o) > os.path.getmtime(SIM) for o in host_objs + [tool_o]):
+        _run([cxx, "-o", SIM + ".tmp", tool_o, *host_objs, "-pthread"])
+        shutil.move(SIM + ".tmp", SIM)
     return OUT
 
 

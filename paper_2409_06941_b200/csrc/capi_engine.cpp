@@ -1,11 +1,13 @@
 // C-ABI of the simulated dispatch engine (fr_run_experiment and the RunTrace
 // getters).
+#include <algorithm>
 #include <cstring>
 #include <memory>
 
 #include "capi_util.hpp"
 #include "freeride.h"
 #include "host/freeride.hpp"
+#include "host/io.hpp"
 
 using namespace freeride;
 
@@ -167,6 +169,40 @@ int fr_run_trace_dispositions(const fr_run_trace* t, fr_disposition_record* out,
     frcapi::copy_id(out[i].task, v[i].task);
   }
   return FR_OK;
+}
+
+int fr_run_trace_check(const fr_run_trace* t, char* buf, int64_t cap, int32_t* n) {
+  if (!t || !n) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  return frcapi::guard([&]() -> int {
+    const std::vector<std::string> v = replay_check(t->t);
+    *n = static_cast<int32_t>(v.size());
+    if (buf && cap > 0) {
+      std::string all;
+      for (const auto& s : v) all += s + "\n";
+      const std::size_t k = std::min<std::size_t>(all.size(), static_cast<std::size_t>(cap - 1));
+      std::memcpy(buf, all.data(), k);
+      buf[k] = 0;
+    }
+    return FR_OK;
+  });
+}
+
+int fr_run_trace_write_jsonl(const fr_run_trace* t, const char* path) {
+  if (!t || !path) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  return frcapi::guard([&]() -> int {
+    write_trace_file(t->t, path);
+    return FR_OK;
+  });
+}
+
+int fr_run_trace_read_jsonl(const char* path, fr_run_trace** out) {
+  if (!path || !out) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  return frcapi::guard([&]() -> int {
+    auto tr = std::make_unique<fr_run_trace>();
+    tr->t = read_trace_file(path);
+    *out = tr.release();
+    return FR_OK;
+  });
 }
 
 }  // extern "C"

@@ -648,7 +648,11 @@ class Engine {
 
 RunTrace run_experiment(const ExperimentConfig& config, bool with_tasks, std::uint64_t seed) {
   Engine e(config, with_tasks, seed);
-  return e.run();
+  RunTrace t = e.run();
+  t.config = config;
+  t.seed = seed;
+  t.with_tasks = with_tasks;
+  return t;
 }
 
 }  // namespace freeride

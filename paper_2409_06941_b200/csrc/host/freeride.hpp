@@ -365,15 +365,27 @@ struct RuntimeOptions {  // config.hpp:19-27
   GateEstimate gate_estimate = GateEstimate::Mean;
 };
 
-struct ExperimentConfig {  // config.hpp:36-46 (JSON, prices and sweep out of scope)
+struct SweepGrid {  // config.hpp:29-35
+  std::vector<int> micro_batches;
+  std::vector<std::string> model_sizes;
+  std::vector<int> batch_sizes;
+};
+
+struct ExperimentConfig {  // config.hpp:36-46 (JSON I/O: host/io.hpp)
   PipelineConfig pipeline;
   std::vector<SideTaskSpec> tasks;
   LimitConfig limits;
+  PriceConfig prices;
   RuntimeOptions runtime;
+  std::optional<SweepGrid> sweep;
   std::uint64_t seed = 0;
 };
 
 struct RunTrace {  // engine.hpp:75-92
+  // RunMeta (engine.hpp:67-73)
+  ExperimentConfig config;
+  std::uint64_t seed = 0;
+  bool with_tasks = false;
   std::vector<OpEvent> ops;
   std::vector<Bubble> bubbles;            // as signalled on the delayed timeline
   std::vector<AssignRecord> submits;      // worker -1
