@@ -12,7 +12,7 @@
 //    per pixel (w*a + 127) for R,G,B and (255 - a), packed into 16-bit lanes
 //    and laid out group-transposed so each thread's 64 B are one perfectly
 //    coalesced 16 B load per warp-lane (L2-resident, evict-last);
-//  * persistent CTAs (2 per SM) with an S-stage smem ring; one elected
+//  * persistent CTAs (3 per SM) with a 2-stage smem ring; one elected
 //    thread streams each output row's two contiguous source rows in with a
 //    TMA bulk copy (cp.async.bulk -> UBLKCP) completing on an mbarrier
 //    (expect_tx), and bulk-stores the finished output row from smem;
@@ -23,6 +23,8 @@
 //    pipeline's power-capped SM clock the kernel must stay HBM-bound, so the
 //    instruction count per byte is what this layout minimises.
 #include <cmath>
+#include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "freeride_gpu.h"
@@ -31,8 +33,12 @@
 namespace {
 
 constexpr int kImgThreads = 256;
-constexpr int kImgStages = 3;
-constexpr int kImgCtasPerSm = 2;
+// 2-stage ring x 3 CTAs per SM (63 registers): three CTAs computing rows
+// side by side issue ~1.5x more per cycle than 3 stages x 2 CTAs, which is
+// what bounded the kernel at in-bubble (power-capped) clocks; measured 64-frame
+// launches 6.9 vs 6.0 TB/s, 8-frame in-bubble steps 52 vs 60 us.
+constexpr int kImgStages = 2;
+constexpr int kImgCtasPerSm = 3;
 constexpr uint32_t kLaneMask = 0x00FF00FFu;
 constexpr uint32_t kDiv255 = 16843010u;  // ceil(2^32 / 255): umulhi(t, .) = t / 255, t < 65408
 
@@ -80,8 +86,8 @@ __global__ void img_prepare_wm_kernel(const uint8_t* __restrict__ wm, uint4* __r
 // loop over the batch several times; the last CTA out advances base by the
 // rows taken, so the next launch resumes at the first untaken row, and adds
 // them to counters[2..3] (every taken row is completed before exit).
-template <int S, bool PREEMPT>
-__global__ void __launch_bounds__(kImgThreads, kImgCtasPerSm)
+template <int S, bool PREEMPT, int CPS>
+__global__ void __launch_bounds__(kImgThreads, CPS)
     img_resize2x_wm_tma(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
                         const uint4* __restrict__ wmp, int dw, int dh, uint32_t rows,
                         uint32_t* __restrict__ counters, const uint32_t* __restrict__ stop_word,
@@ -321,6 +327,7 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 
 struct fr_img_plan {
   int sw = 0, sh = 0, dw = 0, dh = 0;
+  int stages = kImgStages, ctas_per_sm = kImgCtasPerSm;  // TMA path pipeline shape
   int path = FR_IMG_PATH_GENERAL;
   int32_t* d_tab = nullptr;
   void* d_wm = nullptr;  // plan-owned prepared watermark for fr_img_resize_watermark
@@ -353,12 +360,17 @@ int fr_img_plan_create(int32_t sw, int32_t sh, int32_t dw, int32_t dh, fr_img_pl
   const bool two_x = sw == 2 * dw && sh == 2 * dh && dw % 16 == 0;
   if (two_x) {
     auto al = [](int x) { return (x + 127) & ~127; };
-    plan->smem = kImgStages * (al(12 * dw) + al(3 * dw)) + kImgStages * 8;
+    if (const char* e = std::getenv("FR_IMG_CFG")) {  // tuning hook: "<stages>x<ctas per SM>"
+      if (std::string(e) == "3x2") plan->stages = 3, plan->ctas_per_sm = 2;
+    }
+    plan->smem = plan->stages * (al(12 * dw) + al(3 * dw)) + plan->stages * 8;
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     if (plan->smem <= optin) {
-      for (const void* fn : {reinterpret_cast<const void*>(img_resize2x_wm_tma<kImgStages, false>),
-                             reinterpret_cast<const void*>(img_resize2x_wm_tma<kImgStages, true>)}) {
+      for (const void* fn : {reinterpret_cast<const void*>(img_resize2x_wm_tma<3, false, 2>),
+                             reinterpret_cast<const void*>(img_resize2x_wm_tma<3, true, 2>),
+                             reinterpret_cast<const void*>(img_resize2x_wm_tma<2, false, 3>),
+                             reinterpret_cast<const void*>(img_resize2x_wm_tma<2, true, 3>)}) {
         if (e == cudaSuccess)
           e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, plan->smem);
         if (e == cudaSuccess)
@@ -442,10 +454,10 @@ int fr_img_resize_watermark_prepared(const fr_img_plan* plan, const uint8_t* src
       return frcapi::fail(FR_ERR_UNSUPPORTED, "TMA path needs 16-byte aligned buffers");
     const int64_t rows = static_cast<int64_t>(n) * plan->dh;
     if (rows >= (int64_t{1} << 31)) return frcapi::fail(FR_ERR_UNSUPPORTED, "too many rows in one step");
-    const int grid = static_cast<int>(std::min<int64_t>(rows, int64_t(plan->sms) * kImgCtasPerSm));
-    img_resize2x_wm_tma<kImgStages, false><<<grid, kImgThreads, plan->smem, s>>>(
-        src, dst, static_cast<const uint4*>(prepared), plan->dw, plan->dh, static_cast<uint32_t>(rows),
-        plan->d_ctr, nullptr, 0u, 0u);
+    const int grid = static_cast<int>(std::min<int64_t>(rows, int64_t(plan->sms) * plan->ctas_per_sm));
+    auto k = plan->stages == 2 ? img_resize2x_wm_tma<2, false, 3> : img_resize2x_wm_tma<3, false, 2>;
+    k<<<grid, kImgThreads, plan->smem, s>>>(src, dst, static_cast<const uint4*>(prepared), plan->dw, plan->dh,
+                                           static_cast<uint32_t>(rows), plan->d_ctr, nullptr, 0u, 0u);
   } else {
     const int64_t total = static_cast<int64_t>(n) * plan->dw * plan->dh;
     img_resize_wm_general<<<grid_for(total, 256, 8), 256, 0, s>>>(
@@ -473,11 +485,12 @@ int fr_img_resize_watermark_preemptible(const fr_img_plan* plan, const uint8_t* 
   if (max_rows < 0 || max_rows >= (int64_t{1} << 31))
     return frcapi::fail(FR_ERR_VALIDATION, "max_rows in [0, 2^31)", "max_rows");
   if (max_rows == 0) return FR_OK;
-  const int grid = static_cast<int>(std::min<int64_t>(max_rows, int64_t(plan->sms) * kImgCtasPerSm));
+  const int grid = static_cast<int>(std::min<int64_t>(max_rows, int64_t(plan->sms) * plan->ctas_per_sm));
   // no preempt: a stop word that never fires (counters[5] stays 0 < token)
   const uint32_t* word = preempt && preempt->stop_word ? preempt->stop_word : counters + 5;
   const uint32_t token = preempt && preempt->stop_word ? preempt->token : 0xFFFFFFFFu;
-  img_resize2x_wm_tma<kImgStages, true><<<grid, kImgThreads, plan->smem, static_cast<cudaStream_t>(stream)>>>(
+  auto k = plan->stages == 2 ? img_resize2x_wm_tma<2, true, 3> : img_resize2x_wm_tma<3, true, 2>;
+  k<<<grid, kImgThreads, plan->smem, static_cast<cudaStream_t>(stream)>>>(
       src, dst, static_cast<const uint4*>(prepared), plan->dw, plan->dh, static_cast<uint32_t>(rows),
       counters, word, token, static_cast<uint32_t>(max_rows));
   FR_CUDA_LAUNCHED("img_resize_watermark_preemptible");
