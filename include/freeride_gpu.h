@@ -181,6 +181,9 @@ int fr_image_task_memory(const fr_image_task_config* cfg, double* gib);
 /* device pointers of the last processed batch slot (for checking) */
 int fr_image_task_buffers(void* user, const uint8_t** src, uint8_t** dst, const uint8_t** wm,
                           int64_t* steps_done);
+/* host_io = 1: the pinned host output batch [batch][dh][dw][3] (null before
+ * the first InitSideTask); rows of frames not yet processed are undefined */
+int fr_image_task_host_output(void* user, const uint8_t** h_dst);
 
 /* Synthetic side task: the reference's SideTaskSpec (task.hpp:33-50) made
  * real -- each RunNextStep is a spin kernel occupying every SM for step_ns,

@@ -559,6 +559,7 @@ GPU_PROTOTYPES.update({
     "fr_image_task_create": (C.c_int, [P(ImageTaskConfigC), P(SideTaskVTableC), P(vp)]),
     "fr_image_task_memory": (C.c_int, [P(ImageTaskConfigC), P(dbl)]),
     "fr_image_task_buffers": (C.c_int, [vp, P(vp), P(vp), P(vp), P(i64)]),
+    "fr_image_task_host_output": (C.c_int, [vp, P(vp)]),
     "fr_harness_create": (C.c_int, [P(HarnessConfigC), P(vp)]),
     "fr_synthetic_task_create": (C.c_int, [P(SyntheticTaskConfigC), P(SideTaskVTableC), P(vp)]),
     "fr_harness_task_status": (C.c_int, [vp, C.c_char_p, P(i32), P(i32), P(dbl)]),

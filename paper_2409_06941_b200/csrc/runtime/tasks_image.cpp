@@ -25,6 +25,13 @@ struct ImageTask {
   void* wmp = nullptr;  // prepared watermark (fr_img_prepare_watermark)
   uint8_t* h_src = nullptr;  // pinned host batch (host_io)
   uint8_t* h_dst = nullptr;
+  // host_io: double-buffered device frames; the next step's frames are
+  // prefetched on `pf` while this step's kernel and D2H run (joined before
+  // the step ends, so no work outlives its step)
+  cudaStream_t pf = nullptr;
+  cudaEvent_t e_pf = nullptr, e_free[2] = {nullptr, nullptr};
+  int cur = 0;
+  bool ready = false;
   uint32_t* ctr = nullptr;   // imperative: preemptible row cursor + rows completed
   uint64_t rows_base = 0;    // rows completed by earlier Init..Stop lifetimes
   int64_t cursor = 0;
@@ -68,8 +75,18 @@ int img_init(void* u, void* stream) {
   t->last = s;
   const fr_image_task_config& c = t->cfg;
   const std::size_t resident = c.host_io ? static_cast<std::size_t>(c.images_per_step) : static_cast<std::size_t>(c.batch);
-  int rc = cu(cudaMallocAsync(reinterpret_cast<void**>(&t->src), resident * t->src_img(), s), "src");
+  int rc = cu(cudaMallocAsync(reinterpret_cast<void**>(&t->src), (c.host_io ? 2 : 1) * resident * t->src_img(), s), "src");
   if (rc == FR_OK) rc = cu(cudaMallocAsync(reinterpret_cast<void**>(&t->dst), resident * t->dst_img(), s), "dst");
+  if (rc == FR_OK && c.host_io) {
+    if (!t->pf) {
+      rc = cu(cudaStreamCreateWithFlags(&t->pf, cudaStreamNonBlocking), "prefetch stream");
+      for (cudaEvent_t* e : {&t->e_pf, &t->e_free[0], &t->e_free[1]})
+        if (rc == FR_OK) rc = cu(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "prefetch events");
+    }
+    for (int b = 0; rc == FR_OK && b < 2; ++b) rc = cu(cudaEventRecord(t->e_free[b], s), "prefetch events");
+    t->cur = 0;
+    t->ready = false;
+  }
   if (rc == FR_OK) rc = cu(cudaMallocAsync(reinterpret_cast<void**>(&t->wm), static_cast<std::size_t>(c.dw) * c.dh * 4, s), "wm");
   int64_t pbytes = 0;
   if (rc == FR_OK) rc = fr_img_prepared_bytes(t->plan, &pbytes);
@@ -103,9 +120,25 @@ int img_step(void* u, void* stream) {
   const int n = c.images_per_step;
   int rc;
   if (c.host_io) {
-    rc = cu(cudaMemcpyAsync(t->src, t->h_src + i0 * t->src_img(), n * t->src_img(), cudaMemcpyHostToDevice, s), "H2D step");
-    if (rc == FR_OK) rc = fr_img_resize_watermark_prepared(t->plan, t->src, t->dst, t->wmp, n, s);
+    // frames i0.. are in buffer `cur` (prefetched by the previous step) or
+    // copied now; then kernel + D2H on the step's stream while the next
+    // step's frames stream into the other buffer on `pf` (PCIe is full
+    // duplex: H2D of step i+1 overlaps D2H of step i)
+    const std::size_t fb = static_cast<std::size_t>(n) * t->src_img();
+    uint8_t* buf = t->src + t->cur * fb;
+    rc = FR_OK;
+    if (!t->ready) rc = cu(cudaMemcpyAsync(buf, t->h_src + i0 * t->src_img(), fb, cudaMemcpyHostToDevice, s), "H2D step");
+    if (rc == FR_OK) rc = fr_img_resize_watermark_prepared(t->plan, buf, t->dst, t->wmp, n, s);
+    if (rc == FR_OK) rc = cu(cudaEventRecord(t->e_free[t->cur], s), "buffer free");
     if (rc == FR_OK) rc = cu(cudaMemcpyAsync(t->h_dst + i0 * t->dst_img(), t->dst, n * t->dst_img(), cudaMemcpyDeviceToHost, s), "D2H step");
+    const int other = t->cur ^ 1;
+    const int64_t next = (i0 + n) % c.batch;
+    if (rc == FR_OK) rc = cu(cudaStreamWaitEvent(t->pf, t->e_free[other], 0), "prefetch wait");
+    if (rc == FR_OK) rc = cu(cudaMemcpyAsync(t->src + other * fb, t->h_src + next * t->src_img(), fb, cudaMemcpyHostToDevice, t->pf), "H2D prefetch");
+    if (rc == FR_OK) rc = cu(cudaEventRecord(t->e_pf, t->pf), "prefetch done");
+    if (rc == FR_OK) rc = cu(cudaStreamWaitEvent(s, t->e_pf, 0), "prefetch join");
+    t->cur = other;
+    t->ready = true;
   } else {
     rc = fr_img_resize_watermark_prepared(t->plan, t->src + i0 * t->src_img(), t->dst + i0 * t->dst_img(), t->wmp, n, s);
   }
@@ -160,6 +193,9 @@ void img_destroy(void* u) {
   if (t->last) cudaStreamSynchronize(t->last);
   if (t->h_src) cudaFreeHost(t->h_src);
   if (t->h_dst) cudaFreeHost(t->h_dst);
+  for (cudaEvent_t e : {t->e_pf, t->e_free[0], t->e_free[1]})
+    if (e) cudaEventDestroy(e);
+  if (t->pf) cudaStreamDestroy(t->pf);
   fr_img_plan_destroy(t->plan);
   delete t;
 }
@@ -171,7 +207,8 @@ extern "C" {
 int fr_image_task_memory(const fr_image_task_config* c, double* gib) {
   if (!c || !gib) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
   const double resident = c->host_io ? c->images_per_step : c->batch;
-  const double bytes = resident * (double(c->sw) * c->sh * 3 + double(c->dw) * c->dh * 3) + double(c->dw) * c->dh * 12;
+  const double bytes = resident * ((c->host_io ? 2.0 : 1.0) * double(c->sw) * c->sh * 3 + double(c->dw) * c->dh * 3) +
+                       double(c->dw) * c->dh * 12;
   *gib = bytes / (1024.0 * 1024.0 * 1024.0);
   return FR_OK;
 }
@@ -211,6 +248,13 @@ int fr_image_task_buffers(void* user, const uint8_t** src, uint8_t** dst, const 
   if (dst) *dst = t->dst;
   if (wm) *wm = t->wm;
   if (steps) *steps = t->steps;
+  return FR_OK;
+}
+
+int fr_image_task_host_output(void* user, const uint8_t** h_dst) {
+  auto* t = static_cast<ImageTask*>(user);
+  if (!t || !h_dst) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  *h_dst = t->h_dst;
   return FR_OK;
 }
 

@@ -157,6 +157,18 @@ class ImageTask:
         self.h2d_per_step = images_per_step * sw * sh * 3 if host_io else 0
         self.d2h_per_step = images_per_step * dw * dh * 3 if host_io else 0
 
+    def host_outputs(self):
+        """host_io tasks: copy of the pinned host output batch (numpy)."""
+        import numpy as np
+        p = C.c_void_p()
+        check(glib().fr_image_task_host_output(self.user, C.byref(p)))
+        if not p.value:
+            return None
+        torch.cuda.synchronize()
+        n = self.batch * self.dh * self.dw * 3
+        return np.ctypeslib.as_array((C.c_uint8 * n).from_address(p.value)).copy().reshape(
+            self.batch, self.dh, self.dw, 3)
+
     def outputs(self):
         """Copy of the task's resident output batch [batch, dh, dw, 3] (None
         when the task holds no GPU state)."""
