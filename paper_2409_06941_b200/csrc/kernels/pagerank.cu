@@ -27,6 +27,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include "freeride_gpu.h"
@@ -177,11 +178,22 @@ __global__ void pr_reset_kernel(const int32_t* __restrict__ rowc, const float* _
   }
 }
 
-constexpr int kPrThreads = 1024;     // persistent: one CTA per SM
-constexpr int kPrWarps = kPrThreads / 32;
+// Persistent grid shape (tuning hook FR_PR_CFG): "1024x1" = one 1024-thread
+// CTA per SM with a 48 Ki-column hot prefix (default), "768x2" = two
+// 768-thread CTAs per SM (48 warps) with 27 Ki columns each.
+struct PrCfg {
+  int threads, ctas_per_sm, hot;
+};
+PrCfg pr_cfg() {
+  static const PrCfg c = [] {
+    const char* e = std::getenv("FR_PR_CFG");
+    if (e && std::string(e) == "768x2") return PrCfg{768, 2, 27648};
+    return PrCfg{1024, 1, 49152};
+  }();
+  return c;
+}
 constexpr int kSplitEdges = 256;     // default: rows with more in-edges are split into chunks
-constexpr int kDefaultHot = 49152;   // c[] prefix staged in shared memory (192 KB)
-constexpr int kMaxCtas = 256;        // split-row chunk lists per CTA (grid = SM count)
+constexpr int kMaxCtas = 512;        // split-row chunk lists per CTA (grid = SMs x CTAs per SM)
 constexpr int kMaxSlots = 256;       // split rows per CTA (shared-memory accumulators)
 
 struct PrArgs {
@@ -274,7 +286,9 @@ __device__ __forceinline__ double group_sum(double s, int lanes) {
 //      static round-robin over all warps (items are ordered heavy first and
 //      carry ~64..256 edges each);
 //  (3) the zero-in-degree tail, when asked.
-__global__ void __launch_bounds__(kPrThreads, 1) pr_pull_kernel(PrArgs a) {
+template <int kPrThreads, int MINB>
+__global__ void __launch_bounds__(kPrThreads, MINB) pr_pull_kernel(PrArgs a) {
+  constexpr int kPrWarps = kPrThreads / 32;
   extern __shared__ float4 hot4[];
   __shared__ double sacc[kMaxSlots];
   __shared__ int scnt[kMaxSlots];
@@ -349,7 +363,7 @@ int split_edges() {
 int hot_vertices(int32_t V) {
   static const int want = [] {
     const char* e = std::getenv("FR_PR_HOT");  // tuning hook
-    return e ? std::max(0, std::atoi(e)) : kDefaultHot;
+    return e ? std::max(0, std::atoi(e)) : pr_cfg().hot;
   }();
   return std::min(want, V) & ~3;
 }
@@ -425,7 +439,7 @@ int build_work(fr_pr_graph* g, cudaStream_t s) {
   g->istart[0] = items;
   // split rows -> CTAs, longest first onto the least-loaded CTA (LPT), at
   // most kMaxSlots rows per CTA; each CTA's chunks are contiguous.
-  const int ctas = std::min(g->sms, kMaxCtas);
+  const int ctas = std::min(g->sms * pr_cfg().ctas_per_sm, kMaxCtas);
   if (count[7] > ctas * kMaxSlots)
     return frcapi::fail(FR_ERR_UNSUPPORTED, "too many split rows for the per-CTA accumulators");
   std::vector<int32_t> order(count[7]);
@@ -686,9 +700,11 @@ int fr_pr_step(fr_pr_state* st, int32_t iters, float damping, void* stream) {
   a.damp = static_cast<double>(damping);
   a.base = (1.0 - static_cast<double>(damping)) / static_cast<double>(g->V);
   const size_t smem = static_cast<size_t>(a.hot) * sizeof(float);
+  const PrCfg cfg = pr_cfg();
+  auto kern = cfg.threads == 768 ? pr_pull_kernel<768, 2> : pr_pull_kernel<1024, 1>;
   static int smem_set = -1;  // per process; the attribute is per function
   if (static_cast<int>(smem) > smem_set) {
-    FR_CUDA_TRY(cudaFuncSetAttribute(pr_pull_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    FR_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
     smem_set = static_cast<int>(smem);
   }
@@ -700,7 +716,7 @@ int fr_pr_step(fr_pr_state* st, int32_t iters, float damping, void* stream) {
     a.c_in = st->c[st->cur];
     a.c_out = st->c[st->cur ^ 1];
     a.do_tail = st->tail_pending > 0;
-    pr_pull_kernel<<<std::min(g->sms, kMaxCtas), kPrThreads, smem, s>>>(a);
+    kern<<<std::min(g->sms * cfg.ctas_per_sm, kMaxCtas), cfg.threads, smem, s>>>(a);
     if (st->tail_pending > 0) --st->tail_pending;
     st->cur ^= 1;
     st->iterations++;
