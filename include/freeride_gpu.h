@@ -27,6 +27,10 @@ int fr_stream_create(int32_t priority_class /* 0 = lowest, 1 = highest */, void*
 int fr_stream_destroy(void* stream);
 int fr_stream_synchronize(void* stream);
 int fr_device_sm_count(int32_t* sms);
+/* the library's current device for the calling thread (it links its own
+ * CUDA runtime; set it once per thread, e.g. after torch.cuda.set_device) */
+int fr_set_device(int32_t device);
+int fr_get_device(int32_t* device);
 /* synchronous copy between any host/device buffers (unified addressing) */
 int fr_memcpy(void* dst, const void* src, int64_t bytes);
 /* diagnostics: spin `cycles` SM clocks on one warp, write {cycles, ns} */

@@ -433,6 +433,8 @@ GPU_PROTOTYPES = {
     "fr_stream_destroy": (C.c_int, [vp]),
     "fr_stream_synchronize": (C.c_int, [vp]),
     "fr_device_sm_count": (C.c_int, [P(i32)]),
+    "fr_set_device": (C.c_int, [i32]),
+    "fr_get_device": (C.c_int, [P(i32)]),
     "fr_clock_probe": (C.c_int, [vp, i64, vp]),
     "fr_memcpy": (C.c_int, [vp, vp, i64]),
     "fr_img_plan_create": (C.c_int, [i32, i32, i32, i32, P(vp)]),

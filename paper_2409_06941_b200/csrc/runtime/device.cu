@@ -56,6 +56,22 @@ int fr_stream_synchronize(void* stream) {
   return FR_OK;
 }
 
+// The library links its own (static) CUDA runtime: make its current device
+// explicit for the calling thread instead of relying on the driver context
+// another runtime (torch's) left current.
+int fr_set_device(int32_t device) {
+  FR_CUDA_TRY(cudaSetDevice(device));
+  return FR_OK;
+}
+
+int fr_get_device(int32_t* device) {
+  if (!device) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  int d = 0;
+  FR_CUDA_TRY(cudaGetDevice(&d));
+  *device = d;
+  return FR_OK;
+}
+
 int fr_device_sm_count(int32_t* sms) {
   int dev = 0, n = 0;
   FR_CUDA_TRY(cudaGetDevice(&dev));

@@ -1125,6 +1125,7 @@ int fr_harness_run(fr_harness* h, int32_t epochs, int32_t with_tasks, fr_run_rep
   if (!h || !out) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
   if (epochs < 1) return frcapi::fail(FR_ERR_VALIDATION, "epochs must be >= 1", "epochs");
   try {
+    ck(cudaSetDevice(h->device), "cudaSetDevice");  // any calling thread
     h->run(epochs, with_tasks != 0, out);
     return FR_OK;
   } catch (const HookError& e) {

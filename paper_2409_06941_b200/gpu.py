@@ -23,7 +23,15 @@ def glib() -> C.CDLL:
         lib = _load_lib()
         A.bind(lib, A.HOST_PROTOTYPES)
         _glib = A.bind(lib, A.GPU_PROTOTYPES)
+        if torch.cuda.is_available():  # start on torch's current device (this thread)
+            A.raise_for(_glib, _glib.fr_set_device(torch.cuda.current_device()))
     return _glib
+
+
+def set_device(device: int):
+    """The library links its own CUDA runtime: select its device for the
+    calling thread (glib() does it once for torch's current device)."""
+    check(glib().fr_set_device(device))
 
 
 def check(rc: int):

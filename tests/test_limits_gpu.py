@@ -70,12 +70,18 @@ def test_pause_timeout_kill(g, cooperative):
                            cooperative=cooperative)
     ok, _ = h.submit("overrun", task, profile_steps=4)
     assert ok
-    r = h.run(2, True)
-    assert r["kills_pause_timeout"] == 1 and r["kills_oom"] == 0
+    kills, longest = 0, 0.0
+    for _ in range(4):           # the overrunning step needs a bubble after InitSideTask's
+        r = h.run(2, True)
+        assert r["kills_oom"] == 0
+        kills += r["kills_pause_timeout"]
+        if r["kills_pause_timeout"]:
+            longest = max(b - a for a, b in h.timeline(2))
+            break
+    assert kills == 1
     st = h.task_status("overrun")
     assert st["state"] == "stopped" and st["disposition"] == "killed_pause_timeout"
     assert st["memory_used_gib"] < 1e-6
-    longest = max(b - a for a, b in h.timeline(2))
     if cooperative:
         assert longest < 0.3                     # cancelled, not run to 0.4 s
     else:
