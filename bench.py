@@ -10,10 +10,10 @@ SURVEY.md §7); with --gpus N each rank is an independent replica (no
 collective on the data path) -> scaling "weak".
 
 Headline workload (BASELINE.json configs[1]): the image resize + watermark
-side task (64 synthetic 4K RGB frames -> 1080p, RGBA watermark, 8 frames per
+side task (64 synthetic 4K RGB frames -> 1080p, RGBA watermark, 16 frames per
 RunNextStep).  The same run also measures configs[0] (PageRank, RMAT-20,
 one pull iteration per step), configs[2] (Graph-SGD, Orkut shape, rank
-16, 2^20 edges per step), configs[3] (mixed, 3.6B-shaped stages) and the
+16, 2^21 edges per step), configs[3] (mixed, 3.6B-shaped stages) and the
 image task through the imperative interface (device-preempted workload)
 under "workloads".
 
@@ -52,11 +52,11 @@ SHAPE_36B = dict(layers=9, hidden=2880, tokens=8192, ffn_mult=4)    # nanoGPT-3.
 LAYERS_6B, HIDDEN_6B = 32, 4096                                       # nanoGPT-6B (configs[4])
 FRAMES = dict(sw=3840, sh=2160, dw=1920, dh=1080)
 BATCH = 64
-IMAGES_PER_STEP = 8
+IMAGES_PER_STEP = 16   # ~100 us steps: 3 us inter-step gaps cost 3 % (8 frames: 5.5 %)
 E2E_IMAGES_PER_STEP = 1
 OUT_PX = FRAMES["dw"] * FRAMES["dh"]
-PR = dict(scale=20, edge_factor=16, seed=1, iters_per_step=1)
-SGD = dict(V=3072441, E=117185083, k=16, edge_seed=2, init_seed=3, edges_per_step=1 << 20)
+PR = dict(scale=20, edge_factor=16, seed=1, iters_per_step=2)
+SGD = dict(V=3072441, E=117185083, k=16, edge_seed=2, init_seed=3, edges_per_step=1 << 21)
 METRIC = "side-task px/s per bubble-sec at <=1% pipeline dT (image 4K->1080p+watermark); HBM GB/s vs peak"
 UNIT = "px/bubble-s"
 WORKLOAD = ("image resize+watermark side task (64x 3840x2160 RGB -> 1920x1080, RGBA watermark), "
@@ -363,7 +363,7 @@ def emit(args, results, ws, names, csr):
     traffic, timgs = load_ncu_traffic()
     if traffic and timgs and timgs != IMAGES_PER_STEP:
         traffic = traffic / timgs * IMAGES_PER_STEP
-    image_roof = roof("image", "img_resize2x_wm_tma (8 frames/launch, in-pipeline)")
+    image_roof = roof("image", f"img_resize2x_wm_tma ({IMAGES_PER_STEP} frames/launch, in-pipeline)")
     image_roof["traffic"] = traffic
     cpu = cpu_image(args.cpu_seconds) if not args.no_cpu else None
     e2e = None
@@ -374,15 +374,15 @@ def emit(args, results, ws, names, csr):
                "dT": dT("image_e2e"), "fill": fill("image_e2e"),
                "path": "fr_image_task host_io=1: pinned host frames, H2D + K5 + D2H per RunNextStep"}
     workloads = {
-        "pagerank": {"config": "configs[0]: RMAT scale 20 (edge factor 16, seed 1), pull, d=0.85, 1 iteration/step",
+        "pagerank": {"config": "configs[0]: RMAT scale 20 (edge factor 16, seed 1), pull, d=0.85, 2 iterations/step",
                      "value": rate("pagerank"), "unit": "edges/bubble-s", "dT": dT("pagerank"),
                      "fill": fill("pagerank"),
-                     "roofline": roof("pagerank", "pr_pull_kernel (1 iteration/launch, in-pipeline); "
+                     "roofline": roof("pagerank", "pr_pull_kernel (2 launches of 1 iteration per step, in-pipeline); "
                                       "working set L2-resident: latency-bound gathers, not HBM"),
                      "cpu_baseline": cpu_pagerank(args.cpu_seconds / 2, csr) if csr is not None else None},
-        "sgd": {"config": "configs[2]: Orkut shape V=3,072,441 E=117,185,083 k=16, 2^20 edges/step",
+        "sgd": {"config": "configs[2]: Orkut shape V=3,072,441 E=117,185,083 k=16, 2^21 edges/step",
                 "value": rate("sgd"), "unit": "edges/bubble-s", "dT": dT("sgd"), "fill": fill("sgd"),
-                "roofline": roof("sgd", "sgd_step_kernel<16> (2^20 edges/launch, in-pipeline)"),
+                "roofline": roof("sgd", "sgd_step_kernel<16> (2^21 edges/launch, in-pipeline)"),
                 "cpu_baseline": cpu_sgd(args.cpu_seconds / 2) if not args.no_cpu else None},
     }
     imp = results[0]["image_imperative"]
