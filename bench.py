@@ -302,6 +302,20 @@ def ours(args):
         mixed["dT_max"] = max(x["dT"] for x in mixed["stages"])
         mixed["fill_mean"] = statistics.fmean(x["fill"] for x in mixed["stages"])
     local_res["mixed"] = mixed
+    # configs[4] at N = 1: one stage of the 8-stage, m = 8 pipeline of
+    # nanoGPT-6B-shaped stages (32/8 layers of h = 4096 each), replayed
+    c5 = None
+    if not args.no_c5:
+        h = gpu.Harness(num_stages=8, num_micro_batches=8, stage=3, layers=LAYERS_6B // 8, hidden=HIDDEN_6B,
+                        tokens=8192, ffn_mult=4)
+        prof = h.profile()
+        r = harvest(h, "image", gpu.ImageTask(batch=BATCH, images_per_step=IMAGES_PER_STEP, **FRAMES), K, W)
+        h.close()
+        c5 = {"bubble_rate": prof["bubble_rate"], "fp_ms": prof["fp_ticks"] / 1e6, "bp_ms": prof["bp_ticks"] / 1e6,
+              "units_per_bubble_s": r["with"]["work_units"] / r["base"]["bubble_s"],
+              "dT": (r["with"]["makespan_s"] - r["base"]["makespan_s"]) / r["base"]["makespan_s"],
+              "fill": r["with"]["used_s"] / r["with"]["bubble_s"]}
+    local_res["c5"] = c5
     # configs[4] / SURVEY §8(e): with N > 1 GPUs, additionally a REAL N-stage
     # pipeline (6B-shaped stages, rank s = stage s) whose activations and
     # gradients travel through the peer-linked mailboxes (NVLink), one
@@ -428,6 +442,11 @@ def emit(args, results, ws, names, csr):
             "stages": [{"stage": x["stage"], "dT": (x["with"]["makespan_s"] - x["base"]["makespan_s"])
                         / x["base"]["makespan_s"], "fill": x["with"]["used_s"] / max(1e-12, x["with"]["bubble_s"])}
                        for x in ls]}
+    if results[0].get("c5"):
+        workloads["c5_stage_replay"] = dict(
+            results[0]["c5"], unit=UNIT,
+            config="configs[4] at one GPU: stage 3 of an 8-stage m=8 1F1B pipeline of nanoGPT-6B-shaped "
+                   "stages (4 layers x h 4096 each) replayed, image side task, 16 frames/step")
     if results[0].get("mixed"):
         workloads["mixed"] = dict(results[0]["mixed"],
                                   config="configs[3]: PageRank + SGD + Image + PageRank on a "
@@ -470,6 +489,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-mixed", action="store_true")
     ap.add_argument("--no-linked", action="store_true", help="skip the real N-stage pipeline (N > 1)")
+    ap.add_argument("--no-c5", action="store_true", help="skip the 8-stage 6B-shaped stage replay")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
