@@ -442,6 +442,27 @@ def emit(args, results, ws, names, csr):
             "stages": [{"stage": x["stage"], "dT": (x["with"]["makespan_s"] - x["base"]["makespan_s"])
                         / x["base"]["makespan_s"], "fill": x["with"]["used_s"] / max(1e-12, x["with"]["bubble_s"])}
                        for x in ls]}
+    if not args.no_cpu:
+        # host hot path: ours vs the reference's own sources
+        # (oracle/_ref) as the CPU baseline, same C-ABI, C++ time only
+        sys.path.insert(0, os.path.join(ROOT, "scripts"))
+        import host_path_bench  # noqa: E402
+        from paper_2409_06941_b200 import api as host_api
+        from paper_2409_06941_b200.bubblesim import BubbleSim, PipelineConfig
+        import ctypes
+        ref_so = os.path.join(ROOT, "oracle", "_ref", "libbubblesim_ref.so")
+        ref = BubbleSim(ctypes.CDLL(ref_so)) if os.path.exists(ref_so) else None
+        hp = {}
+        for name, (p, m) in {"C1_p4_m4_128ep": (4, 4), "C5_p8_m8_128ep": (8, 8)}.items():
+            cfg = PipelineConfig(p, m, [220], [347], 128, 48.0, [1.0] * p, 1e-3)
+            (b, x), n_ops, n_b = host_path_bench.time_host(host_api(), cfg)
+            row = {"ops": n_ops, "bubbles": n_b, "build_schedule_ms": b * 1e3, "extract_bubbles_ms": x * 1e3}
+            if ref:
+                (rb, rx), _, _ = host_path_bench.time_host(ref, cfg)
+                row["cpu_baseline"] = {"kind": "reference", "cores": 1, "build_schedule_ms": rb * 1e3,
+                                       "extract_bubbles_ms": rx * 1e3, "speedup": (rb + rx) / (b + x)}
+            hp[name] = row
+        workloads["host_path"] = hp
     if results[0].get("c5"):
         workloads["c5_stage_replay"] = dict(
             results[0]["c5"], unit=UNIT,
