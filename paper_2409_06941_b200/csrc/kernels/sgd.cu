@@ -97,8 +97,13 @@ __device__ __forceinline__ void apply(float4* p, const float4& d) { atomicAdd(p,
 // iteration (EPI x 2 latent-row loads in flight per lane), and the next
 // iteration's (u, v, r) load while this iteration's rows are in flight.
 // MINB: CTAs per SM the register allocation must allow (occupancy vs ILP).
+// Register cap: four 256-thread CTAs per SM with <= 60 registers leave room
+// for a resident 1-warp kernel (the stage's dependency wait in a bubble);
+// at 64 registers the fourth CTA of that SM could not launch and ran its
+// static share as a tail (in-bubble steps 34 % slower than alone).
 template <int K, int MINB, int EPI>
-__global__ void __launch_bounds__(kSgdThreads, MINB) sgd_step_kernel(
+__global__ void __launch_bounds__(kSgdThreads)
+    __maxnreg__(EPI >= 4 ? (MINB >= 4 ? 64 : 128) : (MINB >= 6 ? 40 : 60)) sgd_step_kernel(
     const int32_t* __restrict__ us, const int32_t* __restrict__ vs, const float* __restrict__ rs,
     float* __restrict__ L, int64_t e0, int64_t e1, float eta, float lam) {
   constexpr int LN = Row<K>::kLanes;
