@@ -205,11 +205,18 @@ def harvest(h, name, task, K, W):
 def ours(args):
     import torch
     ws, rank, local = dist_env()
-    torch.cuda.set_device(local)
+    # one rank per GPU; FR_DIST_BACKEND=gloo + more ranks than GPUs is the
+    # single-GPU rehearsal of the multi-rank path (ranks share a device)
+    device = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(device)
     dist = None
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("FR_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", device))
+        else:
+            dist.init_process_group(backend)
     from paper_2409_06941_b200 import gpu
     gpu.glib()
     K, W = args.steps, args.warmup
@@ -219,7 +226,7 @@ def ours(args):
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    with Clocks(local) as clk:
+    with Clocks(device) as clk:
         for s in range(STAGES):
             h = gpu.Harness(num_stages=STAGES, num_micro_batches=MICRO_BATCHES, stage=s, **SHAPE)
             stage_prof.append(h.profile())
