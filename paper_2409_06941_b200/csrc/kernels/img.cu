@@ -71,6 +71,56 @@ __global__ void img_prepare_wm_kernel(const uint8_t* __restrict__ wm, uint4* __r
   }
 }
 
+// One thread's 8 output pixels: the two source rows' 48 B each (ra/rb at the
+// group's offset), the 16 prepared-watermark words, 24 B written to po.
+__device__ __forceinline__ void img_group8(const uint8_t* __restrict__ ra, const uint8_t* __restrict__ rb,
+                                       const uint32_t (&wv)[16], uint8_t* po8, int g) {
+  uint32_t va[12], vb[12];
+  const uint4* pa = reinterpret_cast<const uint4*>(ra + 48 * g);
+  const uint4* pb = reinterpret_cast<const uint4*>(rb + 48 * g);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const uint4 x = pa[i], z = pb[i];
+    va[4 * i + 0] = x.x; va[4 * i + 1] = x.y; va[4 * i + 2] = x.z; va[4 * i + 3] = x.w;
+    vb[4 * i + 0] = z.x; vb[4 * i + 1] = z.y; vb[4 * i + 2] = z.z; vb[4 * i + 3] = z.w;
+  }
+  // vertical sums in 16-bit lanes: ev = bytes (0,2), od = bytes (1,3)
+  uint32_t ev[12], od[12];
+#pragma unroll
+  for (int i = 0; i < 12; ++i) {
+    ev[i] = (va[i] & kLaneMask) + (vb[i] & kLaneMask);
+    od[i] = __byte_perm(va[i], 0u, 0x4341) + __byte_perm(vb[i], 0u, 0x4341);
+  }
+  uint32_t rgb[8];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {  // pixel pair (2q, 2q+1) = source words 3q..3q+2
+    const uint32_t e0 = ev[3 * q], e1 = ev[3 * q + 1], e2 = ev[3 * q + 2];
+    const uint32_t o0 = od[3 * q], o1 = od[3 * q + 1], o2 = od[3 * q + 2];
+    uint32_t rg[2], bb;
+    rg[0] = __byte_perm(e0, o0, 0x5410) + __byte_perm(o0, e1, 0x5432) + 0x00020002u;  // R0|G0
+    rg[1] = __byte_perm(e1, o1, 0x7632) + __byte_perm(o2, e2, 0x7610) + 0x00020002u;  // R1|G1
+    bb = __byte_perm(e0, e2, 0x5432) + __byte_perm(o1, o2, 0x7610) + 0x00020002u;     // B0|B1
+    rg[0] = (rg[0] >> 2) & kLaneMask;
+    rg[1] = (rg[1] >> 2) & kLaneMask;
+    bb = (bb >> 2) & kLaneMask;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const uint32_t wrg = wv[4 * q + 2 * j], wbna = wv[4 * q + 2 * j + 1];
+      const uint32_t na = wbna >> 16;
+      const uint32_t t = rg[j] * na + wrg;  // R,G lanes share alpha
+      const uint32_t u = t + __byte_perm(t, 0u, 0x4341) + 0x00010001u;
+      const uint32_t qrg = __byte_perm(u, 0u, 0x4341);  // (t + 1 + (t>>8)) >> 8 per lane
+      const uint32_t b = j ? (bb >> 16) : (bb & 0xFFFFu);
+      const uint32_t qb = __umulhi(b * na + (wbna & 0xFFFFu), kDiv255);
+      rgb[2 * q + j] = __byte_perm(qrg, qb, 0x0420);  // R G B _
+    }
+  }
+  uint2* po = reinterpret_cast<uint2*>(po8);
+  po[0] = make_uint2(__byte_perm(rgb[0], rgb[1], 0x4210), __byte_perm(rgb[1], rgb[2], 0x5421));
+  po[1] = make_uint2(__byte_perm(rgb[2], rgb[3], 0x6542), __byte_perm(rgb[4], rgb[5], 0x4210));
+  po[2] = make_uint2(__byte_perm(rgb[5], rgb[6], 0x5421), __byte_perm(rgb[6], rgb[7], 0x6542));
+    }
+
 // Rows are handed out dynamically (one atomicAdd per row by the elected
 // thread) rather than statically strided: in a pipeline bubble some SMs may
 // be unavailable (the stage's dependency-wait kernel, an NCCL receive, the
@@ -160,50 +210,7 @@ __global__ void __launch_bounds__(kImgThreads, CPS)
         wv[4 * j + 0] = x.x; wv[4 * j + 1] = x.y; wv[4 * j + 2] = x.z; wv[4 * j + 3] = x.w;
       }
       frk::mbar_wait(&full[s], (k / S) & 1u);
-      uint32_t va[12], vb[12];
-      const uint4* pa = reinterpret_cast<const uint4*>(ra + 48 * g);
-      const uint4* pb = reinterpret_cast<const uint4*>(rb + 48 * g);
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        const uint4 x = pa[i], z = pb[i];
-        va[4 * i + 0] = x.x; va[4 * i + 1] = x.y; va[4 * i + 2] = x.z; va[4 * i + 3] = x.w;
-        vb[4 * i + 0] = z.x; vb[4 * i + 1] = z.y; vb[4 * i + 2] = z.z; vb[4 * i + 3] = z.w;
-      }
-      // vertical sums in 16-bit lanes: ev = bytes (0,2), od = bytes (1,3)
-      uint32_t ev[12], od[12];
-#pragma unroll
-      for (int i = 0; i < 12; ++i) {
-        ev[i] = (va[i] & kLaneMask) + (vb[i] & kLaneMask);
-        od[i] = __byte_perm(va[i], 0u, 0x4341) + __byte_perm(vb[i], 0u, 0x4341);
-      }
-      uint32_t rgb[8];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {  // pixel pair (2q, 2q+1) = source words 3q..3q+2
-        const uint32_t e0 = ev[3 * q], e1 = ev[3 * q + 1], e2 = ev[3 * q + 2];
-        const uint32_t o0 = od[3 * q], o1 = od[3 * q + 1], o2 = od[3 * q + 2];
-        uint32_t rg[2], bb;
-        rg[0] = __byte_perm(e0, o0, 0x5410) + __byte_perm(o0, e1, 0x5432) + 0x00020002u;  // R0|G0
-        rg[1] = __byte_perm(e1, o1, 0x7632) + __byte_perm(o2, e2, 0x7610) + 0x00020002u;  // R1|G1
-        bb = __byte_perm(e0, e2, 0x5432) + __byte_perm(o1, o2, 0x7610) + 0x00020002u;     // B0|B1
-        rg[0] = (rg[0] >> 2) & kLaneMask;
-        rg[1] = (rg[1] >> 2) & kLaneMask;
-        bb = (bb >> 2) & kLaneMask;
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const uint32_t wrg = wv[4 * q + 2 * j], wbna = wv[4 * q + 2 * j + 1];
-          const uint32_t na = wbna >> 16;
-          const uint32_t t = rg[j] * na + wrg;  // R,G lanes share alpha
-          const uint32_t u = t + __byte_perm(t, 0u, 0x4341) + 0x00010001u;
-          const uint32_t qrg = __byte_perm(u, 0u, 0x4341);  // (t + 1 + (t>>8)) >> 8 per lane
-          const uint32_t b = j ? (bb >> 16) : (bb & 0xFFFFu);
-          const uint32_t qb = __umulhi(b * na + (wbna & 0xFFFFu), kDiv255);
-          rgb[2 * q + j] = __byte_perm(qrg, qb, 0x0420);  // R G B _
-        }
-      }
-      uint2* po = reinterpret_cast<uint2*>(orow + 24 * g);
-      po[0] = make_uint2(__byte_perm(rgb[0], rgb[1], 0x4210), __byte_perm(rgb[1], rgb[2], 0x5421));
-      po[1] = make_uint2(__byte_perm(rgb[2], rgb[3], 0x6542), __byte_perm(rgb[4], rgb[5], 0x4210));
-      po[2] = make_uint2(__byte_perm(rgb[5], rgb[6], 0x5421), __byte_perm(rgb[6], rgb[7], 0x6542));
+      img_group8(ra, rb, wv, orow + 24 * g, g);
     }
     frk::fence_proxy_async_smem();
     // Before anyone writes the next stage's output buffer, the bulk store
@@ -456,8 +463,9 @@ int fr_img_resize_watermark_prepared(const fr_img_plan* plan, const uint8_t* src
     if (rows >= (int64_t{1} << 31)) return frcapi::fail(FR_ERR_UNSUPPORTED, "too many rows in one step");
     const int grid = static_cast<int>(std::min<int64_t>(rows, int64_t(plan->sms) * plan->ctas_per_sm));
     auto k = plan->stages == 2 ? img_resize2x_wm_tma<2, false, 3> : img_resize2x_wm_tma<3, false, 2>;
-    k<<<grid, kImgThreads, plan->smem, s>>>(src, dst, static_cast<const uint4*>(prepared), plan->dw, plan->dh,
-                                           static_cast<uint32_t>(rows), plan->d_ctr, nullptr, 0u, 0u);
+    k<<<grid, kImgThreads, plan->smem, s>>>(
+        src, dst, static_cast<const uint4*>(prepared), plan->dw, plan->dh, static_cast<uint32_t>(rows), plan->d_ctr,
+        nullptr, 0u, 0u);
   } else {
     const int64_t total = static_cast<int64_t>(n) * plan->dw * plan->dh;
     img_resize_wm_general<<<grid_for(total, 256, 8), 256, 0, s>>>(
