@@ -1,0 +1,47 @@
+"""Small invocations of every side-task kernel for compute-sanitizer
+(memcheck / racecheck / synccheck): K5 TMA + general + preemptible paths,
+PageRank build + pull, SGD generate + step + RMSE, the synthetic step."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2409_06941_b200 import gpu  # noqa: E402
+
+gpu.glib()
+s = gpu.low_priority_stream()
+# K5: exact-2x TMA path, general path, preemptible path
+plan = gpu.ImagePlan(640, 360, 320, 180)
+src = gpu.img_generate(3, 640, 360, seed=1)
+wm = gpu.img_generate_watermark(320, 180, seed=2)
+dst = torch.empty((3, 180, 320, 3), dtype=torch.uint8, device="cuda")
+plan.run(src, dst, wm, stream=s)
+prep = plan.prepare(wm, stream=s)
+ctr = torch.zeros(8, dtype=torch.int32, device="cuda")
+plan.run_preemptible(src, dst, prep, ctr, max_rows=700, stream=s)
+gen = gpu.ImagePlan(300, 200, 170, 90)
+src2 = gpu.img_generate(2, 300, 200, seed=3)
+wm2 = gpu.img_generate_watermark(170, 90, seed=4)
+dst2 = torch.empty((2, 90, 170, 3), dtype=torch.uint8, device="cuda")
+gen.run(src2, dst2, wm2, stream=s)
+# PageRank: all-hot (scale 12) and partial hot prefix + split rows (scale 16)
+for scale in (12, 16):
+    g = gpu.PageRankGraph(scale=scale, edge_factor=16, seed=5)
+    st = gpu.PageRankState(g)
+    st.reset(stream=s)
+    st.step(3, 0.85, stream=s)
+    s.synchronize()
+# SGD
+p = gpu.SgdProblem(V=5000, E=40000, k=16, edge_seed=6, init_seed=7)
+p.step(0, 40000, stream=s)
+p.rmse()
+s.synchronize()
+# the runtime: gap / stamp kernels, a short harvest with the synthetic task
+h = gpu.Harness(num_stages=2, num_micro_batches=2, stage=1, layers=1, hidden=512, tokens=1024,
+                profile_reps=1, profile_epochs=1)
+h.submit("syn", gpu.SyntheticTask(step_ns=50_000, memory_demand_gib=0.01), profile_steps=2)
+h.run(2, True)
+h.close()
+torch.cuda.synchronize()
+print("sanitize workload done")
