@@ -106,3 +106,63 @@ def test_host_io_prefetch_pipeline_bit_exact(g, sidetask_oracle):
     import numpy as np
     assert np.array_equal(task.host_outputs(), want)
     h.close()
+
+
+def test_python_side_task(g):
+    """The paper's Python interface: a side task written as
+    Python hooks, its steps torch ops enqueued on the worker's low-priority
+    stream; the hook order follows the state machine and finished() stops it."""
+    import torch
+
+    class Axpy(g.PythonTask):
+        work_units_per_step = 1.0
+
+        def __init__(self):
+            super().__init__()
+            self.calls = []
+            self.x = None
+
+        def create(self):
+            self.calls.append("create")
+
+        def init(self, stream):
+            self.calls.append("init")
+            with torch.cuda.stream(torch.cuda.ExternalStream(stream)):
+                self.x = torch.ones(1 << 24, device="cuda")
+
+        def start(self):
+            self.calls.append("start")
+
+        def run_next_step(self, stream):
+            with torch.cuda.stream(torch.cuda.ExternalStream(stream)):
+                self.x.mul_(0.5).add_(0.5)   # stays 1.0 exactly
+
+        def pause(self):
+            self.calls.append("pause")
+
+        def stop(self):
+            self.calls.append("stop")
+
+        def finished(self, steps):
+            return steps >= 40
+
+    h = small_harness(g, stage=1)
+    task = Axpy()
+    ok, prof = h.submit("py", task, profile_steps=4)
+    assert ok and prof["est_per_step_duration"] > 0 and task.error is None
+    done = 0
+    for _ in range(6):
+        r = h.run(2, True)
+        done += r["steps_completed"]
+        if h.task_status("py")["state"] == "stopped":
+            break
+    assert task.error is None
+    assert h.task_status("py")["state"] == "stopped" and h.task_status("py")["disposition"] == "completed"
+    assert done >= 40
+    # profiling instance: create, init, stop; then the run: create, init, start, ..., stop
+    c = task.calls
+    assert c[:3] == ["create", "init", "stop"] and c[3:5] == ["create", "init"] and c[5] == "start"
+    assert c[-1] == "stop" and all(x in ("start", "pause") for x in c[6:-1])
+    torch.cuda.synchronize()
+    assert float(task.x.min()) == 1.0 and float(task.x.max()) == 1.0
+    h.close()
