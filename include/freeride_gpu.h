@@ -156,7 +156,13 @@ typedef struct fr_side_task_vtable {
    * preempt word fires, keeping its progress for the next call); work_done
    * reports cumulative completed work units (may synchronise `stream`). */
   int32_t interface_kind;     /* enum fr_interface: FR_ITERATIVE = 0, FR_IMPERATIVE = 1 */
-  int32_t reserved;
+  /* L1/shared split the task's kernels want on the SMs during its bubbles
+   * (cudaFuncAttributePreferredSharedMemoryCarveout percent; -1 = no
+   * preference).  The stage's resident dependency-wait kernel pins its SM's
+   * split for the whole bubble, so the harness launches it with the split the
+   * tasks want: max-L1 (0) only when every task asks for it (random-access
+   * kernels whose loads in flight live in L1), else max-shared. */
+  int32_t carveout_hint;
   int (*run_gpu_workload)(void* user, void* stream, const fr_preempt* preempt);
   int (*work_done)(void* user, void* stream, double* units);
   /* Framework-enforced kill (limits.hpp:34 framework_enforce, check_memory

@@ -462,7 +462,7 @@ class SideTaskVTableC(Struct):
         ("destroy", C.CFUNCTYPE(None, vp)),
         ("work_units_per_step", C.c_double),
         ("interface_kind", i32),
-        ("reserved", i32),
+        ("carveout_hint", i32),
         ("run_gpu_workload", C.CFUNCTYPE(C.c_int, vp, vp, vp)),
         ("work_done", C.CFUNCTYPE(C.c_int, vp, vp, P(C.c_double))),
         ("cancel", C.CFUNCTYPE(C.c_int, vp)),

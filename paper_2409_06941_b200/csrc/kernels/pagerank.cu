@@ -872,6 +872,7 @@ int fr_pagerank_task_create(const fr_pagerank_task_config* c, fr_side_task_vtabl
     return rc;
   }
   std::memset(vt, 0, sizeof(*vt));
+  vt->carveout_hint = 100;
   vt->create = pr_task_create;
   vt->init = pr_task_init;
   vt->run_next_step = pr_task_step;

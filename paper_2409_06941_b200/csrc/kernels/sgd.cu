@@ -103,7 +103,7 @@ __device__ __forceinline__ void apply(float4* p, const float4& d) { atomicAdd(p,
 // static share as a tail (in-bubble steps 34 % slower than alone).
 template <int K, int MINB, int EPI>
 __global__ void __launch_bounds__(kSgdThreads)
-    __maxnreg__(EPI >= 4 ? (MINB >= 4 ? 64 : 128) : (MINB >= 6 ? 40 : 60)) sgd_step_kernel(
+    __maxnreg__(EPI >= 4 ? (MINB >= 4 ? 64 : 128) : (MINB >= 6 ? 40 : 56)) sgd_step_kernel(
     const int32_t* __restrict__ us, const int32_t* __restrict__ vs, const float* __restrict__ rs,
     float* __restrict__ L, int64_t e0, int64_t e1, float eta, float lam) {
   constexpr int LN = Row<K>::kLanes;
@@ -221,6 +221,12 @@ template <int K, int MINB, int EPI>
 void launch_step_v(fr_sgd_problem* p, int64_t a, int64_t b, float eta, float lam, cudaStream_t s) {
   // persistent-style grid: exactly the resident CTAs (no second partial wave)
   static const int per_sm = [] {
+    // The random latent-row loads land in L1: with the max-shared carveout
+    // the pipeline's GEMMs leave behind (28 KB of L1) the loads in flight per
+    // SM are capped and a step is ~45 % slower.  Ask for the max-L1 split so
+    // the SMs are reconfigured when the step's CTAs arrive.
+    cudaFuncSetAttribute(sgd_step_kernel<K, MINB, EPI>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxL1);
     int n = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sgd_step_kernel<K, MINB, EPI>, kSgdThreads, 0);
     return std::max(1, n);
@@ -460,6 +466,7 @@ int fr_sgd_task_create(const fr_sgd_task_config* c, fr_side_task_vtable* vt, voi
     return rc;
   }
   std::memset(vt, 0, sizeof(*vt));
+  vt->carveout_hint = 0;
   vt->create = sgd_task_create;
   vt->init = sgd_task_init;
   vt->run_next_step = sgd_task_step;

@@ -398,6 +398,17 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
   pool_used = 0;
   std::memset(ring, 0, sizeof(RingSlot) * kRingSlots);
   ck(cudaMemset(&ctl->end_seq, 0, 2 * sizeof(std::uint32_t)), "end_seq / link_timeouts reset");
+  // the wait kernels' L1/shared split: max-L1 only if every task wants it
+  bool all_l1 = false;
+  for (const auto& kv : tasks) {
+    if (kv.second->rt.state == SideTaskState::Stopped) continue;
+    if (kv.second->vt.carveout_hint != 0) {
+      all_l1 = false;
+      break;
+    }
+    all_l1 = true;
+  }
+  set_wait_kernel_carveout(all_l1 ? cudaSharedmemCarveoutMaxL1 : cudaSharedmemCarveoutMaxShared);
   calibrate();
   // this harness's streams only: a device-wide sync would wait on a linked
   // neighbour's dependency spin in the same process (deadlock)

@@ -225,6 +225,7 @@ int fr_image_task_create(const fr_image_task_config* c, fr_side_task_vtable* vt,
   if (!t) return frcapi::fail(FR_ERR_INVARIANT, "out of host memory");
   t->cfg = *c;
   std::memset(vt, 0, sizeof(*vt));
+  vt->carveout_hint = 100;
   vt->create = img_create;
   vt->init = img_init;
   vt->run_next_step = img_step;

@@ -134,6 +134,7 @@ extern "C" int fr_synthetic_task_create(const fr_synthetic_task_config* c, fr_si
     return rc;
   }
   std::memset(vt, 0, sizeof(*vt));
+  vt->carveout_hint = -1;
   vt->init = syn_init;
   vt->run_next_step = syn_step;
   vt->stop = syn_stop;

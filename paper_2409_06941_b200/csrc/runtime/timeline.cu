@@ -107,17 +107,20 @@ __global__ void fill_bf16_kernel(__nv_bfloat16* p, std::size_t n, std::uint64_t 
 // lands with the default (L1-heavy) carveout would lock the side task's
 // smem-hungry CTAs out of that SM for the bubble; ask for the max-shared
 // configuration so side-task CTAs can co-reside with it.
+void set_wait_kernel_carveout(int percent) {
+  static int current = -2;
+  if (percent == current) return;
+  for (const void* fn : {reinterpret_cast<const void*>(gap_kernel), reinterpret_cast<const void*>(stamp_kernel),
+                         reinterpret_cast<const void*>(link_wait_kernel),
+                         reinterpret_cast<const void*>(link_signal_kernel)})
+    cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, percent);
+  current = percent;
+}
+
 void configure_timeline_kernels() {
   static bool done = false;
   if (done) return;
-  cudaFuncSetAttribute(gap_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                       cudaSharedmemCarveoutMaxShared);
-  cudaFuncSetAttribute(stamp_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                       cudaSharedmemCarveoutMaxShared);
-  cudaFuncSetAttribute(link_wait_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                       cudaSharedmemCarveoutMaxShared);
-  cudaFuncSetAttribute(link_signal_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                       cudaSharedmemCarveoutMaxShared);
+  set_wait_kernel_carveout(cudaSharedmemCarveoutMaxShared);
   done = true;
 }
 

@@ -72,6 +72,8 @@ void launch_link_wait(const LinkWaitArgs& a, cudaStream_t s);
 void launch_link_signal(std::uint32_t* flag, std::uint32_t v, cudaStream_t s);
 
 void configure_timeline_kernels();
+// preferred L1/shared split (percent) of the gap / link / stamp kernels
+void set_wait_kernel_carveout(int percent);
 void launch_gap(const GapArgs& a, cudaStream_t s);
 // Writes %globaltimer to *host_mapped and publishes it through *flag.
 void launch_stamp(std::uint64_t* host_mapped, volatile std::uint32_t* flag, std::uint32_t val,

@@ -378,6 +378,7 @@ class PythonTask:
 
     work_units_per_step = 0.0
     memory_gib = 0.0
+    carveout_hint = -1  # L1/shared split the task's kernels want (-1: none, 0: max L1)
 
     def create(self): pass
     def init(self, stream: int): pass
@@ -419,6 +420,7 @@ class PythonTask:
             ty["destroy"](lambda u: None),
         ]
         self.vt = A.SideTaskVTableC(*self._cbs, float(self.work_units_per_step))
+        self.vt.carveout_hint = int(self.carveout_hint)
         self.user = C.c_void_p(0)
         self.units_per_step = float(self.work_units_per_step)
         self.error = None
