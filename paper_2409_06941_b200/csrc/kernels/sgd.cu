@@ -26,8 +26,7 @@
 namespace {
 
 constexpr int kSgdThreads = 256;
-constexpr int kSgdDefaultMinBlocks = 1;
-constexpr int kSgdDefaultEpi = 2;  // edges per lane group per iteration
+constexpr int kSgdEpi = 2;  // edges per lane group per iteration (4 was measured slower: register-capped occupancy)
 constexpr int kSgdConflictDiv = 8;  // in-flight edges <= V / 8
 constexpr uint64_t kSgdPermMul = 2654435761ull;
 
@@ -96,14 +95,15 @@ __device__ __forceinline__ void apply(float4* p, const float4& d) { atomicAdd(p,
 // Each lane group handles edges g, g + G, g + 2G, ..., EPI of them per
 // iteration (EPI x 2 latent-row loads in flight per lane), and the next
 // iteration's (u, v, r) load while this iteration's rows are in flight.
-// MINB: CTAs per SM the register allocation must allow (occupancy vs ILP).
-// Register cap: four 256-thread CTAs per SM with <= 60 registers leave room
-// for a resident 1-warp kernel (the stage's dependency wait in a bubble);
-// at 64 registers the fourth CTA of that SM could not launch and ran its
-// static share as a tail (in-bubble steps 34 % slower than alone).
-template <int K, int MINB, int EPI>
-__global__ void __launch_bounds__(kSgdThreads)
-    __maxnreg__(EPI >= 4 ? (MINB >= 4 ? 64 : 128) : (MINB >= 6 ? 40 : 56)) sgd_step_kernel(
+// Register cap (SGD_MAXNREG): registers are allocated in units of 8 per
+// thread, so four 256-thread CTAs at 64 fill the register file and leave no
+// room for the stage's resident 1-warp dependency-wait kernel inside a
+// bubble; at 56 they do.
+#ifndef SGD_MAXNREG
+#define SGD_MAXNREG 56
+#endif
+template <int K, int EPI = kSgdEpi>
+__global__ void __launch_bounds__(kSgdThreads) __maxnreg__(K >= 16 ? SGD_MAXNREG : 64) sgd_step_kernel(
     const int32_t* __restrict__ us, const int32_t* __restrict__ vs, const float* __restrict__ rs,
     float* __restrict__ L, int64_t e0, int64_t e1, float eta, float lam) {
   constexpr int LN = Row<K>::kLanes;
@@ -217,18 +217,18 @@ struct fr_sgd_problem {
 
 namespace {
 
-template <int K, int MINB, int EPI>
-void launch_step_v(fr_sgd_problem* p, int64_t a, int64_t b, float eta, float lam, cudaStream_t s) {
+template <int K>
+void launch_step(fr_sgd_problem* p, int64_t a, int64_t b, float eta, float lam, cudaStream_t s) {
   // persistent-style grid: exactly the resident CTAs (no second partial wave)
   static const int per_sm = [] {
     // The random latent-row loads land in L1: with the max-shared carveout
     // the pipeline's GEMMs leave behind (28 KB of L1) the loads in flight per
     // SM are capped and a step is ~45 % slower.  Ask for the max-L1 split so
     // the SMs are reconfigured when the step's CTAs arrive.
-    cudaFuncSetAttribute(sgd_step_kernel<K, MINB, EPI>, cudaFuncAttributePreferredSharedMemoryCarveout,
+    cudaFuncSetAttribute(sgd_step_kernel<K>, cudaFuncAttributePreferredSharedMemoryCarveout,
                          cudaSharedmemCarveoutMaxL1);
     int n = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sgd_step_kernel<K, MINB, EPI>, kSgdThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sgd_step_kernel<K>, kSgdThreads, 0);
     return std::max(1, n);
   }();
   // Conflict-sparse Hogwild: at most V / kSgdConflictDiv edges in flight, so
@@ -238,30 +238,11 @@ void launch_step_v(fr_sgd_problem* p, int64_t a, int64_t b, float eta, float lam
     const char* e = std::getenv("FR_SGD_CONFLICT_DIV");  // tuning hook
     return e ? std::max(1, std::atoi(e)) : kSgdConflictDiv;
   }();
-  const int64_t groups = (b - a + EPI - 1) / EPI;
-  const int64_t cap_groups = std::max<int64_t>(1, int64_t(p->V) / div / EPI);
+  const int64_t groups = (b - a + kSgdEpi - 1) / kSgdEpi;
+  const int64_t cap_groups = std::max<int64_t>(1, int64_t(p->V) / div / kSgdEpi);
   const int64_t want = (std::min(groups, cap_groups) * Row<K>::kLanes + kSgdThreads - 1) / kSgdThreads;
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(p->sms) * per_sm)));
-  sgd_step_kernel<K, MINB, EPI><<<grid, kSgdThreads, 0, s>>>(p->u, p->v, p->r, p->L, a, b, eta, lam);
-}
-
-template <int K>
-void launch_step(fr_sgd_problem* p, int64_t a, int64_t b, float eta, float lam, cudaStream_t s) {
-  static const int minb = [] {
-    const char* e = std::getenv("FR_SGD_MINB");  // tuning hooks
-    return e ? std::atoi(e) : kSgdDefaultMinBlocks;
-  }();
-  static const int epi = [] {
-    const char* e = std::getenv("FR_SGD_EPI");
-    return e ? std::atoi(e) : kSgdDefaultEpi;
-  }();
-  if (epi >= 4) {
-    if (minb >= 4) launch_step_v<K, 4, 4>(p, a, b, eta, lam, s);
-    else launch_step_v<K, 1, 4>(p, a, b, eta, lam, s);
-  } else {
-    if (minb >= 6) launch_step_v<K, 6, 2>(p, a, b, eta, lam, s);
-    else launch_step_v<K, 1, 2>(p, a, b, eta, lam, s);
-  }
+  sgd_step_kernel<K><<<grid, kSgdThreads, 0, s>>>(p->u, p->v, p->r, p->L, a, b, eta, lam);
 }
 
 template <int K>
