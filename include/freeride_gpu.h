@@ -107,6 +107,8 @@ int fr_pr_state_destroy(fr_pr_state* st);
 int fr_pr_reset(fr_pr_state* st, void* stream);
 /* `iters` pull iterations: r' = (1-d)/V + d * A_in^T c ; c' = r' * inv_outdeg */
 int fr_pr_step(fr_pr_state* st, int32_t iters, float damping, void* stream);
+/* ranks in original vertex ids (device pointer, V floats).  A readout point:
+ * synchronises the device, then permutes the step's row-order ranks. */
 int fr_pr_ranks(const fr_pr_state* st, const float** r, int64_t* iterations);
 
 /* ------------------------------------------- K3/K4: Graph-SGD (rank k MF) */

@@ -201,7 +201,7 @@ struct PrArgs {
   const int32_t* col;    // column ids
   const float* rinv;     // per row: 1 / out-degree (0 if dangling)
   const int32_t* rowc;   // per row: column id (c' store)
-  const int32_t* rowr;   // per row: original id (r' store)
+  // r is written in row order (coalesced); fr_pr_ranks permutes it back
   const int4* chunks;    // {row, e_begin, e_end, slot | chunks of the row << 8}, grouped by CTA
   const float* c_in;
   float* r_out;
@@ -255,7 +255,7 @@ __device__ __forceinline__ Item prep(const PrArgs& a, int it, bool valid, int la
     x.e = __ldg(&a.off[row]) + sub;
     x.e1 = __ldg(&a.off[row + 1]);
     if (sub == 0) {
-      x.rr = __ldg(&a.rowr[row]);
+      x.rr = row;
       x.rc = __ldg(&a.rowc[row]);
       x.inv = __ldg(&a.rinv[row]);
     }
@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(kPrThreads, MINB) pr_pull_kernel(PrArgs a) {
       if (atomicAdd(&scnt[slot], 1) + 1 == need) {
         __threadfence_block();
         const double tot = *static_cast<volatile double*>(&sacc[slot]);
-        store(a, __ldg(&a.rowr[ch.x]), __ldg(&a.rowc[ch.x]), __ldg(&a.rinv[ch.x]), tot);
+        store(a, ch.x, __ldg(&a.rowc[ch.x]), __ldg(&a.rinv[ch.x]), tot);
       }
     }
   }
@@ -340,8 +340,15 @@ __global__ void __launch_bounds__(kPrThreads, MINB) pr_pull_kernel(PrArgs a) {
   }
   if (a.do_tail) {
     for (int32_t i = a.bstart[0] + blockIdx.x * kPrThreads + tid; i < a.V; i += gridDim.x * kPrThreads)
-      store(a, __ldg(&a.rowr[i]), __ldg(&a.rowc[i]), __ldg(&a.rinv[i]), 0.0);
+      store(a, i, __ldg(&a.rowc[i]), __ldg(&a.rinv[i]), 0.0);
   }
+}
+
+// r is kept in row order by the step; readout permutes it to original ids
+__global__ void pr_unpermute_kernel(const float* __restrict__ r_row, const int32_t* __restrict__ rowr,
+                                    int32_t V, float* __restrict__ r_orig) {
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < V; i += gridDim.x * blockDim.x)
+    r_orig[rowr[i]] = r_row[i];
 }
 
 int grid_for(int64_t work, int threads, int per_sm) {
@@ -394,7 +401,8 @@ struct fr_pr_graph {
 
 struct fr_pr_state {
   const fr_pr_graph* g = nullptr;
-  float* r = nullptr;
+  float* r = nullptr;       // row order (written by the step)
+  float* r_orig = nullptr;  // original vertex order (filled by readout)
   float* c[2] = {nullptr, nullptr};
   int cur = 0;
   int64_t iterations = 0;
@@ -403,6 +411,17 @@ struct fr_pr_state {
 };
 
 namespace {
+
+// Readout (a synchronisation point by contract): wait for the steps, then
+// permute the row-order ranks to original vertex ids.
+int pr_readout(const fr_pr_state* st) {
+  FR_CUDA_TRY(cudaDeviceSynchronize());
+  const fr_pr_graph* g = st->g;
+  pr_unpermute_kernel<<<grid_for(g->V, 256, 8), 256>>>(st->r, g->rowr, g->V, st->r_orig);
+  FR_CUDA_TRY(cudaGetLastError());
+  FR_CUDA_TRY(cudaDeviceSynchronize());
+  return FR_OK;
+}
 
 void free_graph(fr_pr_graph* g) {
   for (void* p : {static_cast<void*>(g->offsets), static_cast<void*>(g->col),
@@ -643,10 +662,11 @@ int fr_pr_state_create(const fr_pr_graph* g, fr_pr_state** out) {
   st->g = g;
   const size_t b = sizeof(float) * static_cast<size_t>(std::max(4, g->V));
   cudaError_t e = cudaMalloc(&st->r, b);
+  if (e == cudaSuccess) e = cudaMalloc(&st->r_orig, b);
   if (e == cudaSuccess) e = cudaMalloc(&st->c[0], b);
   if (e == cudaSuccess) e = cudaMalloc(&st->c[1], b);
   if (e != cudaSuccess) {
-    for (void* p : {static_cast<void*>(st->r), static_cast<void*>(st->c[0]),
+    for (void* p : {static_cast<void*>(st->r), static_cast<void*>(st->r_orig), static_cast<void*>(st->c[0]),
                     static_cast<void*>(st->c[1])})
       if (p) cudaFree(p);
     delete st;
@@ -658,7 +678,7 @@ int fr_pr_state_create(const fr_pr_graph* g, fr_pr_state** out) {
 
 int fr_pr_state_destroy(fr_pr_state* st) {
   if (!st) return FR_OK;
-  for (void* p : {static_cast<void*>(st->r), static_cast<void*>(st->c[0]),
+  for (void* p : {static_cast<void*>(st->r), static_cast<void*>(st->r_orig), static_cast<void*>(st->c[0]),
                   static_cast<void*>(st->c[1])})
     if (p) cudaFree(p);
   delete st;
@@ -689,7 +709,6 @@ int fr_pr_step(fr_pr_state* st, int32_t iters, float damping, void* stream) {
   a.col = g->xcol;
   a.rinv = g->rinv;
   a.rowc = g->rowc;
-  a.rowr = g->rowr;
   a.chunks = g->chunks;
   a.r_out = st->r;
   std::memcpy(a.cta_chunk, g->cta_chunk, sizeof(a.cta_chunk));
@@ -727,7 +746,11 @@ int fr_pr_step(fr_pr_state* st, int32_t iters, float damping, void* stream) {
 
 int fr_pr_ranks(const fr_pr_state* st, const float** r, int64_t* iterations) {
   if (!st) return frcapi::fail(FR_ERR_ARGUMENT, "null state");
-  if (r) *r = st->r;
+  if (r) {
+    const int rc = pr_readout(st);
+    if (rc != FR_OK) return rc;
+    *r = st->r_orig;
+  }
   if (iterations) *iterations = st->iterations;
   return FR_OK;
 }
@@ -812,7 +835,7 @@ int pr_task_init(void* u, void* stream) {
   FR_CUDA_TRY(up(reinterpret_cast<void**>(&g.chunks), t->h_chunks, size_t(g.n_chunk) * sizeof(int4)));
   t->st = fr_pr_state{};
   t->st.g = &g;
-  for (float** p : {&t->st.r, &t->st.c[0], &t->st.c[1]})
+  for (float** p : {&t->st.r, &t->st.r_orig, &t->st.c[0], &t->st.c[1]})
     FR_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(p), std::max<size_t>(V, 4) * 4, s));
   t->on_gpu = true;
   return fr_pr_reset(&t->st, s);
@@ -830,7 +853,7 @@ int pr_task_stop(void* u) {
   for (void* p : {static_cast<void*>(t->g.xoff), static_cast<void*>(t->g.xcol),
                   static_cast<void*>(t->g.rowc), static_cast<void*>(t->g.rowr),
                   static_cast<void*>(t->g.rinv), static_cast<void*>(t->g.chunks),
-                  static_cast<void*>(t->st.r), static_cast<void*>(t->st.c[0]),
+                  static_cast<void*>(t->st.r), static_cast<void*>(t->st.r_orig), static_cast<void*>(t->st.c[0]),
                   static_cast<void*>(t->st.c[1])})
     if (p) FR_CUDA_TRY(cudaFreeAsync(p, t->last));
   t->g = fr_pr_graph{};
@@ -891,11 +914,18 @@ int fr_pagerank_task_info(void* user, int32_t* V, int64_t* E, double* memory_gib
   const fr_pr_graph& g = t->shape;
   if (V) *V = g.V;
   if (E) *E = g.E;
-  // xoff + xcol + rowc/rowr/rinv + r + 2 c + chunk list
+  // xoff + xcol + rowc/rowr/rinv + r (row and original order) + 2 c + chunk list
   if (memory_gib)
-    *memory_gib = (4.0 * (g.V + 1) + 4.0 * g.E + 4.0 * g.V * 6 + 16.0 * g.n_chunk) /
+    *memory_gib = (4.0 * (g.V + 1) + 4.0 * g.E + 4.0 * g.V * 7 + 16.0 * g.n_chunk) /
                   (1024.0 * 1024.0 * 1024.0);
-  if (ranks) *ranks = t->on_gpu ? t->st.r : nullptr;
+  if (ranks) {
+    *ranks = nullptr;
+    if (t->on_gpu) {
+      const int rc = pr_readout(&t->st);
+      if (rc != FR_OK) return rc;
+      *ranks = t->st.r_orig;
+    }
+  }
   if (iterations) *iterations = t->st.iterations;
   return FR_OK;
 }
