@@ -169,11 +169,12 @@ def cpu_pagerank(seconds, csr):
 def cpu_sgd(seconds, edges=1 << 24):
     o = _oracle()
     u, v, r = o.sgd_edges(SGD["V"], edges, seed=SGD["edge_seed"])
+    u, v, r = o.sgd_group_by_user(SGD["V"], u, v, r, window=SGD["edges_per_step"])   # the GPU task's layout
     L = o.sgd_init(SGD["V"], SGD["k"], seed=SGD["init_seed"])
     reps, el = _timed(lambda: o.sgd_epoch(u, v, r, L, 0.01, 0.05, nthreads=0), seconds)
     return {"value": reps * edges / el, "unit": "edges/s", "cores": os.cpu_count(), "kind": "port",
-            "seconds": el, "sample": f"{reps} passes over {edges} Orkut-shaped edges (V={SGD['V']}, k=16), "
-                                     f"Hogwild OpenMP on {os.cpu_count()} host threads"}
+            "seconds": el, "sample": f"{reps} passes over {edges} Orkut-shaped edges (V={SGD['V']}, k=16, "
+                                     f"by-user layout), Hogwild OpenMP on {os.cpu_count()} host threads"}
 
 
 # ---------------------------------------------------------------- harvest
@@ -401,9 +402,11 @@ def emit(args, results, ws, names, csr):
                      "roofline": roof("pagerank", "pr_pull_kernel (2 launches of 1 iteration per step, in-pipeline); "
                                       "working set L2-resident: latency-bound gathers, not HBM"),
                      "cpu_baseline": cpu_pagerank(args.cpu_seconds / 2, csr) if csr is not None else None},
-        "sgd": {"config": "configs[2]: Orkut shape V=3,072,441 E=117,185,083 k=16, 2^21 edges/step",
+        "sgd": {"config": "configs[2]: Orkut shape V=3,072,441 E=117,185,083 k=16, 2^21 edges/step, "
+                          "by-user layout (fr_sgd_group_by_user)",
                 "value": rate("sgd"), "unit": "edges/bubble-s", "dT": dT("sgd"), "fill": fill("sgd"),
-                "roofline": roof("sgd", "sgd_step_kernel<16> (2^21 edges/launch, in-pipeline)"),
+                "roofline": roof("sgd", "sgd_user_kernel<16> (2^21 edges/launch, in-pipeline; "
+                                        "alg bytes 12 + 128 per edge + 128 per L_u load)"),
                 "cpu_baseline": cpu_sgd(args.cpu_seconds / 2) if not args.no_cpu else None},
     }
     imp = results[0]["image_imperative"]

@@ -124,6 +124,15 @@ int fr_sgd_reinit(fr_sgd_problem* p, uint64_t init_seed, void* stream);
 /* one step: edges [e_begin, e_end) */
 int fr_sgd_step(fr_sgd_problem* p, int64_t e_begin, int64_t e_end, float eta, float lambda,
                 void* stream);
+/* Re-lays the edges out by user (Gardenia's CSR input order: ratings of one
+ * user contiguous, generated order within a user), each user's ratings cut
+ * into 64-edge pieces dealt over R = ceil(E / window_edges) rounds (piece k
+ * of np -> round (k R / np + h(u)) mod R, then stable by round), so one
+ * window-sized step holds at most ~one piece of any user.  Later steps run the
+ * user-grouped kernel (L_u held in registers across a run, ~143 instead of
+ * 268 B/edge at k = 16; k < 16 keeps the per-edge kernel).  Synchronous;
+ * E < 2^31.  oracle/sidetasks.c orc_sgd_group_by_user is the same layout. */
+int fr_sgd_group_by_user(fr_sgd_problem* p, int64_t window_edges, void* stream);
 /* K4: *d_acc (device fp64) += sum of squared errors over [e_begin, e_end) */
 int fr_sgd_sqerr(const fr_sgd_problem* p, int64_t e_begin, int64_t e_end, double* d_acc,
                  void* stream);
@@ -241,7 +250,10 @@ typedef struct fr_sgd_task_config {
   float eta;              /* 0.01 */
   float lambda;           /* 0.05 */
   int64_t total_steps;    /* <= 0: unbounded */
+  int32_t layout;         /* FR_SGD_LAYOUT_COO (generated order) or FR_SGD_LAYOUT_BY_USER */
 } fr_sgd_task_config;
+#define FR_SGD_LAYOUT_COO 0
+#define FR_SGD_LAYOUT_BY_USER 1
 /* generates the rating graph on the device immediately (setup) */
 int fr_sgd_task_create(const fr_sgd_task_config* cfg, fr_side_task_vtable* vt, void** user);
 int fr_sgd_task_problem(void* user, fr_sgd_problem** p, int64_t* epochs_done);

@@ -190,6 +190,64 @@ void orc_sgd_edges(int32_t V, int64_t E, uint64_t seed, int32_t* u, int32_t* v, 
   }
 }
 
+/* fr_sgd_group_by_user's layout (paper_2409_06941_b200/csrc/kernels/sgd.cu):
+ * Gardenia's CSR input order -- a stable counting sort by u -- then each
+ * user's run cut into 64-edge pieces, piece k of np going to round
+ * (k R / np + h(u)) mod R with R = ceil(E / window), and a stable counting
+ * sort by round. */
+#define SGD_PIECE 64
+static int32_t sgd_round(int32_t u, int64_t rank, int64_t deg, int32_t R) {
+  const int64_t np = (deg + SGD_PIECE - 1) / SGD_PIECE, k = rank / SGD_PIECE;
+  const uint64_t h = orc_splitmix64(0x5347445250ull ^ (uint64_t)u) % (uint64_t)R;
+  return (int32_t)(((uint64_t)(k * R / np) + h) % (uint64_t)R);
+}
+
+static void sgd_counting_sort(int64_t E, const int32_t* key, int64_t nkeys, const int32_t* u,
+                              const int32_t* v, const float* r, int32_t* u2, int32_t* v2, float* r2,
+                              int64_t* start /* nkeys + 1, zeroed */) {
+  for (int64_t e = 0; e < E; ++e) start[key[e] + 1]++;
+  for (int64_t i = 0; i < nkeys; ++i) start[i + 1] += start[i];
+  for (int64_t e = 0; e < E; ++e) {
+    const int64_t at = start[key[e]]++;
+    u2[at] = u[e];
+    v2[at] = v[e];
+    r2[at] = r[e];
+  }
+}
+
+void orc_sgd_group_by_user(int32_t V, int64_t E, int64_t window, int32_t* u, int32_t* v, float* r) {
+  const size_t n = (size_t)(E > 0 ? E : 1);
+  int64_t R = window > 0 ? (E + window - 1) / window : 1;
+  if (R < 1) R = 1;
+  if (R > (1 << 20)) R = 1 << 20;
+  int64_t* start = (int64_t*)calloc((size_t)V + 1, sizeof(int64_t));
+  int32_t* u2 = (int32_t*)malloc(n * sizeof(int32_t));
+  int32_t* v2 = (int32_t*)malloc(n * sizeof(int32_t));
+  float* r2 = (float*)malloc(n * sizeof(float));
+  sgd_counting_sort(E, u, V, u, v, r, u2, v2, r2, start);
+  if (R > 1) {
+    /* start[x] now = end of x's run; deg from the run bounds */
+    int32_t* key = (int32_t*)malloc(n * sizeof(int32_t));
+    for (int64_t e = 0; e < E; ++e) {
+      const int32_t x = u2[e];
+      const int64_t b = x ? start[x - 1] : 0, deg = start[x] - b;
+      key[e] = sgd_round(x, e - b, deg, (int32_t)R);
+    }
+    int64_t* rs = (int64_t*)calloc((size_t)R + 1, sizeof(int64_t));
+    sgd_counting_sort(E, key, R, u2, v2, r2, u, v, r, rs);
+    free(rs);
+    free(key);
+  } else {
+    memcpy(u, u2, (size_t)E * sizeof(int32_t));
+    memcpy(v, v2, (size_t)E * sizeof(int32_t));
+    memcpy(r, r2, (size_t)E * sizeof(float));
+  }
+  free(start);
+  free(u2);
+  free(v2);
+  free(r2);
+}
+
 void orc_sgd_init(int32_t V, int k, uint64_t seed, float* L, int nthreads) {
   const float scale = (float)(1.0 / sqrt((double)k)) * (1.0f / 16777216.0f);
 #pragma omp parallel for num_threads(nth(nthreads)) schedule(static)

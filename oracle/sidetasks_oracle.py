@@ -32,6 +32,7 @@ class SideTaskOracle:
         lib.orc_rmat_edges.argtypes = [C.c_int, C.c_int64, C.c_uint64, i32p, i32p, C.c_int]
         lib.orc_pr_run.argtypes = [C.c_int32, i32p, i32p, i32p, C.c_double, C.c_int, f64p, C.c_int]
         lib.orc_sgd_edges.argtypes = [C.c_int32, C.c_int64, C.c_uint64, i32p, i32p, f32p, C.c_int]
+        lib.orc_sgd_group_by_user.argtypes = [C.c_int32, C.c_int64, C.c_int64, i32p, i32p, f32p]
         lib.orc_sgd_init.argtypes = [C.c_int32, C.c_int, C.c_uint64, f32p, C.c_int]
         lib.orc_sgd_epoch.argtypes = [C.c_int64, i32p, i32p, f32p, f32p, C.c_int, C.c_float, C.c_float, C.c_int]
         lib.orc_sgd_rmse.restype = C.c_double
@@ -92,6 +93,12 @@ class SideTaskOracle:
     def sgd_edges(self, V, E, seed=2, nthreads=0):
         u, v, r = np.empty(E, np.int32), np.empty(E, np.int32), np.empty(E, np.float32)
         self.lib.orc_sgd_edges(V, E, seed, u, v, r, nthreads)
+        return u, v, r
+
+    def sgd_group_by_user(self, V, u, v, r, window=1 << 21):
+        """fr_sgd_group_by_user's layout, in place: stable by u, each user's run
+        cut into 64-edge pieces dealt over ceil(E / window) rounds"""
+        self.lib.orc_sgd_group_by_user(V, len(u), window, u, v, r)
         return u, v, r
 
     def sgd_init(self, V, k=16, seed=3, nthreads=0):

@@ -510,14 +510,17 @@ GPU_PROTOTYPES.update({
 class SgdTaskConfigC(Struct):
     _fields_ = [("V", i32), ("k", i32), ("E", i64), ("edge_seed", u64), ("init_seed", u64),
                 ("edges_per_step", i64), ("eta", C.c_float), ("lambda_", C.c_float),
-                ("total_steps", i64)]
+                ("total_steps", i64), ("layout", i32)]
 
+
+SGD_LAYOUT_COO, SGD_LAYOUT_BY_USER = 0, 1
 
 GPU_PROTOTYPES.update({
     "fr_sgd_problem_generate": (C.c_int, [i32, i64, i32, u64, u64, vp, P(vp)]),
     "fr_sgd_problem_destroy": (C.c_int, [vp]),
     "fr_sgd_reinit": (C.c_int, [vp, u64, vp]),
     "fr_sgd_step": (C.c_int, [vp, i64, i64, C.c_float, C.c_float, vp]),
+    "fr_sgd_group_by_user": (C.c_int, [vp, i64, vp]),
     "fr_sgd_sqerr": (C.c_int, [vp, i64, i64, vp, vp]),
     "fr_sgd_rmse": (C.c_int, [vp, vp, P(dbl)]),
     "fr_sgd_buffers": (C.c_int, [vp, P(vp), P(vp), P(vp), P(vp), P(i32), P(i64), P(i32)]),

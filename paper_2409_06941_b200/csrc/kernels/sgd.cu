@@ -16,6 +16,20 @@
 // step streams 12 B of edge + 4 x 64 B of random rows per edge from HBM:
 // 268 B/edge algorithmic.  Each lane carries two edges per iteration to keep
 // enough 64 B requests in flight.
+//
+// User-grouped layout (fr_sgd_group_by_user): the edges stable-sorted by u,
+// i.e. Gardenia's CSR input order (one row of ratings per user), with every
+// user's row cut into 64-edge pieces dealt over rounds of about one step's
+// edges (so a hub's thousands of ratings are never all in flight at once:
+// at most ~one piece of a user per round).  Each lane group then walks a
+// contiguous segment, keeps L_u of the current run of
+// equal u in registers (updated edge by edge, exactly the sequential order
+// within the run) and adds L_u's net change back with one vector atomic when
+// the run (or the segment) ends; only L_v is read and atomically updated per
+// edge.  148 B/edge instead of 268 (12 B of edge + 2 x 64 B of L_v + the L_u
+// read/update once per run).
+#include <cub/cub.cuh>
+
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -29,6 +43,17 @@ constexpr int kSgdThreads = 256;
 constexpr int kSgdEpi = 2;  // edges per lane group per iteration (4 was measured slower: register-capped occupancy)
 constexpr int kSgdConflictDiv = 8;  // in-flight edges <= V / 8
 constexpr uint64_t kSgdPermMul = 2654435761ull;
+// by-user step: L_u is handed back and re-read at least every kSgdRefresh
+// edges of a run.  Two groups holding the same hub row (pieces of it in one
+// step) would otherwise each walk it through a long run and add both full
+// moves -- an overshoot that diverges once the factors grow (measured: NaN
+// after ~40 epochs with whole-run holds); refreshing bounds it to a
+// mini-batch of a few x kSgdRefresh edges, like the per-edge kernel's
+// (16: 88.6 us per 2^21-edge step at the Orkut shape; 8: 94.7; whole runs: 82.4).
+#ifndef SGD_REFRESH
+#define SGD_REFRESH 16
+#endif
+constexpr int kSgdRefresh = SGD_REFRESH;
 
 __device__ __forceinline__ int32_t sgd_vertex(uint64_t h, int32_t V) {
   const double x = static_cast<double>(h >> 11) * (1.0 / 9007199254740992.0);
@@ -158,6 +183,138 @@ __global__ void __launch_bounds__(kSgdThreads) __maxnreg__(K >= 16 ? SGD_MAXNREG
   }
 }
 
+// User-grouped step (K >= 16: lane sub of a group fetches the metadata of
+// edge c + (sub % D) of each D-edge chunk and the group shares it through
+// shuffles).  Group g owns edges [e0 + g seg, e0 + (g + 1) seg); slot j of the
+// D-slot ring holds the L_v row of the chunk's j-th edge, re-issued for the
+// next chunk as soon as it is consumed (D rows in flight per group); the
+// metadata runs two chunks ahead of the rows.  A run start (u differs from
+// the previous edge) flushes the held L_u delta and loads the new row (a
+// dependent load, ~1.7 per segment at the Orkut shape).
+template <int K, int D = 4>
+__global__ void __maxnreg__(SGD_MAXNREG) sgd_user_kernel(
+    const int32_t* __restrict__ us, const int32_t* __restrict__ vs, const float* __restrict__ rs,
+    float* __restrict__ L, int64_t e0, int64_t e1, int64_t seg, float eta, float lam) {
+  constexpr int LN = Row<K>::kLanes;
+  static_assert(LN >= D, "grouped step needs K / 4 >= D lanes per group");
+  const int lane = threadIdx.x & 31, sub = lane % LN, base = lane - sub;
+  const int64_t group = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / LN;
+  if (e0 + (group - lane / LN) * seg >= e1) return;  // whole warp past the end (warp-uniform)
+  float4* L4 = reinterpret_cast<float4*>(L);
+  const int64_t s0 = e0 + group * seg, s1 = std::min<int64_t>(e1, s0 + seg);
+  // metadata of edge c + (sub % D): (u, v, r) for chunks c, c + D, c + 2D
+  auto meta = [&](int64_t c, int32_t& mu, int32_t& mv, float& mr) {
+    const int64_t e = c + (sub % D);
+    const bool ok = e < s1;
+    mu = ok ? __ldg(&us[e]) : -1;
+    mv = ok ? __ldg(&vs[e]) : 0;
+    mr = ok ? __ldg(&rs[e]) : 0.0f;
+  };
+  int32_t mu0, mv0, mu1, mv1, mu2, mv2;
+  float mr0, mr1, mr2;
+  meta(s0, mu0, mv0, mr0);
+  meta(s0 + D, mu1, mv1, mr1);
+  float4 b[D];
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    const int32_t v = __shfl_sync(0xffffffffu, mv0, base + j);
+    b[j] = s0 + j < s1 ? L4[static_cast<int64_t>(v) * LN + sub] : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  float4 a = make_float4(0.f, 0.f, 0.f, 0.f), a0 = a;
+  int32_t cu = -1, held = 0;
+  for (int64_t c = s0; c < s0 + seg; c += D) {  // same trip count for every group of the warp
+    meta(c + 2 * D, mu2, mv2, mr2);
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const int32_t u = __shfl_sync(0xffffffffu, mu0, base + j);
+      const int32_t v = __shfl_sync(0xffffffffu, mv0, base + j);
+      const float r = __shfl_sync(0xffffffffu, mr0, base + j);
+      const int32_t nv = __shfl_sync(0xffffffffu, mv1, base + j);
+      const bool ok = u >= 0;
+      if (ok && (u != cu || held >= kSgdRefresh)) {
+        // run start (or kSgdRefresh edges held): hand the held row's change
+        // back and (re)load the row, picking up concurrent updates of it
+        if (cu >= 0)
+          apply(&L4[static_cast<int64_t>(cu) * LN + sub],
+                make_float4(a.x - a0.x, a.y - a0.y, a.z - a0.z, a.w - a0.w));
+        cu = u;
+        a = L4[static_cast<int64_t>(u) * LN + sub];
+        a0 = a;
+        held = 0;
+      }
+      const float4 bj = b[j];
+      const float err = r - group_sum<K>(dot4(a, bj));
+      if (ok) {
+        float4 da, db;
+        deltas(a, bj, err, eta, lam, da, db);
+        a.x += da.x; a.y += da.y; a.z += da.z; a.w += da.w;
+        ++held;
+        apply(&L4[static_cast<int64_t>(v) * LN + sub], db);
+      }
+      b[j] = c + D + j < s1 ? L4[static_cast<int64_t>(nv) * LN + sub] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    mu0 = mu1; mv0 = mv1; mr0 = mr1;
+    mu1 = mu2; mv1 = mv2; mr1 = mr2;
+  }
+  if (cu >= 0)
+    apply(&L4[static_cast<int64_t>(cu) * LN + sub], make_float4(a.x - a0.x, a.y - a0.y, a.z - a0.z, a.w - a0.w));
+}
+
+__global__ void sgd_gather_kernel(const int32_t* __restrict__ perm, const int32_t* __restrict__ v,
+                                  const float* __restrict__ r, int64_t E, int32_t* __restrict__ v2,
+                                  float* __restrict__ r2) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < E;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t e = __ldg(&perm[i]);
+    v2[i] = __ldg(&v[e]);
+    r2[i] = __ldg(&r[e]);
+  }
+}
+
+constexpr int64_t kSgdPiece = 64;  // edges per piece of a user's run (by-user layout)
+
+__global__ void sgd_count_kernel(const int32_t* __restrict__ u, int64_t n, int32_t* __restrict__ cnt) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    atomicAdd(&cnt[__ldg(&u[i])], 1);
+}
+
+// round of the edge at sorted position i: piece k of np pieces of its user's
+// run goes to round (k R / np + h(u)) mod R -- distinct rounds while np <= R,
+// users spread over the rounds by a hash (mirrors oracle/sidetasks.c)
+__host__ __device__ __forceinline__ int32_t sgd_round(int32_t u, int64_t rank, int64_t deg, int32_t R) {
+  const int64_t np = (deg + kSgdPiece - 1) / kSgdPiece, k = rank / kSgdPiece;
+  const uint64_t h = frk::splitmix64(0x5347445250ull ^ static_cast<uint64_t>(u)) % static_cast<uint64_t>(R);
+  return static_cast<int32_t>((static_cast<uint64_t>(k * R / np) + h) % static_cast<uint64_t>(R));
+}
+
+__global__ void sgd_round_kernel(const int32_t* __restrict__ u, int64_t n, const int32_t* __restrict__ start,
+                                 const int32_t* __restrict__ cnt, int32_t R, int32_t* __restrict__ key) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t x = __ldg(&u[i]);
+    key[i] = sgd_round(x, i - __ldg(&start[x]), __ldg(&cnt[x]), R);
+  }
+}
+
+__global__ void sgd_gather3_kernel(const int32_t* __restrict__ perm, const int32_t* __restrict__ u,
+                                   const int32_t* __restrict__ v, const float* __restrict__ r, int64_t E,
+                                   int32_t* __restrict__ u2, int32_t* __restrict__ v2, float* __restrict__ r2) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < E;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t e = __ldg(&perm[i]);
+    u2[i] = __ldg(&u[e]);
+    v2[i] = __ldg(&v[e]);
+    r2[i] = __ldg(&r[e]);
+  }
+}
+
+__global__ void sgd_iota_kernel(int32_t* __restrict__ x, int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    x[i] = static_cast<int32_t>(i);
+}
+
 // K4: sum of squared errors over [e0, e1) into *acc (fp64).
 template <int K>
 __global__ void __launch_bounds__(kSgdThreads) sgd_sqerr_kernel(
@@ -213,6 +370,7 @@ struct fr_sgd_problem {
   float* L = nullptr;
   double* acc = nullptr;
   int sms = 148;
+  bool grouped = false;  // edges stable-sorted by u (fr_sgd_group_by_user)
 };
 
 namespace {
@@ -243,6 +401,31 @@ void launch_step(fr_sgd_problem* p, int64_t a, int64_t b, float eta, float lam, 
   const int64_t want = (std::min(groups, cap_groups) * Row<K>::kLanes + kSgdThreads - 1) / kSgdThreads;
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(p->sms) * per_sm)));
   sgd_step_kernel<K><<<grid, kSgdThreads, 0, s>>>(p->u, p->v, p->r, p->L, a, b, eta, lam);
+}
+
+// grouped layout: contiguous segments, D rows in flight per group
+template <int K>
+void launch_user_step(fr_sgd_problem* p, int64_t a, int64_t b, float eta, float lam, cudaStream_t s) {
+  constexpr int D = 4, LN = Row<K>::kLanes;
+  static const int per_sm = [] {
+    cudaFuncSetAttribute(sgd_user_kernel<K, D>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxL1);
+    int n = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sgd_user_kernel<K, D>, kSgdThreads, 0);
+    return std::max(1, n);
+  }();
+  static const int div = [] {
+    const char* e = std::getenv("FR_SGD_CONFLICT_DIV");
+    return e ? std::max(1, std::atoi(e)) : kSgdConflictDiv;
+  }();
+  const int64_t n = b - a;
+  const int64_t cap_groups = std::max<int64_t>(1, int64_t(p->V) / div / D);
+  const int64_t max_groups = int64_t(p->sms) * per_sm * kSgdThreads / LN;
+  const int64_t groups = std::min({(n + D - 1) / D, cap_groups, max_groups});
+  const int64_t seg = ((n + groups - 1) / groups + D - 1) / D * D;
+  const int64_t used = (n + seg - 1) / seg;
+  const int grid = static_cast<int>((used * LN + kSgdThreads - 1) / kSgdThreads);
+  sgd_user_kernel<K, D><<<grid, kSgdThreads, 0, s>>>(p->u, p->v, p->r, p->L, a, b, seg, eta, lam);
 }
 
 template <int K>
@@ -313,6 +496,16 @@ int fr_sgd_step(fr_sgd_problem* p, int64_t e_begin, int64_t e_end, float eta, fl
     return frcapi::fail(FR_ERR_VALIDATION, "edge range outside [0, E]", "edges");
   if (e_begin == e_end) return FR_OK;
   auto s = static_cast<cudaStream_t>(stream);
+  if (p->grouped && p->K >= 16) {
+    switch (p->K) {
+      case 16: launch_user_step<16>(p, e_begin, e_end, eta, lambda, s); break;
+      case 32: launch_user_step<32>(p, e_begin, e_end, eta, lambda, s); break;
+      case 64: launch_user_step<64>(p, e_begin, e_end, eta, lambda, s); break;
+      default: launch_user_step<128>(p, e_begin, e_end, eta, lambda, s); break;
+    }
+    FR_CUDA_LAUNCHED("sgd_user_step");
+    return FR_OK;
+  }
   switch (p->K) {
     case 4: launch_step<4>(p, e_begin, e_end, eta, lambda, s); break;
     case 8: launch_step<8>(p, e_begin, e_end, eta, lambda, s); break;
@@ -322,6 +515,87 @@ int fr_sgd_step(fr_sgd_problem* p, int64_t e_begin, int64_t e_end, float eta, fl
     default: launch_step<128>(p, e_begin, e_end, eta, lambda, s); break;
   }
   FR_CUDA_LAUNCHED("sgd_step");
+  return FR_OK;
+}
+
+int fr_sgd_group_by_user(fr_sgd_problem* p, int64_t window_edges, void* stream) {
+  if (!p) return frcapi::fail(FR_ERR_ARGUMENT, "null problem");
+  if (window_edges < 1) return frcapi::fail(FR_ERR_VALIDATION, "window_edges >= 1", "window_edges");
+  if (p->grouped || p->E == 0) {
+    p->grouped = true;
+    return FR_OK;
+  }
+  if (p->E > INT32_MAX) return frcapi::fail(FR_ERR_VALIDATION, "grouping needs E < 2^31", "E");
+  auto s = static_cast<cudaStream_t>(stream);
+  const int n = static_cast<int>(p->E);
+  const int32_t R = static_cast<int32_t>(std::min<int64_t>((p->E + window_edges - 1) / window_edges, 1 << 20));
+  auto bits_for = [](int64_t x) {
+    int b = 1;
+    while (b < 31 && (int64_t(1) << b) < x) ++b;
+    return b;
+  };
+  int32_t *u2 = nullptr, *v2 = nullptr, *idx = nullptr, *perm = nullptr, *key = nullptr, *key2 = nullptr;
+  int32_t *cnt = nullptr, *start = nullptr;
+  float* r2 = nullptr;
+  void* tmp = nullptr;
+  size_t need = 0, need2 = 0, need3 = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, need, p->u, u2, idx, perm, n, 0, bits_for(p->V), s);
+  cub::DeviceRadixSort::SortPairs(nullptr, need2, key, key2, idx, perm, n, 0, bits_for(R), s);
+  cub::DeviceScan::ExclusiveSum(nullptr, need3, cnt, start, p->V, s);
+  need = std::max({need, need2, need3, size_t(1)});
+  cudaError_t e = cudaSuccess;
+  for (auto [q, bytes] : {std::pair<void**, size_t>{reinterpret_cast<void**>(&u2), size_t(n) * 4},
+                          {reinterpret_cast<void**>(&v2), size_t(n) * 4},
+                          {reinterpret_cast<void**>(&r2), size_t(n) * 4},
+                          {reinterpret_cast<void**>(&idx), size_t(n) * 4},
+                          {reinterpret_cast<void**>(&perm), size_t(n) * 4},
+                          {reinterpret_cast<void**>(&key), size_t(n) * 4},
+                          {reinterpret_cast<void**>(&key2), size_t(n) * 4},
+                          {reinterpret_cast<void**>(&cnt), size_t(p->V) * 4},
+                          {reinterpret_cast<void**>(&start), size_t(p->V) * 4},
+                          {&tmp, need}})
+    if (e == cudaSuccess) e = cudaMalloc(q, bytes);
+  const int gn = grid_for(n, 256, 16);
+  auto swap3 = [&] {  // (u2, v2, r2) -> the problem's arrays
+    std::swap(p->u, u2);
+    std::swap(p->v, v2);
+    std::swap(p->r, r2);
+  };
+  // 1. stable sort by u (LSD radix keeps the generated order within a user)
+  if (e == cudaSuccess) {
+    sgd_iota_kernel<<<gn, 256, 0, s>>>(idx, n);
+    e = cub::DeviceRadixSort::SortPairs(tmp, need, p->u, u2, idx, perm, n, 0, bits_for(p->V), s);
+  }
+  if (e == cudaSuccess) {
+    sgd_gather_kernel<<<gn, 256, 0, s>>>(perm, p->v, p->r, n, v2, r2);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) swap3();
+  // 2. rounds: each user's run cut into kSgdPiece-edge pieces spread over R
+  //    rounds of ~window_edges (stable sort by round keeps u order inside)
+  if (e == cudaSuccess && R > 1) {
+    e = cudaMemsetAsync(cnt, 0, size_t(p->V) * 4, s);
+    if (e == cudaSuccess) {
+      sgd_count_kernel<<<gn, 256, 0, s>>>(p->u, n, cnt);
+      e = cub::DeviceScan::ExclusiveSum(tmp, need, cnt, start, p->V, s);
+    }
+    if (e == cudaSuccess) {
+      sgd_round_kernel<<<gn, 256, 0, s>>>(p->u, n, start, cnt, R, key);
+      e = cub::DeviceRadixSort::SortPairs(tmp, need, key, key2, idx, perm, n, 0, bits_for(R), s);
+    }
+    if (e == cudaSuccess) {
+      sgd_gather3_kernel<<<gn, 256, 0, s>>>(perm, p->u, p->v, p->r, n, u2, v2, r2);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) swap3();
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  for (void* q : {static_cast<void*>(u2), static_cast<void*>(v2), static_cast<void*>(r2),
+                  static_cast<void*>(idx), static_cast<void*>(perm), static_cast<void*>(key),
+                  static_cast<void*>(key2), static_cast<void*>(cnt), static_cast<void*>(start), tmp})
+    if (q) cudaFree(q);
+  if (e != cudaSuccess) return frcapi::cuda_status(e, "sgd group by user");
+  p->grouped = true;
   return FR_OK;
 }
 
@@ -388,8 +662,9 @@ struct SgdTask {
 int sgd_task_create(void* u) {
   auto* t = static_cast<SgdTask*>(u);
   if (t->p) return FR_OK;
-  const int rc = fr_sgd_problem_generate(t->cfg.V, t->cfg.E, t->cfg.k, t->cfg.edge_seed,
-                                         t->cfg.init_seed, nullptr, &t->p);
+  int rc = fr_sgd_problem_generate(t->cfg.V, t->cfg.E, t->cfg.k, t->cfg.edge_seed,
+                                   t->cfg.init_seed, nullptr, &t->p);
+  if (rc == FR_OK && t->cfg.layout == FR_SGD_LAYOUT_BY_USER) rc = fr_sgd_group_by_user(t->p, t->cfg.edges_per_step, nullptr);
   if (rc == FR_OK) FR_CUDA_TRY(cudaDeviceSynchronize());
   return rc;
 }
@@ -437,6 +712,8 @@ extern "C" {
 
 int fr_sgd_task_create(const fr_sgd_task_config* c, fr_side_task_vtable* vt, void** user) {
   if (!c || !vt || !user) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  if (c->layout != FR_SGD_LAYOUT_COO && c->layout != FR_SGD_LAYOUT_BY_USER)
+    return frcapi::fail(FR_ERR_VALIDATION, "layout must be FR_SGD_LAYOUT_COO or FR_SGD_LAYOUT_BY_USER", "layout");
   if (c->edges_per_step < 1 || c->E < 1)
     return frcapi::fail(FR_ERR_VALIDATION, "E and edges_per_step must be >= 1", "edges_per_step");
   auto* t = new SgdTask;

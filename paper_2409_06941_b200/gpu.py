@@ -303,12 +303,16 @@ class SgdProblem:
     """fr_sgd_problem: rating graph + fp32 latent matrix on the device."""
 
     def __init__(self, V=3072441, E=117185083, k=16, edge_seed=2, init_seed=3, stream=None,
-                 handle=None):
+                 handle=None, by_user=False, window=1 << 21):
+        """by_user: lay the edges out by user (fr_sgd_group_by_user, rounds of
+        `window` edges) -> the user-grouped step kernel."""
         self._owned = handle is None
         if handle is None:
             handle = C.c_void_p()
             check(glib().fr_sgd_problem_generate(V, E, k, edge_seed, init_seed, _stream(stream),
                                                  C.byref(handle)))
+            if by_user:
+                check(glib().fr_sgd_group_by_user(handle, window, _stream(stream)))
         self._h = handle
         u, v, r, L = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p()
         Vc, Ec, kc = C.c_int32(), C.c_int64(), C.c_int32()
@@ -351,22 +355,44 @@ class SgdTask:
     """Built-in Graph-SGD side task (fr_sgd_task_create)."""
 
     def __init__(self, V=3072441, E=117185083, k=16, edge_seed=2, init_seed=3,
-                 edges_per_step=1 << 21, eta=0.01, lam=0.05, total_steps=0):
+                 edges_per_step=1 << 21, eta=0.01, lam=0.05, total_steps=0, by_user=True):
         self.cfg = A.SgdTaskConfigC(V=V, k=k, E=E, edge_seed=edge_seed, init_seed=init_seed,
                                     edges_per_step=edges_per_step, eta=eta, lambda_=lam,
-                                    total_steps=total_steps)
+                                    total_steps=total_steps,
+                                    layout=A.SGD_LAYOUT_BY_USER if by_user else A.SGD_LAYOUT_COO)
         self.vt = A.SideTaskVTableC()
         self.user = C.c_void_p()
         check(glib().fr_sgd_task_create(C.byref(self.cfg), C.byref(self.vt), C.byref(self.user)))
         self.memory_gib = (E * 12 + V * k * 4) / 2 ** 30
         self.units_per_step = self.vt.work_units_per_step
-        self.bytes_per_step = edges_per_step * (12 + 4 * 4 * k)   # 268 B/edge at k = 16
+        # algorithmic bytes: 12 B of edge + L_u and L_v read + written (268 B/edge at
+        # k = 16); by user, L_v per edge (12 + 8k) and L_u once per held block
+        # (a run of equal u, re-read every SGD_REFRESH = 16 edges): + 8k each
+        self.by_user = by_user and k >= 16
+        self.u_loads_per_edge = self._u_loads_per_edge() if self.by_user else 1.0
+        self.bytes_per_step = edges_per_step * (12 + 8 * k + 8 * k * self.u_loads_per_edge)
         self.h2d_per_step = self.d2h_per_step = 0
 
     def problem(self):
         p, ep = C.c_void_p(), C.c_int64()
         check(glib().fr_sgd_task_problem(self.user, C.byref(p), C.byref(ep)))
         return SgdProblem(handle=p), ep.value
+
+    REFRESH = 16   # sgd.cu SGD_REFRESH
+
+    def _u_loads_per_edge(self) -> float:
+        """L_u row loads per edge of the by-user kernel: one per run of equal u
+        and one every REFRESH edges within it (segment cuts ignored: ~1 %)."""
+        u = self.problem()[0].edges()[0]
+        n = u.numel()
+        if n == 0:
+            return 0.0
+        start = torch.ones(n, dtype=torch.bool, device=u.device)
+        start[1:] = u[1:] != u[:-1]
+        idx = torch.arange(n, device=u.device, dtype=torch.int64)
+        run_start = torch.cummax(torch.where(start, idx, torch.zeros_like(idx)), 0).values
+        loads = int((((idx - run_start) % self.REFRESH) == 0).sum())
+        return loads / n
 
 
 class PythonTask:

@@ -44,6 +44,42 @@ def test_oracle_sgd_matches_numpy_bitwise(sidetask_oracle):
     assert abs(sidetask_oracle.sgd_rmse(z["u"], z["v"], z["r"], L) - float(z["rmse"])) < 1e-12
 
 
+def _splitmix64(x):
+    x = (x + np.uint64(0x9E3779B97F4A7C15))
+    x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return x ^ (x >> np.uint64(31))
+
+
+def _by_user_numpy(u, R):
+    """fr_sgd_group_by_user's layout restated with numpy (independent of the C oracle)"""
+    o = np.argsort(u, kind="stable")
+    us = u[o].astype(np.int64)
+    cnt = np.bincount(us, minlength=int(us.max()) + 1)
+    start = np.concatenate([[0], np.cumsum(cnt)[:-1]])
+    rank = np.arange(len(us)) - start[us]
+    deg = cnt[us]
+    npieces, k = (deg + 63) // 64, rank // 64
+    with np.errstate(over="ignore"):
+        h = (_splitmix64(np.uint64(0x5347445250) ^ us.astype(np.uint64)) % np.uint64(R)).astype(np.int64)
+    rnd = (k * R // npieces + h) % R
+    return o[np.argsort(rnd, kind="stable")]
+
+
+@pytest.mark.parametrize("window", [1 << 30, 20000, 4096])
+def test_oracle_sgd_group_by_user_layout(sidetask_oracle, window):
+    """by-user layout: stable by u (Gardenia's CSR order) when one round, else
+    64-edge pieces of each user's run dealt over ceil(E / window) rounds"""
+    V, E = 5000, 200000
+    u, v, r = sidetask_oracle.sgd_edges(V, E, seed=9)
+    R = max(1, -(-E // window))
+    o = _by_user_numpy(u, R) if R > 1 else np.argsort(u, kind="stable")
+    gu, gv, gr = sidetask_oracle.sgd_group_by_user(V, u.copy(), v.copy(), r.copy(), window=window)
+    assert np.array_equal(gu, u[o]) and np.array_equal(gv, v[o]) and np.array_equal(gr, r[o])
+    if R > 1:   # every user's pieces: at most ceil(pieces / R) per window-sized round
+        assert len(np.unique(gu[: E // R])) > 0.5 * min(V, E // R // 40)
+
+
 def test_appendix_a1_issue_order(product, ref):
     want = {0: "F1 F2 F3 F4 B1 B2 B3 B4", 1: "F1 F2 F3 B1 F4 B2 B3 B4",
             2: "F1 F2 B1 F3 B2 F4 B3 B4", 3: "F1 B1 F2 B2 F3 B3 F4 B4"}
