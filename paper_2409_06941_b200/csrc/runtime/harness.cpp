@@ -29,6 +29,8 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <functional>
@@ -108,6 +110,7 @@ struct Task {
   SideTaskRuntime rt;
   TaskProfile prof;
   bool initializing = false;
+  double init_host_us = 0.0;  // host time of the last init hook call (FR_HARNESS_TRACE)
   bool imperative() const { return vt.interface_kind == FR_IMPERATIVE; }
   cudaEvent_t init_a = nullptr, init_b = nullptr;
   bool init_recorded = false;
@@ -680,8 +683,10 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
         }
         ck(cudaEventRecord(t.init_a, side), "record");
         {
+          const auto h0 = std::chrono::steady_clock::now();
           PoolScope ps(device, t.pool);
           hook(t.vt.init(t.user, side), "init");
+          t.init_host_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count();
         }
         ck(cudaEventRecord(t.init_b, side), "record");
         t.initializing = true;
@@ -814,6 +819,8 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
   ck(cudaStreamSynchronize(side), "side sync");
   drain_completions();
   finish_init();
+  for (auto& kv : tasks)  // StopSideTask freed the task's memory: give the pages back
+    if (kv.second->rt.state == SideTaskState::Stopped && kv.second->pool) cudaMemPoolTrimTo(kv.second->pool, 0);
   if (cfg.transport == 1) {
     std::uint32_t timeouts = 0;
     ck(cudaMemcpy(&timeouts, &ctl->link_timeouts, sizeof(timeouts), cudaMemcpyDeviceToHost), "timeouts");
@@ -885,6 +892,9 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
       const double a = elapsed_s(run_start, kv.second->init_a);
       const double b = elapsed_s(run_start, kv.second->init_b);
       if (b > 0) bi.activities.push_back(ActivityRecord{tick_of(std::max(0.0, a)), tick_of(b), kv.first, 0, ActivityKind::Init, false});
+      if (std::getenv("FR_HARNESS_TRACE"))
+        std::fprintf(stderr, "[harness] %s InitSideTask on device %.3f..%.3f ms after run start (hook %.0f us on host)\n",
+                     kv.first.c_str(), a * 1e3, b * 1e3, kv.second->init_host_us);
       kv.second->init_recorded = false;
     }
   }
@@ -1106,7 +1116,6 @@ int fr_harness_submit(fr_harness* h, const char* task_id, const fr_side_task_vta
     cudaMemPoolGetAttribute(t->pool, cudaMemPoolAttrUsedMemHigh, &high);
     std::uint64_t zero = 0;
     cudaMemPoolSetAttribute(t->pool, cudaMemPoolAttrUsedMemHigh, &zero);
-    cudaMemPoolTrimTo(t->pool, 0);
     TaskProfile p;
     p.task_id = task_id;
     p.profiled_steps = n;
@@ -1124,7 +1133,13 @@ int fr_harness_submit(fr_harness* h, const char* task_id, const fr_side_task_vta
       apply_transition(t->rt, TransitionKind::CreateSideTask, 0);
       hook(vt->create ? vt->create(user) : FR_OK, "create");
       h->tasks[task_id] = std::move(t);
+      // The profiling instance's pages stay mapped in the task's pool (the
+      // worker reserved est_memory for it under Alg. 1): InitSideTask then
+      // reuses them instead of growing the pool inside a bubble, which
+      // stalls the dispatch thread 3-23 ms for the image task's 0.5 GB
+      // (FR_HARNESS_TRACE) and once cost a whole 2-epoch warm-up.
     } else {
+      cudaMemPoolTrimTo(t->pool, 0);
       t->user = nullptr;  // rejected: ownership stays with the caller
       t->disp = Disposition::Rejected;
     }
