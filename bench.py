@@ -54,6 +54,7 @@ FRAMES = dict(sw=3840, sh=2160, dw=1920, dh=1080)
 BATCH = 64
 IMAGES_PER_STEP = 16   # ~100 us steps: 3 us inter-step gaps cost 3 % (8 frames: 5.5 %)
 E2E_IMAGES_PER_STEP = 1
+E2E_RING = int(os.environ.get("FR_E2E_RING", "64"))   # device staging slots: the copy engines run ahead of the steps
 OUT_PX = FRAMES["dw"] * FRAMES["dh"]
 PR = dict(scale=20, edge_factor=16, seed=1, iters_per_step=2)
 SGD = dict(V=3072441, E=117185083, k=16, edge_seed=2, init_seed=3, edges_per_step=1 << 21)
@@ -237,7 +238,8 @@ def ours(args):
                 elif n == "image_imperative":
                     task = gpu.ImageTask(batch=BATCH, images_per_step=IMAGES_PER_STEP, imperative=True, **FRAMES)
                 elif n == "image_e2e":
-                    task = gpu.ImageTask(batch=BATCH, images_per_step=E2E_IMAGES_PER_STEP, host_io=True, **FRAMES)
+                    task = gpu.ImageTask(batch=BATCH, images_per_step=E2E_IMAGES_PER_STEP, host_io=True,
+                                         host_ring=E2E_RING, **FRAMES)
                 elif n == "pagerank":
                     task = gpu.PageRankTask(**PR)
                 else:
@@ -394,7 +396,8 @@ def emit(args, results, ws, names, csr):
                "h2d_bytes_per_step": sum(r["image_e2e"]["h2d"] for r in results) / (K * STAGES),
                "d2h_bytes_per_step": sum(r["image_e2e"]["d2h"] for r in results) / (K * STAGES),
                "dT": dT("image_e2e"), "fill": fill("image_e2e"),
-               "path": "fr_image_task host_io=1: pinned host frames, H2D + K5 + D2H per RunNextStep"}
+               "path": f"fr_image_task host_io=1: pinned host frames -> {E2E_RING}-slot device ring filled by the "
+                       "copy engines ahead of the steps (also while the pipeline computes) -> K5 -> D2H per frame"}
     workloads = {
         "pagerank": {"config": "configs[0]: RMAT scale 20 (edge factor 16, seed 1), pull, d=0.85, 2 iterations/step",
                      "value": rate("pagerank"), "unit": "edges/bubble-s", "dT": dT("pagerank"),

@@ -195,6 +195,10 @@ typedef struct fr_image_task_config {
                                    whole batch, paused on the device per output row */
   uint64_t seed;
   int64_t total_steps;          /* <= 0: unbounded */
+  int32_t host_ring;            /* host_io: device staging slots, in steps (>= 2; 0 -> 2).
+                                   The H2D of later steps' frames runs ahead on the copy
+                                   engines -- also while the pipeline computes -- and each
+                                   step's D2H leaves on its own stream */
 } fr_image_task_config;
 int fr_image_task_create(const fr_image_task_config* cfg, fr_side_task_vtable* vt, void** user);
 /* bytes resident on the GPU once InitSideTask ran (memory_demand) */

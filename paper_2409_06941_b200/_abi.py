@@ -483,7 +483,7 @@ class ImageTaskConfigC(Struct):
     _fields_ = [
         ("sw", i32), ("sh", i32), ("dw", i32), ("dh", i32),
         ("batch", i32), ("images_per_step", i32), ("host_io", i32), ("interface_kind", i32),
-        ("seed", u64), ("total_steps", i64),
+        ("seed", u64), ("total_steps", i64), ("host_ring", i32),
     ]
 
 

@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cstring>
 #include <new>
+#include <vector>
 
 #include "capi_util.hpp"
 #include "freeride_gpu.h"
@@ -25,13 +26,17 @@ struct ImageTask {
   void* wmp = nullptr;  // prepared watermark (fr_img_prepare_watermark)
   uint8_t* h_src = nullptr;  // pinned host batch (host_io)
   uint8_t* h_dst = nullptr;
-  // host_io: double-buffered device frames; the next step's frames are
-  // prefetched on `pf` while this step's kernel and D2H run (joined before
-  // the step ends, so no work outlives its step)
-  cudaStream_t pf = nullptr;
-  cudaEvent_t e_pf = nullptr, e_free[2] = {nullptr, nullptr};
-  int cur = 0;
-  bool ready = false;
+  // host_io: a ring of `ring` step slots in device memory, fed like a data
+  // loader.  The copy engines run ahead of the steps: slot j's H2D (stream
+  // pf) waits only for the slot's previous D2H (stream dh), so while the
+  // pipeline computes -- when no step may run -- PCIe keeps filling the ring,
+  // and a bubble's steps find their frames resident.  A step is just the
+  // K5 kernel behind its slot's `ready` event; its D2H leaves on dh.
+  cudaStream_t pf = nullptr, dh = nullptr;
+  std::vector<cudaEvent_t> e_ready, e_done, e_free;
+  int ring = 0;
+  int64_t issued = 0;   // steps whose frames were queued on pf
+  bool primed = false;
   uint32_t* ctr = nullptr;   // imperative: preemptible row cursor + rows completed
   uint64_t rows_base = 0;    // rows completed by earlier Init..Stop lifetimes
   int64_t cursor = 0;
@@ -48,6 +53,13 @@ int cu(cudaError_t e, const char* what) {
 
 int release(ImageTask* t, cudaStream_t s) {
   int rc = FR_OK;
+  if (t->primed) {  // the copy streams may still run ahead: join them before freeing
+    for (cudaStream_t q : {t->pf, t->dh}) {
+      cudaEvent_t e = t->e_free.empty() ? nullptr : t->e_free[0];
+      if (e && cudaEventRecord(e, q) == cudaSuccess) cudaStreamWaitEvent(s, e, 0);
+    }
+    t->primed = false;
+  }
   if (t->ctr) {  // keep the completed-row count across Stop/Init
     uint64_t done = 0;
     if (cudaMemcpyAsync(&done, t->ctr + 2, sizeof(done), cudaMemcpyDeviceToHost, s) == cudaSuccess &&
@@ -69,23 +81,29 @@ int img_create(void* u) {
   return FR_OK;
 }
 
+int host_frames(ImageTask* t, cudaStream_t s);
+
 int img_init(void* u, void* stream) {
   auto* t = static_cast<ImageTask*>(u);
   auto s = static_cast<cudaStream_t>(stream);
   t->last = s;
   const fr_image_task_config& c = t->cfg;
-  const std::size_t resident = c.host_io ? static_cast<std::size_t>(c.images_per_step) : static_cast<std::size_t>(c.batch);
-  int rc = cu(cudaMallocAsync(reinterpret_cast<void**>(&t->src), (c.host_io ? 2 : 1) * resident * t->src_img(), s), "src");
+  const std::size_t resident = c.host_io ? static_cast<std::size_t>(t->ring) * c.images_per_step
+                                         : static_cast<std::size_t>(c.batch);
+  int rc = cu(cudaMallocAsync(reinterpret_cast<void**>(&t->src), resident * t->src_img(), s), "src");
   if (rc == FR_OK) rc = cu(cudaMallocAsync(reinterpret_cast<void**>(&t->dst), resident * t->dst_img(), s), "dst");
   if (rc == FR_OK && c.host_io) {
     if (!t->pf) {
       rc = cu(cudaStreamCreateWithFlags(&t->pf, cudaStreamNonBlocking), "prefetch stream");
-      for (cudaEvent_t* e : {&t->e_pf, &t->e_free[0], &t->e_free[1]})
-        if (rc == FR_OK) rc = cu(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "prefetch events");
+      if (rc == FR_OK) rc = cu(cudaStreamCreateWithFlags(&t->dh, cudaStreamNonBlocking), "D2H stream");
+      for (auto* v : {&t->e_ready, &t->e_done, &t->e_free}) {
+        v->assign(t->ring, nullptr);
+        for (cudaEvent_t& e : *v)
+          if (rc == FR_OK) rc = cu(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "ring events");
+      }
     }
-    for (int b = 0; rc == FR_OK && b < 2; ++b) rc = cu(cudaEventRecord(t->e_free[b], s), "prefetch events");
-    t->cur = 0;
-    t->ready = false;
+    t->issued = 0;
+    t->primed = false;
   }
   if (rc == FR_OK) rc = cu(cudaMallocAsync(reinterpret_cast<void**>(&t->wm), static_cast<std::size_t>(c.dw) * c.dh * 4, s), "wm");
   int64_t pbytes = 0;
@@ -99,6 +117,16 @@ int img_init(void* u, void* stream) {
   }
   if (rc != FR_OK) return rc;
   if (!c.host_io) return fr_img_generate(t->src, c.batch, c.sw, c.sh, 3, c.seed, 0, s);
+  rc = host_frames(t, s);
+  // every slot starts free once Init's work on s is done (the first Init
+  // uses the device ring as scratch to generate the host frames)
+  for (int j = 0; rc == FR_OK && j < t->ring; ++j) rc = cu(cudaEventRecord(t->e_free[j], s), "ring events");
+  return rc;
+}
+
+int host_frames(ImageTask* t, cudaStream_t s) {
+  const fr_image_task_config& c = t->cfg;
+  int rc = FR_OK;
   if (!t->h_src) {  // host frames: generated once, kept across Stop/Init cycles
     rc = cu(cudaMallocHost(reinterpret_cast<void**>(&t->h_src), static_cast<std::size_t>(c.batch) * t->src_img()), "pinned src");
     if (rc == FR_OK) rc = cu(cudaMallocHost(reinterpret_cast<void**>(&t->h_dst), static_cast<std::size_t>(c.batch) * t->dst_img()), "pinned dst");
@@ -120,25 +148,30 @@ int img_step(void* u, void* stream) {
   const int n = c.images_per_step;
   int rc;
   if (c.host_io) {
-    // frames i0.. are in buffer `cur` (prefetched by the previous step) or
-    // copied now; then kernel + D2H on the step's stream while the next
-    // step's frames stream into the other buffer on `pf` (PCIe is full
-    // duplex: H2D of step i+1 overlaps D2H of step i)
-    const std::size_t fb = static_cast<std::size_t>(n) * t->src_img();
-    uint8_t* buf = t->src + t->cur * fb;
+    const std::size_t fb = static_cast<std::size_t>(n) * t->src_img(), ob = static_cast<std::size_t>(n) * t->dst_img();
+    // queue H2D for the steps up to `ring` ahead of this one (each waits for
+    // its slot's previous D2H; the first call after Init fills the ring)
+    auto prefetch = [&](int64_t k) {  // step k = frames (i0 + (k - steps) n) % batch
+      const int j = static_cast<int>(k % t->ring);
+      const int64_t f = (i0 + (k - t->steps) * n) % c.batch;
+      int r = cu(cudaStreamWaitEvent(t->pf, t->e_free[j], 0), "ring wait");
+      if (r == FR_OK) r = cu(cudaMemcpyAsync(t->src + j * fb, t->h_src + f * t->src_img(), fb, cudaMemcpyHostToDevice, t->pf), "H2D ring");
+      if (r == FR_OK) r = cu(cudaEventRecord(t->e_ready[j], t->pf), "ring ready");
+      return r;
+    };
     rc = FR_OK;
-    if (!t->ready) rc = cu(cudaMemcpyAsync(buf, t->h_src + i0 * t->src_img(), fb, cudaMemcpyHostToDevice, s), "H2D step");
-    if (rc == FR_OK) rc = fr_img_resize_watermark_prepared(t->plan, buf, t->dst, t->wmp, n, s);
-    if (rc == FR_OK) rc = cu(cudaEventRecord(t->e_free[t->cur], s), "buffer free");
-    if (rc == FR_OK) rc = cu(cudaMemcpyAsync(t->h_dst + i0 * t->dst_img(), t->dst, n * t->dst_img(), cudaMemcpyDeviceToHost, s), "D2H step");
-    const int other = t->cur ^ 1;
-    const int64_t next = (i0 + n) % c.batch;
-    if (rc == FR_OK) rc = cu(cudaStreamWaitEvent(t->pf, t->e_free[other], 0), "prefetch wait");
-    if (rc == FR_OK) rc = cu(cudaMemcpyAsync(t->src + other * fb, t->h_src + next * t->src_img(), fb, cudaMemcpyHostToDevice, t->pf), "H2D prefetch");
-    if (rc == FR_OK) rc = cu(cudaEventRecord(t->e_pf, t->pf), "prefetch done");
-    if (rc == FR_OK) rc = cu(cudaStreamWaitEvent(s, t->e_pf, 0), "prefetch join");
-    t->cur = other;
-    t->ready = true;
+    if (!t->primed) {
+      t->issued = t->steps;
+      t->primed = true;
+    }
+    while (rc == FR_OK && t->issued < t->steps + t->ring) rc = prefetch(t->issued++);
+    const int j = static_cast<int>(t->steps % t->ring);
+    if (rc == FR_OK) rc = cu(cudaStreamWaitEvent(s, t->e_ready[j], 0), "frames ready");
+    if (rc == FR_OK) rc = fr_img_resize_watermark_prepared(t->plan, t->src + j * fb, t->dst + j * ob, t->wmp, n, s);
+    if (rc == FR_OK) rc = cu(cudaEventRecord(t->e_done[j], s), "step done");
+    if (rc == FR_OK) rc = cu(cudaStreamWaitEvent(t->dh, t->e_done[j], 0), "D2H wait");
+    if (rc == FR_OK) rc = cu(cudaMemcpyAsync(t->h_dst + i0 * t->dst_img(), t->dst + j * ob, ob, cudaMemcpyDeviceToHost, t->dh), "D2H step");
+    if (rc == FR_OK) rc = cu(cudaEventRecord(t->e_free[j], t->dh), "slot free");
   } else {
     rc = fr_img_resize_watermark_prepared(t->plan, t->src + i0 * t->src_img(), t->dst + i0 * t->dst_img(), t->wmp, n, s);
   }
@@ -193,9 +226,11 @@ void img_destroy(void* u) {
   if (t->last) cudaStreamSynchronize(t->last);
   if (t->h_src) cudaFreeHost(t->h_src);
   if (t->h_dst) cudaFreeHost(t->h_dst);
-  for (cudaEvent_t e : {t->e_pf, t->e_free[0], t->e_free[1]})
-    if (e) cudaEventDestroy(e);
-  if (t->pf) cudaStreamDestroy(t->pf);
+  for (auto* v : {&t->e_ready, &t->e_done, &t->e_free})
+    for (cudaEvent_t e : *v)
+      if (e) cudaEventDestroy(e);
+  for (cudaStream_t q : {t->pf, t->dh})
+    if (q) cudaStreamDestroy(q);
   fr_img_plan_destroy(t->plan);
   delete t;
 }
@@ -206,8 +241,8 @@ extern "C" {
 
 int fr_image_task_memory(const fr_image_task_config* c, double* gib) {
   if (!c || !gib) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
-  const double resident = c->host_io ? c->images_per_step : c->batch;
-  const double bytes = resident * ((c->host_io ? 2.0 : 1.0) * double(c->sw) * c->sh * 3 + double(c->dw) * c->dh * 3) +
+  const double resident = c->host_io ? double(std::max(2, c->host_ring)) * c->images_per_step : c->batch;
+  const double bytes = resident * (double(c->sw) * c->sh * 3 + double(c->dw) * c->dh * 3) +
                        double(c->dw) * c->dh * 12;
   *gib = bytes / (1024.0 * 1024.0 * 1024.0);
   return FR_OK;
@@ -221,9 +256,11 @@ int fr_image_task_create(const fr_image_task_config* c, fr_side_task_vtable* vt,
     return frcapi::fail(FR_ERR_VALIDATION, "interface_kind must be FR_ITERATIVE or FR_IMPERATIVE", "interface_kind");
   if (c->interface_kind == FR_IMPERATIVE && c->host_io)
     return frcapi::fail(FR_ERR_UNSUPPORTED, "the imperative image task keeps its batch resident (host_io = 0)");
+  if (c->host_ring < 0) return frcapi::fail(FR_ERR_VALIDATION, "host_ring must be >= 0", "host_ring");
   auto* t = new (std::nothrow) ImageTask;
   if (!t) return frcapi::fail(FR_ERR_INVARIANT, "out of host memory");
   t->cfg = *c;
+  t->ring = std::max(2, c->host_ring);
   std::memset(vt, 0, sizeof(*vt));
   vt->carveout_hint = 100;
   vt->create = img_create;
@@ -255,6 +292,10 @@ int fr_image_task_buffers(void* user, const uint8_t** src, uint8_t** dst, const 
 int fr_image_task_host_output(void* user, const uint8_t** h_dst) {
   auto* t = static_cast<ImageTask*>(user);
   if (!t || !h_dst) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  if (t->dh) {  // readout point: the ring's D2H landed
+    const int rc = cu(cudaStreamSynchronize(t->dh), "D2H ring");
+    if (rc != FR_OK) return rc;
+  }
   *h_dst = t->h_dst;
   return FR_OK;
 }

@@ -145,11 +145,13 @@ class ImageTask:
     whose ownership passes to the Harness on submit."""
 
     def __init__(self, sw=3840, sh=2160, dw=1920, dh=1080, batch=64, images_per_step=8,
-                 host_io=False, seed=1, total_steps=0, imperative=False):
+                 host_io=False, seed=1, total_steps=0, imperative=False, host_ring=0):
+        """host_ring (host_io only): device staging slots in steps; the copy
+        engines prefetch that many steps ahead, also while the pipeline computes"""
         self.cfg = A.ImageTaskConfigC(sw=sw, sh=sh, dw=dw, dh=dh, batch=batch,
                                       images_per_step=images_per_step, host_io=int(host_io),
                                       interface_kind=int(bool(imperative)), seed=seed,
-                                      total_steps=total_steps)
+                                      total_steps=total_steps, host_ring=host_ring)
         self.imperative = bool(imperative)
         self.batch, self.dw, self.dh = batch, dw, dh
         self.vt = A.SideTaskVTableC()

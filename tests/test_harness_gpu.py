@@ -85,12 +85,15 @@ def test_work_units_credit_the_completing_task(g):
     h.close()
 
 
-def test_host_io_prefetch_pipeline_bit_exact(g, sidetask_oracle):
-    """e2e mode: frames in pinned host memory, H2D of step i+1 prefetched while
-    step i's kernel and D2H run; every output frame lands in host memory
-    bit-exact once the batch has been covered."""
+@pytest.mark.parametrize("ring", [0, 2, 5])
+def test_host_io_prefetch_pipeline_bit_exact(g, sidetask_oracle, ring):
+    """e2e mode: frames in pinned host memory staged through a ring of device
+    slots the copy engines fill ahead of the steps (also while the pipeline
+    computes), D2H on its own stream; every output frame lands in host memory
+    bit-exact once the batch has been covered (ring 5 > the batch's 3 steps:
+    slots are reused across wrap-arounds of the batch)."""
     h = small_harness(g, stage=2)
-    task = g.ImageTask(batch=6, images_per_step=2, host_io=True, seed=41)
+    task = g.ImageTask(batch=6, images_per_step=2, host_io=True, seed=41, host_ring=ring)
     ok, _ = h.submit("img-host", task, profile_steps=6)
     assert ok
     done = 0
