@@ -54,7 +54,7 @@ FRAMES = dict(sw=3840, sh=2160, dw=1920, dh=1080)
 BATCH = 64
 IMAGES_PER_STEP = 16   # ~100 us steps: 3 us inter-step gaps cost 3 % (8 frames: 5.5 %)
 E2E_IMAGES_PER_STEP = 1
-E2E_RING = int(os.environ.get("FR_E2E_RING", "64"))   # device staging slots: the copy engines run ahead of the steps
+E2E_RING = int(os.environ.get("FR_E2E_RING", "128"))   # device staging slots: the copy engines run ahead of the steps
 OUT_PX = FRAMES["dw"] * FRAMES["dh"]
 PR = dict(scale=20, edge_factor=16, seed=1, iters_per_step=2)
 SGD = dict(V=3072441, E=117185083, k=16, edge_seed=2, init_seed=3, edges_per_step=1 << 21)
