@@ -112,8 +112,13 @@ def linked_harvest(make_task, stage_shape: dict, num_micro_batches: int, epochs:
     h.reprofile_bubbles()
     task = make_task()
     ok, _ = h.submit(task_name, task, profile_steps=16)
-    if not ok:
-        raise RuntimeError(f"stage {rank}: side task rejected by Alg. 1")
+    oks = [None] * p
+    dist.all_gather_object(oks, bool(ok), group=group)  # every stage gives up together
+    if not all(oks):
+        h.close()
+        for x in opened:
+            gpu.ipc_close(x)
+        raise RuntimeError(f"stages {[i for i, o in enumerate(oks) if not o]}: side task rejected by Alg. 1")
     h.run(max(1, warmup), True)
     base = h.run(epochs, False)
     r = h.run(epochs, True)
