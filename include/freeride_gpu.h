@@ -96,6 +96,11 @@ typedef struct fr_pr_graph fr_pr_graph;
 typedef struct fr_pr_state fr_pr_state;
 int fr_pr_graph_rmat(int32_t scale, int32_t edge_factor, uint64_t seed, void* stream,
                      fr_pr_graph** out);
+/* The caller's graph: E directed edges src[e] -> dst[e] (device int32 arrays,
+ * read during the call), ids in [0, V) (else FR_ERR_VALIDATION); self loops
+ * and duplicates dropped like the RMAT path.  Synchronous. */
+int fr_pr_graph_from_edges(int32_t V, int64_t E, const int32_t* src, const int32_t* dst, void* stream,
+                           fr_pr_graph** out);
 int fr_pr_graph_destroy(fr_pr_graph* g);
 int fr_pr_graph_info(const fr_pr_graph* g, int32_t* V, int64_t* E, int32_t* n_blocks);
 /* device pointers: offsets[V+1], col_idx[E], outdeg[V] */

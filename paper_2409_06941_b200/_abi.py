@@ -494,6 +494,7 @@ class PageRankTaskConfigC(Struct):
 
 GPU_PROTOTYPES.update({
     "fr_pr_graph_rmat": (C.c_int, [i32, i32, u64, vp, P(vp)]),
+    "fr_pr_graph_from_edges": (C.c_int, [i32, i64, vp, vp, vp, P(vp)]),
     "fr_pr_graph_destroy": (C.c_int, [vp]),
     "fr_pr_graph_info": (C.c_int, [vp, P(i32), P(i64), P(i32)]),
     "fr_pr_graph_csr": (C.c_int, [vp, P(vp), P(vp), P(vp)]),

@@ -65,6 +65,15 @@ __global__ void rmat_kernel(int scale, int64_t m, uint64_t seed, int32_t* __rest
   }
 }
 
+__global__ void check_ids_kernel(const int32_t* __restrict__ src, const int32_t* __restrict__ dst, int64_t m,
+                                 int32_t V, int32_t* __restrict__ bad) {
+  int32_t n = 0;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < m;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    n += (static_cast<uint32_t>(src[e]) >= static_cast<uint32_t>(V)) + (static_cast<uint32_t>(dst[e]) >= static_cast<uint32_t>(V));
+  if (n) atomicAdd(bad, n);
+}
+
 // key = dst << 32 | src, self loops mapped to the all-ones sentinel (sorted last)
 __global__ void edge_keys_kernel(const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
                                  int64_t m, uint64_t* __restrict__ keys) {
@@ -498,19 +507,15 @@ int build_work(fr_pr_graph* g, cudaStream_t s) {
   return FR_OK;
 }
 
-}  // namespace
-
-extern "C" {
-
-int fr_pr_graph_rmat(int32_t scale, int32_t edge_factor, uint64_t seed, void* stream,
-                     fr_pr_graph** out) {
-  if (!out) return frcapi::fail(FR_ERR_ARGUMENT, "null graph out");
-  if (scale < 1 || scale > 30 || edge_factor < 1)
-    return frcapi::fail(FR_ERR_VALIDATION, "scale in [1,30], edge_factor >= 1", "scale");
-  auto s = static_cast<cudaStream_t>(stream);
-  const int64_t m = static_cast<int64_t>(edge_factor) << scale;
+// Builds the graph from m directed edges src[e] -> dst[e] (device): either
+// RMAT-generated (gen_scale > 0, src/dst ignored) or the caller's (ids
+// checked to lie in [0, V)).  Self loops and duplicates are dropped.
+int build_graph(int32_t Vn, int64_t m, const int32_t* user_src, const int32_t* user_dst, int32_t gen_scale,
+                uint64_t seed, cudaStream_t s, fr_pr_graph** out) {
   auto* g = new fr_pr_graph;
-  g->V = 1 << scale;
+  g->V = Vn;
+  int scale = 1;  // bits of a vertex id
+  while (scale < 31 && (int64_t(1) << scale) < Vn) ++scale;
   const size_t V = static_cast<size_t>(g->V);
   int32_t *src = nullptr, *dst = nullptr, *indeg = nullptr, *d_sel = nullptr;
   int32_t *colid = nullptr, *colinv = nullptr, *rowof = nullptr, *rindeg = nullptr;
@@ -530,25 +535,37 @@ int fr_pr_graph_rmat(int32_t scale, int32_t edge_factor, uint64_t seed, void* st
     if (step(cudaMalloc(&tmp, need), "cub temp")) tmp_bytes = need;
   };
   const int gv = grid_for(g->V, 256, 8), gm = grid_for(m, 256, 16);
-  step(cudaMalloc(&src, m * sizeof(int32_t)), "rmat src");
-  step(cudaMalloc(&dst, m * sizeof(int32_t)), "rmat dst");
-  step(cudaMalloc(&keys, m * sizeof(uint64_t)), "keys");
-  step(cudaMalloc(&sorted, m * sizeof(uint64_t)), "sorted");
+  const size_t mb = static_cast<size_t>(std::max<int64_t>(m, 1));
+  if (gen_scale > 0) {
+    step(cudaMalloc(&src, mb * sizeof(int32_t)), "rmat src");
+    step(cudaMalloc(&dst, mb * sizeof(int32_t)), "rmat dst");
+  }
+  step(cudaMalloc(&keys, mb * sizeof(uint64_t)), "keys");
+  step(cudaMalloc(&sorted, mb * sizeof(uint64_t)), "sorted");
   step(cudaMalloc(&d_sel, sizeof(int32_t)), "count");
-  if (rc == FR_OK) {
-    rmat_kernel<<<gm, 256, 0, s>>>(scale, m, seed, src, dst);
-    edge_keys_kernel<<<gm, 256, 0, s>>>(src, dst, m, keys);
+  if (rc == FR_OK && gen_scale == 0 && m > 0) {  // caller's edges: every id in [0, V)
+    int32_t bad = 0;
+    step(cudaMemsetAsync(d_sel, 0, sizeof(int32_t), s), "memset");
+    check_ids_kernel<<<gm, 256, 0, s>>>(user_src, user_dst, m, Vn, d_sel);
+    step(cudaMemcpyAsync(&bad, d_sel, sizeof(int32_t), cudaMemcpyDeviceToHost, s), "id check");
+    step(cudaStreamSynchronize(s), "id check");
+    if (rc == FR_OK && bad)
+      rc = frcapi::fail(FR_ERR_VALIDATION, std::to_string(bad) + " edge endpoints outside [0, V)", "edges");
+  }
+  if (rc == FR_OK && m > 0) {
+    if (gen_scale > 0) rmat_kernel<<<gm, 256, 0, s>>>(gen_scale, m, seed, src, dst);
+    edge_keys_kernel<<<gm, 256, 0, s>>>(gen_scale > 0 ? src : user_src, gen_scale > 0 ? dst : user_dst, m, keys);
     step(cudaGetLastError(), "rmat / keys");
   }
   size_t need = 0;
-  if (rc == FR_OK) {
+  if (rc == FR_OK && m > 0) {
     cub::DeviceRadixSort::SortKeys(nullptr, need, keys, sorted, static_cast<int>(m), 0, 64, s);
     temp(need);
     cub::DeviceSelect::Unique(nullptr, need, sorted, keys, d_sel, static_cast<int>(m), s);
     temp(need);
   }
   int32_t n_unique = 0;
-  if (rc == FR_OK) {
+  if (rc == FR_OK && m > 0) {
     step(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, keys, sorted, static_cast<int>(m), 0, 64, s), "sort");
     step(cub::DeviceSelect::Unique(tmp, tmp_bytes, sorted, keys, d_sel, static_cast<int>(m), s), "unique");
     step(cudaMemcpyAsync(&n_unique, d_sel, sizeof(int32_t), cudaMemcpyDeviceToHost, s), "count");
@@ -631,6 +648,28 @@ int fr_pr_graph_rmat(int32_t scale, int32_t edge_factor, uint64_t seed, void* st
   }
   *out = g;
   return FR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fr_pr_graph_rmat(int32_t scale, int32_t edge_factor, uint64_t seed, void* stream,
+                     fr_pr_graph** out) {
+  if (!out) return frcapi::fail(FR_ERR_ARGUMENT, "null graph out");
+  if (scale < 1 || scale > 30 || edge_factor < 1)
+    return frcapi::fail(FR_ERR_VALIDATION, "scale in [1,30], edge_factor >= 1", "scale");
+  const int64_t m = static_cast<int64_t>(edge_factor) << scale;
+  if (m > INT32_MAX) return frcapi::fail(FR_ERR_VALIDATION, "edge_factor << scale must be < 2^31", "edge_factor");
+  return build_graph(1 << scale, m, nullptr, nullptr, scale, seed, static_cast<cudaStream_t>(stream), out);
+}
+
+int fr_pr_graph_from_edges(int32_t V, int64_t E, const int32_t* src, const int32_t* dst, void* stream,
+                           fr_pr_graph** out) {
+  if (!out) return frcapi::fail(FR_ERR_ARGUMENT, "null graph out");
+  if (V < 1 || E < 0 || E > INT32_MAX) return frcapi::fail(FR_ERR_VALIDATION, "V >= 1, 0 <= E < 2^31", "V");
+  if (E > 0 && (!src || !dst)) return frcapi::fail(FR_ERR_ARGUMENT, "null edge arrays");
+  return build_graph(V, E, src, dst, 0, 0, static_cast<cudaStream_t>(stream), out);
 }
 
 int fr_pr_graph_destroy(fr_pr_graph* g) {

@@ -222,15 +222,32 @@ class SyntheticTask:
 
 
 class PageRankGraph:
-    """fr_pr_graph: RMAT graph as an incoming CSR on the device."""
+    """fr_pr_graph: an incoming CSR on the device -- RMAT-generated, or the
+    caller's edge list via PageRankGraph.from_edges."""
 
-    def __init__(self, scale=20, edge_factor=16, seed=1, stream=None):
-        h = C.c_void_p()
-        check(glib().fr_pr_graph_rmat(scale, edge_factor, seed, _stream(stream), C.byref(h)))
+    def __init__(self, scale=20, edge_factor=16, seed=1, stream=None, _handle=None):
+        h = _handle
+        if h is None:
+            h = C.c_void_p()
+            check(glib().fr_pr_graph_rmat(scale, edge_factor, seed, _stream(stream), C.byref(h)))
         self._h = h
         V, E, nb = C.c_int32(), C.c_int64(), C.c_int32()
         check(glib().fr_pr_graph_info(h, C.byref(V), C.byref(E), C.byref(nb)))
         self.V, self.E, self.n_blocks = V.value, E.value, nb.value
+
+    @classmethod
+    def from_edges(cls, V: int, src, dst, stream=None) -> "PageRankGraph":
+        """edges src[e] -> dst[e] (int32 torch tensors, copied to the device if needed)"""
+        glib()
+        s = torch.as_tensor(src, dtype=torch.int32).cuda().contiguous()
+        d = torch.as_tensor(dst, dtype=torch.int32).cuda().contiguous()
+        if s.numel() != d.numel():
+            raise ValueError("src and dst must have the same length")
+        torch.cuda.synchronize()
+        h = C.c_void_p()
+        check(glib().fr_pr_graph_from_edges(V, s.numel(), s.data_ptr() if s.numel() else None,
+                                            d.data_ptr() if d.numel() else None, _stream(stream), C.byref(h)))
+        return cls(_handle=h)
 
     def csr(self):
         o, c, d = C.c_void_p(), C.c_void_p(), C.c_void_p()
