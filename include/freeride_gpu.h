@@ -123,6 +123,11 @@ int fr_pr_ranks(const fr_pr_state* st, const float** r, int64_t* iterations);
 typedef struct fr_sgd_problem fr_sgd_problem;
 int fr_sgd_problem_generate(int32_t V, int64_t E, int32_t k, uint64_t edge_seed,
                             uint64_t init_seed, void* stream, fr_sgd_problem** out);
+/* The caller's ratings: E edges (u, v, r) (host or device arrays, copied),
+ * endpoints in [0, V) (else FR_ERR_VALIDATION), latent matrix seeded like the
+ * generator's.  Synchronous. */
+int fr_sgd_problem_from_edges(int32_t V, int64_t E, int32_t k, const int32_t* u, const int32_t* v,
+                              const float* r, uint64_t init_seed, void* stream, fr_sgd_problem** out);
 int fr_sgd_problem_destroy(fr_sgd_problem* p);
 /* L ~ U(0, 1/sqrt(k)), seeded */
 int fr_sgd_reinit(fr_sgd_problem* p, uint64_t init_seed, void* stream);

@@ -518,6 +518,7 @@ SGD_LAYOUT_COO, SGD_LAYOUT_BY_USER = 0, 1
 
 GPU_PROTOTYPES.update({
     "fr_sgd_problem_generate": (C.c_int, [i32, i64, i32, u64, u64, vp, P(vp)]),
+    "fr_sgd_problem_from_edges": (C.c_int, [i32, i64, i32, vp, vp, vp, u64, vp, P(vp)]),
     "fr_sgd_problem_destroy": (C.c_int, [vp]),
     "fr_sgd_reinit": (C.c_int, [vp, u64, vp]),
     "fr_sgd_step": (C.c_int, [vp, i64, i64, C.c_float, C.c_float, vp]),

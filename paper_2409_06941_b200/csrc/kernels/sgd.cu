@@ -33,6 +33,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <string>
 
 #include "freeride_gpu.h"
 #include "kernels/common.cuh"
@@ -309,6 +310,15 @@ __global__ void sgd_gather3_kernel(const int32_t* __restrict__ perm, const int32
   }
 }
 
+__global__ void sgd_check_ids_kernel(const int32_t* __restrict__ u, const int32_t* __restrict__ v, int64_t n,
+                                     int32_t V, int32_t* __restrict__ bad) {
+  int32_t k = 0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    k += (static_cast<uint32_t>(u[i]) >= static_cast<uint32_t>(V)) + (static_cast<uint32_t>(v[i]) >= static_cast<uint32_t>(V));
+  if (k) atomicAdd(bad, k);
+}
+
 __global__ void sgd_iota_kernel(int32_t* __restrict__ x, int64_t n) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -371,9 +381,48 @@ struct fr_sgd_problem {
   double* acc = nullptr;
   int sms = 148;
   bool grouped = false;  // edges stable-sorted by u (fr_sgd_group_by_user)
+  int64_t max_deg = 0;   // largest number of ratings touching one vertex (u or v side)
 };
 
 namespace {
+
+// Hub cap: with F edges in flight a vertex of degree d sees ~F d / E
+// concurrent updates, applied from the same stale row -- a mini-batch whose
+// effective step grows with it.  Keep that <= kSgdHubConc for the hottest
+// vertex (no effect at the Orkut shape: d / E = 8.5e-5 allows 1.9e5 edges in
+// flight; a Zipf(1.3) item with a quarter of all ratings would otherwise
+// take thousands of simultaneous updates and diverge).
+constexpr int64_t kSgdHubConc = 16;
+int64_t hub_cap(const fr_sgd_problem* p) {
+  if (p->max_deg <= 0 || p->E <= 0) return INT64_MAX;
+  return std::max<int64_t>(64, kSgdHubConc * p->E / p->max_deg);
+}
+
+// degree histogram of both endpoints -> p->max_deg (setup, synchronous)
+cudaError_t measure_max_degree(fr_sgd_problem* p, cudaStream_t s) {
+  p->max_deg = 0;
+  if (p->E == 0) return cudaSuccess;
+  int32_t *cnt = nullptr, *mx = nullptr;
+  void* tmp = nullptr;
+  size_t need = 0;
+  cub::DeviceReduce::Max(nullptr, need, cnt, mx, p->V, s);
+  cudaError_t e = cudaMalloc(&cnt, size_t(p->V) * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&mx, sizeof(int32_t));
+  if (e == cudaSuccess) e = cudaMalloc(&tmp, std::max<size_t>(need, 1));
+  if (e == cudaSuccess) e = cudaMemsetAsync(cnt, 0, size_t(p->V) * 4, s);
+  if (e == cudaSuccess) {
+    sgd_count_kernel<<<grid_for(p->E, 256, 16), 256, 0, s>>>(p->u, p->E, cnt);
+    sgd_count_kernel<<<grid_for(p->E, 256, 16), 256, 0, s>>>(p->v, p->E, cnt);
+    e = cub::DeviceReduce::Max(tmp, need, cnt, mx, p->V, s);
+  }
+  int32_t h = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&h, mx, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  for (void* q : {static_cast<void*>(cnt), static_cast<void*>(mx), tmp})
+    if (q) cudaFree(q);
+  if (e == cudaSuccess) p->max_deg = h;
+  return e;
+}
 
 template <int K>
 void launch_step(fr_sgd_problem* p, int64_t a, int64_t b, float eta, float lam, cudaStream_t s) {
@@ -397,7 +446,7 @@ void launch_step(fr_sgd_problem* p, int64_t a, int64_t b, float eta, float lam, 
     return e ? std::max(1, std::atoi(e)) : kSgdConflictDiv;
   }();
   const int64_t groups = (b - a + kSgdEpi - 1) / kSgdEpi;
-  const int64_t cap_groups = std::max<int64_t>(1, int64_t(p->V) / div / kSgdEpi);
+  const int64_t cap_groups = std::max<int64_t>(1, std::min(int64_t(p->V) / div, hub_cap(p)) / kSgdEpi);
   const int64_t want = (std::min(groups, cap_groups) * Row<K>::kLanes + kSgdThreads - 1) / kSgdThreads;
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(p->sms) * per_sm)));
   sgd_step_kernel<K><<<grid, kSgdThreads, 0, s>>>(p->u, p->v, p->r, p->L, a, b, eta, lam);
@@ -419,7 +468,7 @@ void launch_user_step(fr_sgd_problem* p, int64_t a, int64_t b, float eta, float 
     return e ? std::max(1, std::atoi(e)) : kSgdConflictDiv;
   }();
   const int64_t n = b - a;
-  const int64_t cap_groups = std::max<int64_t>(1, int64_t(p->V) / div / D);
+  const int64_t cap_groups = std::max<int64_t>(1, std::min(int64_t(p->V) / div, hub_cap(p)) / D);
   const int64_t max_groups = int64_t(p->sms) * per_sm * kSgdThreads / LN;
   const int64_t groups = std::min({(n + D - 1) / D, cap_groups, max_groups});
   const int64_t seg = ((n + groups - 1) / groups + D - 1) / D * D;
@@ -467,8 +516,62 @@ int fr_sgd_problem_generate(int32_t V, int64_t E, int32_t k, uint64_t edge_seed,
   }
   if (E > 0) sgd_edges_kernel<<<grid_for(E, 256, 16), 256, 0, s>>>(V, E, edge_seed, p->u, p->v, p->r);
   FR_CUDA_LAUNCHED("sgd_edges");
+  if (const cudaError_t me = measure_max_degree(p, s); me != cudaSuccess) {
+    fr_sgd_problem_destroy(p);
+    return frcapi::cuda_status(me, "sgd degree histogram");
+  }
   *out = p;
   return fr_sgd_reinit(p, init_seed, stream);
+}
+
+int fr_sgd_problem_from_edges(int32_t V, int64_t E, int32_t k, const int32_t* u, const int32_t* v,
+                              const float* r, uint64_t init_seed, void* stream, fr_sgd_problem** out) {
+  if (!out) return frcapi::fail(FR_ERR_ARGUMENT, "null problem out");
+  if (V < 1 || E < 0) return frcapi::fail(FR_ERR_VALIDATION, "V >= 1, E >= 0", "V");
+  if (E > 0 && (!u || !v || !r)) return frcapi::fail(FR_ERR_ARGUMENT, "null edge arrays");
+  if (!rank_supported(k)) return frcapi::fail(FR_ERR_UNSUPPORTED, "rank must be 4, 8, 16, 32, 64 or 128");
+  auto s = static_cast<cudaStream_t>(stream);
+  // allocate through the generator with no edges, then take the caller's
+  fr_sgd_problem* p = nullptr;
+  int rc = fr_sgd_problem_generate(V, 0, k, 0, init_seed, stream, &p);
+  if (rc != FR_OK) return rc;
+  p->E = E;
+  cudaError_t e = cudaSuccess;
+  if (E > 0) {
+    for (void* q : {static_cast<void*>(p->u), static_cast<void*>(p->v), static_cast<void*>(p->r)}) cudaFree(q);
+    p->u = p->v = nullptr;
+    p->r = nullptr;
+    e = cudaMalloc(&p->u, size_t(E) * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&p->v, size_t(E) * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&p->r, size_t(E) * 4);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(p->u, u, size_t(E) * 4, cudaMemcpyDefault, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(p->v, v, size_t(E) * 4, cudaMemcpyDefault, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(p->r, r, size_t(E) * 4, cudaMemcpyDefault, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(p->acc, 0, sizeof(double), s);
+  }
+  if (e == cudaSuccess && E > 0) {  // every endpoint in [0, V): count the bad ones on the device
+    int32_t* bad = nullptr;
+    int32_t h_bad = 0;
+    e = cudaMalloc(&bad, sizeof(int32_t));
+    if (e == cudaSuccess) e = cudaMemsetAsync(bad, 0, sizeof(int32_t), s);
+    if (e == cudaSuccess) {
+      sgd_check_ids_kernel<<<grid_for(E, 256, 16), 256, 0, s>>>(p->u, p->v, E, V, bad);
+      e = cudaMemcpyAsync(&h_bad, bad, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (bad) cudaFree(bad);
+    if (e == cudaSuccess && h_bad) {
+      fr_sgd_problem_destroy(p);
+      return frcapi::fail(FR_ERR_VALIDATION, std::to_string(h_bad) + " endpoints outside [0, V)", "edges");
+    }
+  }
+  if (e == cudaSuccess) e = measure_max_degree(p, s);
+  if (e != cudaSuccess) {
+    fr_sgd_problem_destroy(p);
+    return frcapi::cuda_status(e, "sgd problem from edges");
+  }
+  *out = p;
+  return FR_OK;
 }
 
 int fr_sgd_problem_destroy(fr_sgd_problem* p) {

@@ -340,6 +340,27 @@ class SgdProblem:
         self.V, self.E, self.k = Vc.value, Ec.value, kc.value
         self._ptr = dict(u=u.value, v=v.value, r=r.value, L=L.value)
 
+    @classmethod
+    def from_edges(cls, V, u, v, r, k=16, init_seed=3, by_user=False, window=1 << 21, stream=None):
+        """the caller's ratings (u, v, r); by_user re-lays them out like the task"""
+        glib()
+        tu = torch.as_tensor(u, dtype=torch.int32).cuda().contiguous()
+        tv = torch.as_tensor(v, dtype=torch.int32).cuda().contiguous()
+        tr = torch.as_tensor(r, dtype=torch.float32).cuda().contiguous()
+        if not (tu.numel() == tv.numel() == tr.numel()):
+            raise ValueError("u, v, r must have the same length")
+        torch.cuda.synchronize()
+        h = C.c_void_p()
+        n = tu.numel()
+        check(glib().fr_sgd_problem_from_edges(V, n, k, tu.data_ptr() if n else None, tv.data_ptr() if n else None,
+                                               tr.data_ptr() if n else None, init_seed, _stream(stream),
+                                               C.byref(h)))
+        if by_user:
+            check(glib().fr_sgd_group_by_user(h, window, _stream(stream)))
+        p = cls(handle=h)
+        p._owned = True
+        return p
+
     def reinit(self, seed=3, stream=None):
         check(glib().fr_sgd_reinit(self._h, seed, _stream(stream)))
 
