@@ -225,15 +225,39 @@ struct PrArgs {
 // N predicated gathers per lane, `stride` apart: hot sources from shared
 // memory, the rest from L2.  The N values are summed in fp32 (N <= 8 terms,
 // relative error <= N * 2^-24), the caller accumulates these partials in fp64.
+// Predicated loads (no branch): written as C++ `?:` the hot/cold choice
+// compiles to one divergent branch region per element, so each gather issues
+// only after the previous element's branch resolved; as predicated LDS/LDG
+// all 2N loads of a lane issue back to back.
+__device__ __forceinline__ float ld_if_global(const float* p, bool pred) {
+  float v = 0.0f;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.nc.f32 %0, [%1];\n\t}"
+      : "+f"(v) : "l"(p), "r"(static_cast<int>(pred)));
+  return v;
+}
+__device__ __forceinline__ float ld_if_shared(const float* p, bool pred) {
+  float v = 0.0f;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.shared.f32 %0, [%1];\n\t}"
+      : "+f"(v) : "r"(static_cast<unsigned>(__cvta_generic_to_shared(p))), "r"(static_cast<int>(pred)));
+  return v;
+}
+
 template <int N>
 __device__ __forceinline__ double gather(const PrArgs& a, const float* hot, int32_t e, int32_t e1,
                                          int stride) {
   int32_t u[N];
 #pragma unroll
   for (int j = 0; j < N; ++j) u[j] = e + j * stride < e1 ? __ldg(&a.col[e + j * stride]) : -1;
+  float v[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    const bool in = u[j] >= 0, h = u[j] < a.hot;
+    const int32_t x = in ? u[j] : 0;
+    v[j] = ld_if_shared(hot + (h ? x : 0), in && h) + ld_if_global(a.c_in + x, in && !h);
+  }
   float s = 0.0f;
 #pragma unroll
-  for (int j = 0; j < N; ++j) s += u[j] < 0 ? 0.0f : (u[j] < a.hot ? hot[u[j]] : __ldg(&a.c_in[u[j]]));
+  for (int j = 0; j < N; ++j) s += v[j];
   return static_cast<double>(s);
 }
 
@@ -295,8 +319,11 @@ __device__ __forceinline__ double group_sum(double s, int lanes) {
 //      static round-robin over all warps (items are ordered heavy first and
 //      carry ~64..256 edges each);
 //  (3) the zero-in-degree tail, when asked.
+// Registers (MINB CTAs of kPrThreads resident, and at 1024 x 1 room for the
+// stage's 1-warp dependency-wait kernel inside a bubble: 56, allocated 8 at a
+// time; 768 x 2: 40).
 template <int kPrThreads, int MINB>
-__global__ void __launch_bounds__(kPrThreads, MINB) pr_pull_kernel(PrArgs a) {
+__global__ void __maxnreg__(kPrThreads >= 1024 ? 56 : 40) pr_pull_kernel(PrArgs a) {
   constexpr int kPrWarps = kPrThreads / 32;
   extern __shared__ float4 hot4[];
   __shared__ double sacc[kMaxSlots];
