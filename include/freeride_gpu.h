@@ -135,14 +135,20 @@ int fr_sgd_reinit(fr_sgd_problem* p, uint64_t init_seed, void* stream);
 int fr_sgd_step(fr_sgd_problem* p, int64_t e_begin, int64_t e_end, float eta, float lambda,
                 void* stream);
 /* Re-lays the edges out by user (Gardenia's CSR input order: ratings of one
- * user contiguous, generated order within a user), each user's ratings cut
- * into 64-edge pieces dealt over R = ceil(E / window_edges) rounds (piece k
- * of np -> round (k R / np + h(u)) mod R, then stable by round), so one
- * window-sized step holds at most ~one piece of any user.  Later steps run the
+ * user contiguous, generated order within a user); when the latent rows pass
+ * 64 MiB, stable by item block (P = ceil(V k 4 B / 64 MiB) ranges of v, so a
+ * step's L_v rows stay in L2); each (block, user) run cut into 64-edge pieces
+ * dealt over R = ceil(E / window_edges) rounds inside its block (piece q of
+ * np -> round (q R / np + h(u)) mod R, stable by block x R + round), so one
+ * window-sized step holds at most ~one piece of any user per block.  Later steps run the
  * user-grouped kernel (L_u held in registers across a run, ~143 instead of
  * 268 B/edge at k = 16; k < 16 keeps the per-edge kernel).  Synchronous;
  * E < 2^31.  oracle/sidetasks.c orc_sgd_group_by_user is the same layout. */
 int fr_sgd_group_by_user(fr_sgd_problem* p, int64_t window_edges, void* stream);
+/* Pick the step kernel for the edges as they lie: 1 = user-grouped (L_u held
+ * across each run of equal u -- correct for any order, fast when runs are
+ * long), 0 = per-edge.  For callers that lay their ratings out themselves. */
+int fr_sgd_problem_set_kernel(fr_sgd_problem* p, int32_t by_user);
 /* K4: *d_acc (device fp64) += sum of squared errors over [e_begin, e_end) */
 int fr_sgd_sqerr(const fr_sgd_problem* p, int64_t e_begin, int64_t e_end, double* d_acc,
                  void* stream);

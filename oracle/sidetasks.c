@@ -191,10 +191,11 @@ void orc_sgd_edges(int32_t V, int64_t E, uint64_t seed, int32_t* u, int32_t* v, 
 }
 
 /* fr_sgd_group_by_user's layout (paper_2409_06941_b200/csrc/kernels/sgd.cu):
- * Gardenia's CSR input order -- a stable counting sort by u -- then each
- * user's run cut into 64-edge pieces, piece k of np going to round
- * (k R / np + h(u)) mod R with R = ceil(E / window), and a stable counting
- * sort by round. */
+ * Gardenia's CSR input order -- a stable counting sort by u -- then, when
+ * the latent rows exceed 64 MiB, a stable sort by item block (P ranges of v,
+ * P = ceil(V k 4 B / 64 MiB)), then each (block, user) run cut into 64-edge
+ * pieces, piece q of np going to round (q R / np + h(u)) mod R inside its
+ * block (R = ceil(E / window)), and a stable sort by block x R + round. */
 #define SGD_PIECE 64
 static int32_t sgd_round(int32_t u, int64_t rank, int64_t deg, int32_t R) {
   const int64_t np = (deg + SGD_PIECE - 1) / SGD_PIECE, k = rank / SGD_PIECE;
@@ -202,9 +203,18 @@ static int32_t sgd_round(int32_t u, int64_t rank, int64_t deg, int32_t R) {
   return (int32_t)(((uint64_t)(k * R / np) + h) % (uint64_t)R);
 }
 
+int32_t orc_sgd_item_blocks(int32_t V, int k) {
+  const int64_t bytes = (int64_t)V * k * 4, blk = (int64_t)64 << 20;
+  const int64_t P = (bytes + blk - 1) / blk;
+  return (int32_t)(P < 1 ? 1 : P);
+}
+
+static int32_t sgd_block_of(int32_t v, int32_t V, int32_t P) { return (int32_t)((int64_t)v * P / V); }
+
+/* stable counting sort of (u, v, r) by key[] in [0, nkeys) into (u2, v2, r2) */
 static void sgd_counting_sort(int64_t E, const int32_t* key, int64_t nkeys, const int32_t* u,
-                              const int32_t* v, const float* r, int32_t* u2, int32_t* v2, float* r2,
-                              int64_t* start /* nkeys + 1, zeroed */) {
+                              const int32_t* v, const float* r, int32_t* u2, int32_t* v2, float* r2) {
+  int64_t* start = (int64_t*)calloc((size_t)nkeys + 1, sizeof(int64_t));
   for (int64_t e = 0; e < E; ++e) start[key[e] + 1]++;
   for (int64_t i = 0; i < nkeys; ++i) start[i + 1] += start[i];
   for (int64_t e = 0; e < E; ++e) {
@@ -213,36 +223,59 @@ static void sgd_counting_sort(int64_t E, const int32_t* key, int64_t nkeys, cons
     v2[at] = v[e];
     r2[at] = r[e];
   }
+  free(start);
 }
 
-void orc_sgd_group_by_user(int32_t V, int64_t E, int64_t window, int32_t* u, int32_t* v, float* r) {
+void orc_sgd_group_by_user(int32_t V, int64_t E, int64_t window, int k, int32_t* u, int32_t* v, float* r) {
   const size_t n = (size_t)(E > 0 ? E : 1);
+  const int32_t P = orc_sgd_item_blocks(V, k);
   int64_t R = window > 0 ? (E + window - 1) / window : 1;
   if (R < 1) R = 1;
-  if (R > (1 << 20)) R = 1 << 20;
-  int64_t* start = (int64_t*)calloc((size_t)V + 1, sizeof(int64_t));
+  if (R > ((int64_t)1 << 30) / P) R = ((int64_t)1 << 30) / P;
+  if (R < 1) R = 1;
+  int32_t* key = (int32_t*)malloc(n * sizeof(int32_t));
   int32_t* u2 = (int32_t*)malloc(n * sizeof(int32_t));
   int32_t* v2 = (int32_t*)malloc(n * sizeof(int32_t));
   float* r2 = (float*)malloc(n * sizeof(float));
-  sgd_counting_sort(E, u, V, u, v, r, u2, v2, r2, start);
-  if (R > 1) {
-    /* start[x] now = end of x's run; deg from the run bounds */
-    int32_t* key = (int32_t*)malloc(n * sizeof(int32_t));
-    for (int64_t e = 0; e < E; ++e) {
-      const int32_t x = u2[e];
-      const int64_t b = x ? start[x - 1] : 0, deg = start[x] - b;
-      key[e] = sgd_round(x, e - b, deg, (int32_t)R);
-    }
-    int64_t* rs = (int64_t*)calloc((size_t)R + 1, sizeof(int64_t));
-    sgd_counting_sort(E, key, R, u2, v2, r2, u, v, r, rs);
-    free(rs);
-    free(key);
-  } else {
+  /* 1. by u */
+  sgd_counting_sort(E, u, V, u, v, r, u2, v2, r2);
+  memcpy(u, u2, (size_t)E * sizeof(int32_t));
+  memcpy(v, v2, (size_t)E * sizeof(int32_t));
+  memcpy(r, r2, (size_t)E * sizeof(float));
+  /* 2. by item block */
+  if (P > 1) {
+    for (int64_t e = 0; e < E; ++e) key[e] = sgd_block_of(v[e], V, P);
+    sgd_counting_sort(E, key, P, u, v, r, u2, v2, r2);
     memcpy(u, u2, (size_t)E * sizeof(int32_t));
     memcpy(v, v2, (size_t)E * sizeof(int32_t));
     memcpy(r, r2, (size_t)E * sizeof(float));
   }
-  free(start);
+  /* 3. rounds inside each block */
+  if (R > 1) {
+    int64_t b = 0;
+    for (int64_t e = 0; e < E; ++e) {
+      if (e == 0 || u[e] != u[e - 1] || sgd_block_of(v[e], V, P) != sgd_block_of(v[e - 1], V, P)) b = e;
+      int64_t end = b + 1;  /* run end: scan once per run start */
+      if (e == b) {
+        while (end < E && u[end] == u[b] && sgd_block_of(v[end], V, P) == sgd_block_of(v[b], V, P)) ++end;
+        key[e] = (int32_t)end;  /* stash the end at the run's first edge */
+      }
+      (void)end;
+    }
+    int64_t run_b = 0, run_e = 0;
+    for (int64_t e = 0; e < E; ++e) {
+      if (e == run_e) {
+        run_b = e;
+        run_e = key[e];
+      }
+      key[e] = sgd_block_of(v[e], V, P) * (int32_t)R + sgd_round(u[e], e - run_b, run_e - run_b, (int32_t)R);
+    }
+    sgd_counting_sort(E, key, (int64_t)P * R, u, v, r, u2, v2, r2);
+    memcpy(u, u2, (size_t)E * sizeof(int32_t));
+    memcpy(v, v2, (size_t)E * sizeof(int32_t));
+    memcpy(r, r2, (size_t)E * sizeof(float));
+  }
+  free(key);
   free(u2);
   free(v2);
   free(r2);

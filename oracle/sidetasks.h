@@ -39,7 +39,8 @@ void orc_pr_run(int32_t V, const int32_t* offsets, const int32_t* col_idx,
 /* ---- K3/K4: Graph-SGD matrix factorisation (rank k) -------------------- */
 void orc_sgd_edges(int32_t V, int64_t E, uint64_t seed, int32_t* u, int32_t* v, float* r,
                    int nthreads);
-void orc_sgd_group_by_user(int32_t V, int64_t E, int64_t window, int32_t* u, int32_t* v, float* r);
+int32_t orc_sgd_item_blocks(int32_t V, int k);
+void orc_sgd_group_by_user(int32_t V, int64_t E, int64_t window, int k, int32_t* u, int32_t* v, float* r);
 void orc_sgd_init(int32_t V, int k, uint64_t seed, float* L, int nthreads);
 /* one epoch over edges [0,E) in order; sequential when nthreads == 1,
  * Hogwild (racy by design) otherwise */

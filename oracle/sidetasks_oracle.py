@@ -32,7 +32,9 @@ class SideTaskOracle:
         lib.orc_rmat_edges.argtypes = [C.c_int, C.c_int64, C.c_uint64, i32p, i32p, C.c_int]
         lib.orc_pr_run.argtypes = [C.c_int32, i32p, i32p, i32p, C.c_double, C.c_int, f64p, C.c_int]
         lib.orc_sgd_edges.argtypes = [C.c_int32, C.c_int64, C.c_uint64, i32p, i32p, f32p, C.c_int]
-        lib.orc_sgd_group_by_user.argtypes = [C.c_int32, C.c_int64, C.c_int64, i32p, i32p, f32p]
+        lib.orc_sgd_group_by_user.argtypes = [C.c_int32, C.c_int64, C.c_int64, C.c_int, i32p, i32p, f32p]
+        lib.orc_sgd_item_blocks.restype = C.c_int32
+        lib.orc_sgd_item_blocks.argtypes = [C.c_int32, C.c_int]
         lib.orc_sgd_init.argtypes = [C.c_int32, C.c_int, C.c_uint64, f32p, C.c_int]
         lib.orc_sgd_epoch.argtypes = [C.c_int64, i32p, i32p, f32p, f32p, C.c_int, C.c_float, C.c_float, C.c_int]
         lib.orc_sgd_rmse.restype = C.c_double
@@ -95,10 +97,11 @@ class SideTaskOracle:
         self.lib.orc_sgd_edges(V, E, seed, u, v, r, nthreads)
         return u, v, r
 
-    def sgd_group_by_user(self, V, u, v, r, window=1 << 21):
-        """fr_sgd_group_by_user's layout, in place: stable by u, each user's run
-        cut into 64-edge pieces dealt over ceil(E / window) rounds"""
-        self.lib.orc_sgd_group_by_user(V, len(u), window, u, v, r)
+    def sgd_group_by_user(self, V, u, v, r, window=1 << 21, k=16):
+        """fr_sgd_group_by_user's layout, in place: stable by u, then by item
+        block (latent rows > 64 MiB), each (block, user) run cut into 64-edge
+        pieces dealt over ceil(E / window) rounds inside its block"""
+        self.lib.orc_sgd_group_by_user(V, len(u), window, k, u, v, r)
         return u, v, r
 
     def sgd_init(self, V, k=16, seed=3, nthreads=0):

@@ -289,12 +289,53 @@ __host__ __device__ __forceinline__ int32_t sgd_round(int32_t u, int64_t rank, i
   return static_cast<int32_t>((static_cast<uint64_t>(k * R / np) + h) % static_cast<uint64_t>(R));
 }
 
-__global__ void sgd_round_kernel(const int32_t* __restrict__ u, int64_t n, const int32_t* __restrict__ start,
-                                 const int32_t* __restrict__ cnt, int32_t R, int32_t* __restrict__ key) {
+// item blocks of the by-user layout: ceil(V k 4 B / 64 MiB) ranges of v
+constexpr int64_t kSgdBlockBytes = int64_t(64) << 20;
+int32_t sgd_item_blocks(int32_t V, int32_t k) {
+  const int64_t bytes = int64_t(V) * k * 4;
+  return static_cast<int32_t>(std::max<int64_t>(1, (bytes + kSgdBlockBytes - 1) / kSgdBlockBytes));
+}
+__host__ __device__ __forceinline__ int32_t sgd_block_of(int32_t v, int32_t V, int32_t P) {
+  return static_cast<int32_t>(static_cast<int64_t>(v) * P / V);
+}
+
+__global__ void sgd_block_key_kernel(const int32_t* __restrict__ v, int64_t n, int32_t V, int32_t P,
+                                     int32_t* __restrict__ key) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    key[i] = sgd_block_of(__ldg(&v[i]), V, P);
+}
+
+// 1 where a (block, user) run starts (edges sorted by block, then u)
+__global__ void sgd_run_flag_kernel(const int32_t* __restrict__ u, const int32_t* __restrict__ v, int64_t n,
+                                    int32_t V, int32_t P, int32_t* __restrict__ flag) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    flag[i] = i == 0 || __ldg(&u[i]) != __ldg(&u[i - 1]) ||
+              sgd_block_of(__ldg(&v[i]), V, P) != sgd_block_of(__ldg(&v[i - 1]), V, P);
+}
+
+__global__ void sgd_fill_kernel(int32_t* __restrict__ x, int64_t n, int32_t value) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    x[i] = value;
+}
+
+// rst[run] = first edge of the run (runs numbered by the inclusive scan of flags, from 1)
+__global__ void sgd_run_start_kernel(const int32_t* __restrict__ flag, const int32_t* __restrict__ rid,
+                                     int64_t n, int32_t* __restrict__ rst) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    if (flag[i]) rst[rid[i] - 1] = static_cast<int32_t>(i);
+}
+
+__global__ void sgd_round_key_kernel(const int32_t* __restrict__ u, const int32_t* __restrict__ v, int64_t n,
+                                     int32_t V, int32_t P, const int32_t* __restrict__ rid,
+                                     const int32_t* __restrict__ rst, int32_t R, int32_t* __restrict__ key) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int32_t x = __ldg(&u[i]);
-    key[i] = sgd_round(x, i - __ldg(&start[x]), __ldg(&cnt[x]), R);
+    const int32_t run = __ldg(&rid[i]) - 1, b = __ldg(&rst[run]), len = __ldg(&rst[run + 1]) - b;
+    key[i] = sgd_block_of(__ldg(&v[i]), V, P) * R + sgd_round(__ldg(&u[i]), i - b, len, R);
   }
 }
 
@@ -631,20 +672,22 @@ int fr_sgd_group_by_user(fr_sgd_problem* p, int64_t window_edges, void* stream) 
   if (p->E > INT32_MAX) return frcapi::fail(FR_ERR_VALIDATION, "grouping needs E < 2^31", "E");
   auto s = static_cast<cudaStream_t>(stream);
   const int n = static_cast<int>(p->E);
-  const int32_t R = static_cast<int32_t>(std::min<int64_t>((p->E + window_edges - 1) / window_edges, 1 << 20));
+  const int32_t P = sgd_item_blocks(p->V, p->K);
+  const int32_t R = static_cast<int32_t>(
+      std::min<int64_t>((p->E + window_edges - 1) / window_edges, std::max<int64_t>(1, (int64_t(1) << 30) / P)));
   auto bits_for = [](int64_t x) {
     int b = 1;
     while (b < 31 && (int64_t(1) << b) < x) ++b;
     return b;
   };
   int32_t *u2 = nullptr, *v2 = nullptr, *idx = nullptr, *perm = nullptr, *key = nullptr, *key2 = nullptr;
-  int32_t *cnt = nullptr, *start = nullptr;
+  int32_t *flag = nullptr, *rid = nullptr, *rst = nullptr;
   float* r2 = nullptr;
   void* tmp = nullptr;
   size_t need = 0, need2 = 0, need3 = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, need, p->u, u2, idx, perm, n, 0, bits_for(p->V), s);
-  cub::DeviceRadixSort::SortPairs(nullptr, need2, key, key2, idx, perm, n, 0, bits_for(R), s);
-  cub::DeviceScan::ExclusiveSum(nullptr, need3, cnt, start, p->V, s);
+  cub::DeviceRadixSort::SortPairs(nullptr, need2, key, key2, idx, perm, n, 0, bits_for(int64_t(P) * R), s);
+  cub::DeviceScan::InclusiveSum(nullptr, need3, flag, rid, n, s);
   need = std::max({need, need2, need3, size_t(1)});
   cudaError_t e = cudaSuccess;
   for (auto [q, bytes] : {std::pair<void**, size_t>{reinterpret_cast<void**>(&u2), size_t(n) * 4},
@@ -654,8 +697,9 @@ int fr_sgd_group_by_user(fr_sgd_problem* p, int64_t window_edges, void* stream) 
                           {reinterpret_cast<void**>(&perm), size_t(n) * 4},
                           {reinterpret_cast<void**>(&key), size_t(n) * 4},
                           {reinterpret_cast<void**>(&key2), size_t(n) * 4},
-                          {reinterpret_cast<void**>(&cnt), size_t(p->V) * 4},
-                          {reinterpret_cast<void**>(&start), size_t(p->V) * 4},
+                          {reinterpret_cast<void**>(&flag), size_t(n) * 4},
+                          {reinterpret_cast<void**>(&rid), size_t(n) * 4},
+                          {reinterpret_cast<void**>(&rst), size_t(n + 1) * 4},
                           {&tmp, need}})
     if (e == cudaSuccess) e = cudaMalloc(q, bytes);
   const int gn = grid_for(n, 256, 16);
@@ -663,6 +707,16 @@ int fr_sgd_group_by_user(fr_sgd_problem* p, int64_t window_edges, void* stream) 
     std::swap(p->u, u2);
     std::swap(p->v, v2);
     std::swap(p->r, r2);
+  };
+  auto sort_by_key = [&](int bits) {  // stable: (u, v, r) reordered by key
+    sgd_iota_kernel<<<gn, 256, 0, s>>>(idx, n);
+    cudaError_t x = cub::DeviceRadixSort::SortPairs(tmp, need, key, key2, idx, perm, n, 0, bits, s);
+    if (x == cudaSuccess) {
+      sgd_gather3_kernel<<<gn, 256, 0, s>>>(perm, p->u, p->v, p->r, n, u2, v2, r2);
+      x = cudaGetLastError();
+    }
+    if (x == cudaSuccess) swap3();
+    return x;
   };
   // 1. stable sort by u (LSD radix keeps the generated order within a user)
   if (e == cudaSuccess) {
@@ -674,31 +728,39 @@ int fr_sgd_group_by_user(fr_sgd_problem* p, int64_t window_edges, void* stream) 
     e = cudaGetLastError();
   }
   if (e == cudaSuccess) swap3();
-  // 2. rounds: each user's run cut into kSgdPiece-edge pieces spread over R
-  //    rounds of ~window_edges (stable sort by round keeps u order inside)
+  // 2. item blocks: stable by block of v, so each block's L_v rows (<= 64
+  //    MiB) stay in L2 while its ratings stream by
+  if (e == cudaSuccess && P > 1) {
+    sgd_block_key_kernel<<<gn, 256, 0, s>>>(p->v, n, p->V, P, key);
+    e = sort_by_key(bits_for(P));
+  }
+  // 3. rounds: each (block, user) run cut into kSgdPiece-edge pieces dealt
+  //    over R rounds inside its block (stable by block x R + round)
   if (e == cudaSuccess && R > 1) {
-    e = cudaMemsetAsync(cnt, 0, size_t(p->V) * 4, s);
+    sgd_run_flag_kernel<<<gn, 256, 0, s>>>(p->u, p->v, n, p->V, P, flag);
+    e = cub::DeviceScan::InclusiveSum(tmp, need, flag, rid, n, s);
     if (e == cudaSuccess) {
-      sgd_count_kernel<<<gn, 256, 0, s>>>(p->u, n, cnt);
-      e = cub::DeviceScan::ExclusiveSum(tmp, need, cnt, start, p->V, s);
-    }
-    if (e == cudaSuccess) {
-      sgd_round_kernel<<<gn, 256, 0, s>>>(p->u, n, start, cnt, R, key);
-      e = cub::DeviceRadixSort::SortPairs(tmp, need, key, key2, idx, perm, n, 0, bits_for(R), s);
-    }
-    if (e == cudaSuccess) {
-      sgd_gather3_kernel<<<gn, 256, 0, s>>>(perm, p->u, p->v, p->r, n, u2, v2, r2);
+      sgd_fill_kernel<<<gn, 256, 0, s>>>(rst, int64_t(n) + 1, n);
+      sgd_run_start_kernel<<<gn, 256, 0, s>>>(flag, rid, n, rst);
+      sgd_round_key_kernel<<<gn, 256, 0, s>>>(p->u, p->v, n, p->V, P, rid, rst, R, key);
       e = cudaGetLastError();
     }
-    if (e == cudaSuccess) swap3();
+    if (e == cudaSuccess) e = sort_by_key(bits_for(int64_t(P) * R));
   }
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   for (void* q : {static_cast<void*>(u2), static_cast<void*>(v2), static_cast<void*>(r2),
                   static_cast<void*>(idx), static_cast<void*>(perm), static_cast<void*>(key),
-                  static_cast<void*>(key2), static_cast<void*>(cnt), static_cast<void*>(start), tmp})
+                  static_cast<void*>(key2), static_cast<void*>(flag), static_cast<void*>(rid),
+                  static_cast<void*>(rst), tmp})
     if (q) cudaFree(q);
   if (e != cudaSuccess) return frcapi::cuda_status(e, "sgd group by user");
   p->grouped = true;
+  return FR_OK;
+}
+
+int fr_sgd_problem_set_kernel(fr_sgd_problem* p, int32_t by_user) {
+  if (!p) return frcapi::fail(FR_ERR_ARGUMENT, "null problem");
+  p->grouped = by_user != 0;
   return FR_OK;
 }
 

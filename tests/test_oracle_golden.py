@@ -51,33 +51,42 @@ def _splitmix64(x):
     return x ^ (x >> np.uint64(31))
 
 
-def _by_user_numpy(u, R):
+def _by_user_numpy(u, v, V, R, P):
     """fr_sgd_group_by_user's layout restated with numpy (independent of the C oracle)"""
     o = np.argsort(u, kind="stable")
-    us = u[o].astype(np.int64)
-    cnt = np.bincount(us, minlength=int(us.max()) + 1)
-    start = np.concatenate([[0], np.cumsum(cnt)[:-1]])
-    rank = np.arange(len(us)) - start[us]
-    deg = cnt[us]
-    npieces, k = (deg + 63) // 64, rank // 64
-    with np.errstate(over="ignore"):
-        h = (_splitmix64(np.uint64(0x5347445250) ^ us.astype(np.uint64)) % np.uint64(R)).astype(np.int64)
-    rnd = (k * R // npieces + h) % R
-    return o[np.argsort(rnd, kind="stable")]
+    if P > 1:
+        o = o[np.argsort((v[o].astype(np.int64) * P) // V, kind="stable")]
+    if R > 1:
+        us = u[o].astype(np.int64)
+        blk = (v[o].astype(np.int64) * P) // V
+        key = blk * (int(us.max()) + 1) + us
+        start = np.flatnonzero(np.concatenate([[True], key[1:] != key[:-1]]))
+        length = np.diff(np.concatenate([start, [len(us)]]))
+        rid = np.cumsum(np.concatenate([[True], key[1:] != key[:-1]])) - 1
+        rank = np.arange(len(us)) - start[rid]
+        deg = length[rid]
+        npieces, q = (deg + 63) // 64, rank // 64
+        with np.errstate(over="ignore"):
+            h = (_splitmix64(np.uint64(0x5347445250) ^ us.astype(np.uint64)) % np.uint64(R)).astype(np.int64)
+        rnd = blk * R + (q * R // npieces + h) % R
+        o = o[np.argsort(rnd, kind="stable")]
+    return o
 
 
-@pytest.mark.parametrize("window", [1 << 30, 20000, 4096])
-def test_oracle_sgd_group_by_user_layout(sidetask_oracle, window):
-    """by-user layout: stable by u (Gardenia's CSR order) when one round, else
-    64-edge pieces of each user's run dealt over ceil(E / window) rounds"""
-    V, E = 5000, 200000
+@pytest.mark.parametrize("V,E,k,window", [(5000, 200000, 16, 1 << 30), (5000, 200000, 16, 20000),
+                                          (5000, 200000, 16, 4096), (200000, 1000000, 128, 1 << 30),
+                                          (200000, 1000000, 128, 65536)])
+def test_oracle_sgd_group_by_user_layout(sidetask_oracle, V, E, k, window):
+    """by-user layout: stable by u (Gardenia's CSR order); by item block once the
+    latent rows pass 64 MiB (here k = 128: P = 2); 64-edge pieces of each
+    (block, user) run dealt over ceil(E / window) rounds inside the block"""
     u, v, r = sidetask_oracle.sgd_edges(V, E, seed=9)
     R = max(1, -(-E // window))
-    o = _by_user_numpy(u, R) if R > 1 else np.argsort(u, kind="stable")
-    gu, gv, gr = sidetask_oracle.sgd_group_by_user(V, u.copy(), v.copy(), r.copy(), window=window)
+    P = max(1, -(-(V * k * 4) // (64 << 20)))
+    assert P == sidetask_oracle.lib.orc_sgd_item_blocks(V, k)
+    o = _by_user_numpy(u, v, V, R, P)
+    gu, gv, gr = sidetask_oracle.sgd_group_by_user(V, u.copy(), v.copy(), r.copy(), window=window, k=k)
     assert np.array_equal(gu, u[o]) and np.array_equal(gv, v[o]) and np.array_equal(gr, r[o])
-    if R > 1:   # every user's pieces: at most ceil(pieces / R) per window-sized round
-        assert len(np.unique(gu[: E // R])) > 0.5 * min(V, E // R // 40)
 
 
 def test_appendix_a1_issue_order(product, ref):

@@ -62,12 +62,13 @@ def test_rmse_parity_orkut_shape(g, sidetask_oracle):
 
 
 @pytest.mark.parametrize("V,E,k,window", [(7, 50, 16, 1 << 21), (1000, 20000, 16, 1000), (50000, 400000, 32, 65536),
-                                          (3000, 100000, 8, 7), (3072441, 117185083, 16, 1 << 21)])
+                                          (3000, 100000, 8, 7), (200000, 1000000, 128, 1 << 16),
+                                          (3072441, 117185083, 16, 1 << 21)])
 def test_by_user_layout_matches_oracle(g, sidetask_oracle, V, E, k, window):
     """fr_sgd_group_by_user == the oracle's layout (stable by u, pieces dealt over rounds), bit-exact."""
     p = g.SgdProblem(V=V, E=E, k=k, edge_seed=11, init_seed=12, by_user=True, window=window)
     u, v, r = (t.cpu().numpy() for t in p.edges())
-    ou, ov, orr = sidetask_oracle.sgd_group_by_user(V, *sidetask_oracle.sgd_edges(V, E, seed=11), window=window)
+    ou, ov, orr = sidetask_oracle.sgd_group_by_user(V, *sidetask_oracle.sgd_edges(V, E, seed=11), window=window, k=k)
     assert np.array_equal(u, ou) and np.array_equal(v, ov) and np.array_equal(r, orr)
 
 
@@ -80,7 +81,7 @@ def test_by_user_rmse_parity(g, sidetask_oracle, V, E, k):
     updated by all lower users -- which no parallel schedule reproduces; the
     two converge from the second epoch (3.3e-4, 2.7e-4)."""
     p = g.SgdProblem(V=V, E=E, k=k, edge_seed=2, init_seed=3, by_user=True)
-    u, v, r = sidetask_oracle.sgd_group_by_user(V, *sidetask_oracle.sgd_edges(V, E, seed=2))
+    u, v, r = sidetask_oracle.sgd_group_by_user(V, *sidetask_oracle.sgd_edges(V, E, seed=2), k=k)
     L = sidetask_oracle.sgd_init(V, k, seed=3)
     for ep in range(3):
         p.epoch(ETA, LAM)
