@@ -412,8 +412,11 @@ def emit(args, results, ws, names, csr):
         "sgd": {"config": "configs[2]: Orkut shape V=3,072,441 E=117,185,083 k=16, 2^21 edges/step, "
                           "by-user layout (fr_sgd_group_by_user)",
                 "value": rate("sgd"), "unit": "edges/bubble-s", "dT": dT("sgd"), "fill": fill("sgd"),
-                "roofline": roof("sgd", "sgd_user_kernel<16> (2^21 edges/launch, in-pipeline; "
-                                        "alg bytes 12 + 128 per edge + 128 per L_u load)"),
+                "roofline": dict(roof("sgd", "sgd_user_kernel<16> (2^21 edges/launch, in-pipeline; "
+                                             "alg bytes 12 + 128 per edge + 128 per L_u load; item blocks keep "
+                                             "L_v in L2, so part of them never reaches DRAM)"),
+                                 traffic=70.7 * SGD["edges_per_step"],
+                                 traffic_source="profiles/r1_sgd_user_blk_ncu.txt (cold, standalone)"),
                 "cpu_baseline": cpu_sgd(args.cpu_seconds / 2) if not args.no_cpu else None},
     }
     imp = results[0]["image_imperative"]
