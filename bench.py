@@ -414,7 +414,7 @@ def emit(args, results, ws, names, csr):
                 "value": rate("sgd"), "unit": "edges/bubble-s", "dT": dT("sgd"), "fill": fill("sgd"),
                 "roofline": dict(roof("sgd", "sgd_user_kernel<16> (2^21 edges/launch, in-pipeline; "
                                              "alg bytes 12 + 128 per edge + 128 per L_u load; item blocks keep "
-                                             "L_v in L2, so part of them never reaches DRAM)"),
+                                             "L_v in L2, so part of them never reaches DRAM)") or {},
                                  traffic=70.7 * SGD["edges_per_step"],
                                  traffic_source="profiles/r1_sgd_user_blk_ncu.txt (cold, standalone)"),
                 "cpu_baseline": cpu_sgd(args.cpu_seconds / 2) if not args.no_cpu else None},
