@@ -243,11 +243,13 @@ __device__ __forceinline__ float ld_if_shared(const float* p, bool pred) {
 }
 
 template <int N>
-__device__ __forceinline__ double gather(const PrArgs& a, const float* hot, int32_t e, int32_t e1,
-                                         int stride) {
-  int32_t u[N];
+__device__ __forceinline__ void load_cols(const PrArgs& a, int32_t e, int32_t e1, int stride, int32_t (&u)[N]) {
 #pragma unroll
   for (int j = 0; j < N; ++j) u[j] = e + j * stride < e1 ? __ldg(&a.col[e + j * stride]) : -1;
+}
+
+template <int N>
+__device__ __forceinline__ double gather_cols(const PrArgs& a, const float* hot, const int32_t (&u)[N]) {
   float v[N];
 #pragma unroll
   for (int j = 0; j < N; ++j) {
@@ -261,6 +263,14 @@ __device__ __forceinline__ double gather(const PrArgs& a, const float* hot, int3
   return static_cast<double>(s);
 }
 
+template <int N>
+__device__ __forceinline__ double gather(const PrArgs& a, const float* hot, int32_t e, int32_t e1,
+                                         int stride) {
+  int32_t u[N];
+  load_cols<N>(a, e, e1, stride, u);
+  return gather_cols<N>(a, hot, u);
+}
+
 // A bucket item as seen by one lane: its row, edge range and the row's
 // output metadata, all loaded up front (one round trip).
 struct Item {
@@ -268,6 +278,7 @@ struct Item {
   float inv;
   int lanes;
   bool emit;
+  int32_t u0[4];  // the first 4 column ids of this lane (loaded with the item)
 };
 
 __device__ __forceinline__ Item prep(const PrArgs& a, int it, bool valid, int lane) {
@@ -295,6 +306,9 @@ __device__ __forceinline__ Item prep(const PrArgs& a, int it, bool valid, int la
   }
   return x;
 }
+
+// the item's first column ids, once its offsets are in (one item ahead)
+__device__ __forceinline__ void prep_cols(const PrArgs& a, Item& x) { load_cols<4>(a, x.e, x.e1, x.lanes, x.u0); }
 
 __device__ __forceinline__ void store(const PrArgs& a, int32_t rr, int32_t rc, float inv, double s) {
   const float rv = static_cast<float>(a.base + a.damp * s);
@@ -359,14 +373,19 @@ __global__ void __maxnreg__(kPrThreads >= 1024 ? 56 : 40) pr_pull_kernel(PrArgs 
   // software-pipelined: the next pair's offsets and output metadata load
   // while this pair gathers
   Item x = prep(a, gw, gw < n, lane), y = prep(a, gw + nw, gw + nw < n, lane);
+  prep_cols(a, x);
+  prep_cols(a, y);
   for (int it = gw; it < n; it += 2 * nw) {
     const int nx = it + 2 * nw;
-    const Item px = prep(a, nx, nx < n, lane), py = prep(a, nx + nw, nx + nw < n, lane);
-    double sx = 0.0, sy = 0.0;
-    for (int32_t ex = x.e, ey = y.e; ex < x.e1 || ey < y.e1; ex += 4 * x.lanes, ey += 4 * y.lanes) {
+    Item px = prep(a, nx, nx < n, lane), py = prep(a, nx + nw, nx + nw < n, lane);
+    double sx = gather_cols<4>(a, hot, x.u0), sy = gather_cols<4>(a, hot, y.u0);
+    for (int32_t ex = x.e + 4 * x.lanes, ey = y.e + 4 * y.lanes; ex < x.e1 || ey < y.e1;
+         ex += 4 * x.lanes, ey += 4 * y.lanes) {
       sx += gather<4>(a, hot, ex, x.e1, x.lanes);
       sy += gather<4>(a, hot, ey, y.e1, y.lanes);
     }
+    prep_cols(a, px);  // next pair's first columns: in flight while this pair's sums and stores finish
+    prep_cols(a, py);
     sx = group_sum(sx, x.lanes);
     sy = group_sum(sy, y.lanes);
     if (x.emit) store(a, x.rr, x.rc, x.inv, sx);
