@@ -353,10 +353,19 @@ __global__ void __maxnreg__(kPrThreads >= 1024 ? 56 : 40) pr_pull_kernel(PrArgs 
     }
   }
   __syncthreads();
-  for (int c = a.cta_chunk[blockIdx.x] + warp; c < a.cta_chunk[blockIdx.x + 1]; c += kPrWarps) {
-    const int4 ch = __ldg(&a.chunks[c]);
-    double s = 0.0;
-    for (int32_t e = ch.y + lane; e < ch.z; e += 256) s += gather<8>(a, hot, e, ch.z, 32);
+  // split-row chunks, software-pipelined: the next chunk's descriptor and
+  // first 8 column ids per lane load while this chunk gathers
+  const int c_end = a.cta_chunk[blockIdx.x + 1];
+  int c = a.cta_chunk[blockIdx.x] + warp;
+  int4 ch = c < c_end ? __ldg(&a.chunks[c]) : make_int4(0, 0, 0, 0);
+  int32_t cu[8];
+  load_cols<8>(a, ch.y + lane, ch.z, 32, cu);
+  for (; c < c_end; c += kPrWarps) {
+    const int cn = c + kPrWarps;
+    const int4 chn = cn < c_end ? __ldg(&a.chunks[cn]) : make_int4(0, 0, 0, 0);
+    double s = gather_cols<8>(a, hot, cu);
+    for (int32_t e = ch.y + lane + 256; e < ch.z; e += 256) s += gather<8>(a, hot, e, ch.z, 32);
+    load_cols<8>(a, chn.y + lane, chn.z, 32, cu);
     s = group_sum(s, 32);
     if (lane == 0) {
       const int slot = ch.w & 0xFF, need = ch.w >> 8;
@@ -368,6 +377,7 @@ __global__ void __maxnreg__(kPrThreads >= 1024 ? 56 : 40) pr_pull_kernel(PrArgs 
         store(a, ch.x, __ldg(&a.rowc[ch.x]), __ldg(&a.rinv[ch.x]), tot);
       }
     }
+    ch = chn;
   }
   const int nw = gridDim.x * kPrWarps, gw = blockIdx.x * kPrWarps + warp, n = a.istart[0];
   // software-pipelined: the next pair's offsets and output metadata load
