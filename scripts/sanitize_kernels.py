@@ -1,6 +1,7 @@
 """Small invocations of every side-task kernel for compute-sanitizer
-(memcheck / racecheck / synccheck): K5 TMA + general + preemptible paths,
-PageRank build + pull, SGD generate + step + RMSE, the synthetic step."""
+(memcheck / racecheck / synccheck): K5 TMA + general + preemptible paths and
+the host-I/O ring, PageRank build (RMAT and caller edges) + pull, SGD generate
++ per-edge / by-user (rounds, item blocks) steps + RMSE, the synthetic step."""
 import os
 import sys
 
@@ -32,10 +33,33 @@ for scale in (12, 16):
     st.reset(stream=s)
     st.step(3, 0.85, stream=s)
     s.synchronize()
-# SGD
+# PageRank on a caller-supplied edge list (self loops, duplicates, a hub row)
+srcs = torch.cat([torch.arange(1, 3000), torch.tensor([5, 5, 7, 7])]).to(torch.int32)
+dsts = torch.cat([torch.zeros(2999, dtype=torch.int64), torch.tensor([5, 6, 8, 8])]).to(torch.int32)
+ge = gpu.PageRankGraph.from_edges(3001, srcs, dsts)
+ste = gpu.PageRankState(ge)
+ste.reset(stream=s)
+ste.step(2, 0.85, stream=s)
+s.synchronize()
+# SGD: per-edge kernel (COO), by-user kernel on the rounds layout (k = 16) and
+# on the item-blocked layout (k = 128: latent rows > 64 MiB -> 2 blocks)
 p = gpu.SgdProblem(V=5000, E=40000, k=16, edge_seed=6, init_seed=7)
 p.step(0, 40000, stream=s)
 p.rmse()
+pu = gpu.SgdProblem(V=5000, E=40000, k=16, edge_seed=6, init_seed=7, by_user=True, window=4096)
+pu.step(0, 17, stream=s)
+pu.step(17, 40000, stream=s)
+pu.rmse()
+pb = gpu.SgdProblem(V=140000, E=300000, k=128, edge_seed=6, init_seed=7, by_user=True, window=65536)
+pb.step(0, 65536, stream=s)
+pb.rmse()
+s.synchronize()
+# host-I/O image task (ring of device slots fed by the copy engines)
+ht = gpu.ImageTask(sw=640, sh=360, dw=320, dh=180, batch=4, images_per_step=1, host_io=True, host_ring=3, seed=9)
+assert ht.vt.create(ht.user) == 0 and ht.vt.init(ht.user, s.cuda_stream) == 0
+for _ in range(6):
+    assert ht.vt.run_next_step(ht.user, s.cuda_stream) == 0
+assert ht.vt.stop(ht.user) == 0
 s.synchronize()
 # the runtime: gap / stamp kernels, a short harvest with the synthetic task
 h = gpu.Harness(num_stages=2, num_micro_batches=2, stage=1, layers=1, hidden=512, tokens=1024,
