@@ -257,6 +257,11 @@ typedef struct fr_pagerank_task_config {
 /* builds the graph immediately (work_units_per_step = E * iters_per_step) */
 int fr_pagerank_task_create(const fr_pagerank_task_config* cfg, fr_side_task_vtable* vt,
                             void** user);
+/* the same task over the caller's graph (fr_pr_graph_rmat / fr_pr_graph_from_edges):
+ * the step arrays are copied at create, the caller keeps and frees `graph`;
+ * cfg's scale / edge_factor / seed are ignored */
+int fr_pagerank_task_create_from_graph(const fr_pagerank_task_config* cfg, const fr_pr_graph* graph,
+                                       fr_side_task_vtable* vt, void** user);
 int fr_pagerank_task_info(void* user, int32_t* V, int64_t* E, double* memory_gib,
                           const float** ranks, int64_t* iterations);
 

@@ -504,6 +504,7 @@ GPU_PROTOTYPES.update({
     "fr_pr_step": (C.c_int, [vp, i32, C.c_float, vp]),
     "fr_pr_ranks": (C.c_int, [vp, P(vp), P(i64)]),
     "fr_pagerank_task_create": (C.c_int, [P(PageRankTaskConfigC), P(SideTaskVTableC), P(vp)]),
+    "fr_pagerank_task_create_from_graph": (C.c_int, [P(PageRankTaskConfigC), vp, P(SideTaskVTableC), P(vp)]),
     "fr_pagerank_task_info": (C.c_int, [vp, P(i32), P(i64), P(dbl), P(vp), P(i64)]),
 })
 

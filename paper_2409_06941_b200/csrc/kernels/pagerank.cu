@@ -873,15 +873,12 @@ struct PrTask {
   cudaStream_t last = nullptr;
 };
 
-// The task keeps only what the step reads (not the original-order CSR).
-int pr_task_create(void* u) {
-  auto* t = static_cast<PrTask*>(u);
-  if (t->h_xoff) return FR_OK;
-  cudaStream_t s = nullptr;
-  FR_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-  fr_pr_graph* g = nullptr;
-  int rc = fr_pr_graph_rmat(t->cfg.scale, t->cfg.edge_factor, t->cfg.seed, s, &g);
-  if (rc == FR_OK) {
+// The task keeps only what the step reads (not the original-order CSR), in
+// pinned host memory: StopSideTask frees the device copy, InitSideTask
+// uploads it again.
+int pin_graph(PrTask* t, const fr_pr_graph* g) {
+  int rc = FR_OK;
+  {
     fr_pr_graph& sh = t->shape;
     sh.V = g->V;
     sh.E = g->E;
@@ -904,8 +901,19 @@ int pr_task_create(void* u) {
     pin(reinterpret_cast<void**>(&t->h_rowr), V * 4, g->rowr);
     pin(reinterpret_cast<void**>(&t->h_rinv), V * 4, g->rinv);
     pin(reinterpret_cast<void**>(&t->h_chunks), size_t(g->n_chunk) * sizeof(int4), g->chunks);
-    fr_pr_graph_destroy(g);
   }
+  return rc;
+}
+
+int pr_task_create(void* u) {
+  auto* t = static_cast<PrTask*>(u);
+  if (t->h_xoff) return FR_OK;
+  cudaStream_t s = nullptr;
+  FR_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  fr_pr_graph* g = nullptr;
+  int rc = fr_pr_graph_rmat(t->cfg.scale, t->cfg.edge_factor, t->cfg.seed, s, &g);
+  if (rc == FR_OK) rc = pin_graph(t, g);
+  if (g) fr_pr_graph_destroy(g);
   cudaStreamDestroy(s);
   return rc;
 }
@@ -980,11 +988,21 @@ void pr_task_destroy(void* u) {
 extern "C" {
 
 int fr_pagerank_task_create(const fr_pagerank_task_config* c, fr_side_task_vtable* vt, void** user) {
+  return fr_pagerank_task_create_from_graph(c, nullptr, vt, user);
+}
+
+int fr_pagerank_task_create_from_graph(const fr_pagerank_task_config* c, const fr_pr_graph* graph,
+                                       fr_side_task_vtable* vt, void** user) {
   if (!c || !vt || !user) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
   if (c->iters_per_step < 1) return frcapi::fail(FR_ERR_VALIDATION, "iters_per_step must be >= 1", "iters_per_step");
   auto* t = new PrTask;
   t->cfg = *c;
-  const int rc = pr_task_create(t);  // build now: work units per step need E
+  int rc = FR_OK;
+  if (graph) {  // the caller's graph: copy what the step reads, the caller keeps the graph
+    rc = pin_graph(t, graph);
+  } else {
+    rc = pr_task_create(t);  // build now: work units per step need E
+  }
   if (rc != FR_OK) {
     pr_task_destroy(t);
     return rc;

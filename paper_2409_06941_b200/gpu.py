@@ -290,16 +290,21 @@ class PageRankState:
 
 
 class PageRankTask:
-    """Built-in PageRank side task (fr_pagerank_task_create)."""
+    """Built-in PageRank side task (fr_pagerank_task_create); graph= runs it
+    over the caller's PageRankGraph (fr_pagerank_task_create_from_graph)."""
 
     def __init__(self, scale=20, edge_factor=16, seed=1, iters_per_step=1, damping=0.85,
-                 total_steps=0):
+                 total_steps=0, graph: "PageRankGraph | None" = None):
         self.cfg = A.PageRankTaskConfigC(scale=scale, edge_factor=edge_factor, seed=seed,
                                          iters_per_step=iters_per_step, damping=damping,
                                          total_steps=total_steps)
         self.vt = A.SideTaskVTableC()
         self.user = C.c_void_p()
-        check(glib().fr_pagerank_task_create(C.byref(self.cfg), C.byref(self.vt), C.byref(self.user)))
+        if graph is None:
+            check(glib().fr_pagerank_task_create(C.byref(self.cfg), C.byref(self.vt), C.byref(self.user)))
+        else:
+            check(glib().fr_pagerank_task_create_from_graph(C.byref(self.cfg), graph._h, C.byref(self.vt),
+                                                            C.byref(self.user)))
         V, E, gib = C.c_int32(), C.c_int64(), C.c_double()
         check(glib().fr_pagerank_task_info(self.user, C.byref(V), C.byref(E), C.byref(gib), None, None))
         self.V, self.E, self.memory_gib = V.value, E.value, gib.value

@@ -151,3 +151,26 @@ def test_from_edges_rejects_bad_ids(g):
     with pytest.raises(Exception):
         g.PageRankGraph.from_edges(10, np.array([0, -1], np.int32), np.array([1, 2], np.int32))
 
+
+def test_task_over_caller_graph_in_bubbles(g, sidetask_oracle):
+    """fr_pagerank_task_create_from_graph: the harvested task over a
+    caller-built graph reaches the oracle's ranks for its iteration count"""
+    rng = np.random.default_rng(11)
+    V = 20000
+    src = rng.integers(0, V, 200000, dtype=np.int32)
+    dst = ((src.astype(np.int64) * 7 + rng.zipf(1.5, 200000)) % V).astype(np.int32)
+    graph = g.PageRankGraph.from_edges(V, src, dst)
+    task = g.PageRankTask(graph=graph, iters_per_step=1)
+    del graph   # the task keeps its own copy of the step arrays
+    assert task.V == V and task.units_per_step == task.E
+    h = g.Harness(num_stages=4, num_micro_batches=4, stage=1, layers=2, profile_reps=2, profile_epochs=1)
+    ok, _ = h.submit("pr", task, profile_steps=4)
+    assert ok
+    h.run(2, True)
+    ranks, iters = task.ranks()
+    assert iters > 0
+    off, col, outdeg = sidetask_oracle.build_pull_csr(V, src, dst)
+    want = sidetask_oracle.pr_run(off, col, outdeg, iters, 0.85)
+    assert np.abs(ranks.double().cpu().numpy() - want).sum() <= 1e-6
+    h.close()
+
