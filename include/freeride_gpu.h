@@ -281,6 +281,11 @@ typedef struct fr_sgd_task_config {
 #define FR_SGD_LAYOUT_BY_USER 1
 /* generates the rating graph on the device immediately (setup) */
 int fr_sgd_task_create(const fr_sgd_task_config* cfg, fr_side_task_vtable* vt, void** user);
+/* the same task over the caller's ratings (fr_sgd_problem_from_edges): the task
+ * takes `problem` over on success (freed with the task); V / E / k come from it,
+ * cfg->layout BY_USER re-lays it out by user */
+int fr_sgd_task_create_from_problem(const fr_sgd_task_config* cfg, fr_sgd_problem* problem,
+                                    fr_side_task_vtable* vt, void** user);
 int fr_sgd_task_problem(void* user, fr_sgd_problem** p, int64_t* epochs_done);
 
 /* ------------------------------------------------------ the GPU runtime */

@@ -529,6 +529,7 @@ GPU_PROTOTYPES.update({
     "fr_sgd_rmse": (C.c_int, [vp, vp, P(dbl)]),
     "fr_sgd_buffers": (C.c_int, [vp, P(vp), P(vp), P(vp), P(vp), P(i32), P(i64), P(i32)]),
     "fr_sgd_task_create": (C.c_int, [P(SgdTaskConfigC), P(SideTaskVTableC), P(vp)]),
+    "fr_sgd_task_create_from_problem": (C.c_int, [P(SgdTaskConfigC), vp, P(SideTaskVTableC), P(vp)]),
     "fr_sgd_task_problem": (C.c_int, [vp, P(vp), P(i64)]),
 })
 

@@ -876,14 +876,28 @@ void sgd_task_destroy(void* u) {
 extern "C" {
 
 int fr_sgd_task_create(const fr_sgd_task_config* c, fr_side_task_vtable* vt, void** user) {
+  return fr_sgd_task_create_from_problem(c, nullptr, vt, user);
+}
+
+int fr_sgd_task_create_from_problem(const fr_sgd_task_config* c, fr_sgd_problem* problem,
+                                    fr_side_task_vtable* vt, void** user) {
   if (!c || !vt || !user) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
   if (c->layout != FR_SGD_LAYOUT_COO && c->layout != FR_SGD_LAYOUT_BY_USER)
     return frcapi::fail(FR_ERR_VALIDATION, "layout must be FR_SGD_LAYOUT_COO or FR_SGD_LAYOUT_BY_USER", "layout");
-  if (c->edges_per_step < 1 || c->E < 1)
+  if (c->edges_per_step < 1 || (problem ? problem->E : c->E) < 1)
     return frcapi::fail(FR_ERR_VALIDATION, "E and edges_per_step must be >= 1", "edges_per_step");
   auto* t = new SgdTask;
   t->cfg = *c;
-  const int rc = sgd_task_create(t);
+  int rc = FR_OK;
+  if (problem) {  // the caller's ratings: the task takes the problem over (sizes from it)
+    t->p = problem;
+    t->cfg.V = problem->V;
+    t->cfg.E = problem->E;
+    t->cfg.k = problem->K;
+    if (c->layout == FR_SGD_LAYOUT_BY_USER) rc = fr_sgd_group_by_user(problem, c->edges_per_step, nullptr);
+  } else {
+    rc = sgd_task_create(t);
+  }
   if (rc != FR_OK) {
     delete t;
     return rc;

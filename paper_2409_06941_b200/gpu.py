@@ -400,14 +400,26 @@ class SgdTask:
     """Built-in Graph-SGD side task (fr_sgd_task_create)."""
 
     def __init__(self, V=3072441, E=117185083, k=16, edge_seed=2, init_seed=3,
-                 edges_per_step=1 << 21, eta=0.01, lam=0.05, total_steps=0, by_user=True):
+                 edges_per_step=1 << 21, eta=0.01, lam=0.05, total_steps=0, by_user=True,
+                 problem: "SgdProblem | None" = None):
+        """problem=: harvest over the caller's ratings (SgdProblem.from_edges); the
+        task takes the problem over (fr_sgd_task_create_from_problem)"""
+        if problem is not None:
+            V, E, k = problem.V, problem.E, problem.k
         self.cfg = A.SgdTaskConfigC(V=V, k=k, E=E, edge_seed=edge_seed, init_seed=init_seed,
                                     edges_per_step=edges_per_step, eta=eta, lambda_=lam,
                                     total_steps=total_steps,
                                     layout=A.SGD_LAYOUT_BY_USER if by_user else A.SGD_LAYOUT_COO)
         self.vt = A.SideTaskVTableC()
         self.user = C.c_void_p()
-        check(glib().fr_sgd_task_create(C.byref(self.cfg), C.byref(self.vt), C.byref(self.user)))
+        if problem is None:
+            check(glib().fr_sgd_task_create(C.byref(self.cfg), C.byref(self.vt), C.byref(self.user)))
+        else:
+            if not problem._owned:
+                raise ValueError("the problem already belongs to a task")
+            check(glib().fr_sgd_task_create_from_problem(C.byref(self.cfg), problem._h, C.byref(self.vt),
+                                                         C.byref(self.user)))
+            problem._owned = False   # freed with the task now
         self.memory_gib = (E * 12 + V * k * 4) / 2 ** 30
         self.units_per_step = self.vt.work_units_per_step
         # algorithmic bytes: 12 B of edge + L_u and L_v read + written (268 B/edge at

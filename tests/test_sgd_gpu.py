@@ -213,3 +213,25 @@ def test_from_edges_rejects_bad_ids(g):
         g.SgdProblem.from_edges(10, np.array([0, 10], np.int32), np.array([1, 2], np.int32),
                                 np.array([1, 2], np.float32))
 
+
+def test_task_over_caller_ratings_in_bubbles(g):
+    """fr_sgd_task_create_from_problem: the harvested task over the caller's
+    ratings (re-laid out by user) lowers the RMSE"""
+    rng = np.random.default_rng(12)
+    U, I, E = 30000, 8000, 2000000
+    u = rng.integers(0, U, E, dtype=np.int32)
+    v = (U + np.floor(I * rng.random(E) ** 2)).astype(np.int32)
+    r = rng.integers(1, 6, E).astype(np.float32)
+    prob = g.SgdProblem.from_edges(U + I, u, v, r, k=16, init_seed=5)
+    r0 = prob.rmse()
+    task = g.SgdTask(problem=prob, edges_per_step=1 << 18)
+    assert task.units_per_step == 1 << 18
+    h = g.Harness(num_stages=4, num_micro_batches=4, stage=2, layers=2, profile_reps=2, profile_epochs=1)
+    ok, _ = h.submit("sgd-user", task, profile_steps=4)
+    assert ok
+    run = h.run(3, True)
+    assert run["steps_completed"] > 0
+    p2, epochs = task.problem()
+    assert p2.rmse() < r0
+    h.close()
+
