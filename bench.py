@@ -53,6 +53,7 @@ LAYERS_6B, HIDDEN_6B = 32, 4096                                       # nanoGPT-
 FRAMES = dict(sw=3840, sh=2160, dw=1920, dh=1080)
 BATCH = 64
 IMAGES_PER_STEP = 16   # ~100 us steps: 3 us inter-step gaps cost 3 % (8 frames: 5.5 %)
+STEP_GROUP = int(os.environ.get("FR_STEP_GROUP", "3"))   # steps between one pair of timing events
 E2E_IMAGES_PER_STEP = 1
 E2E_RING = int(os.environ.get("FR_E2E_RING", "128"))   # device staging slots: the copy engines run ahead of the steps
 OUT_PX = FRAMES["dw"] * FRAMES["dh"]
@@ -230,7 +231,8 @@ def ours(args):
     torch.cuda.synchronize()
     with Clocks(device) as clk:
         for s in range(STAGES):
-            h = gpu.Harness(num_stages=STAGES, num_micro_batches=MICRO_BATCHES, stage=s, **SHAPE)
+            h = gpu.Harness(num_stages=STAGES, num_micro_batches=MICRO_BATCHES, stage=s, step_group=STEP_GROUP,
+                            **SHAPE)
             stage_prof.append(h.profile())
             for n in names:
                 if n == "image":
@@ -302,7 +304,8 @@ def ours(args):
             s = placement[name]
             if s is None:
                 continue
-            h = gpu.Harness(num_stages=STAGES, num_micro_batches=MICRO_BATCHES, stage=s, **SHAPE_36B)
+            h = gpu.Harness(num_stages=STAGES, num_micro_batches=MICRO_BATCHES, stage=s, step_group=STEP_GROUP,
+                            **SHAPE_36B)
             r = harvest(h, name, make(), K, W)
             h.close()
             mixed["stages"].append({"stage": s, "task": name, "units_per_bubble_s": r["with"]["work_units"] / r["base"]["bubble_s"],
@@ -439,7 +442,7 @@ def emit(args, results, ws, names, csr):
         "config": {"workload": WORKLOAD, "stages": STAGES, "micro_batches": MICRO_BATCHES, "stage_shape": SHAPE,
                    "frames": BATCH, "images_per_step": IMAGES_PER_STEP,
                    "step": "one 1F1B epoch of all 4 stages (replayed) with the side task",
-                   "parallelism": f"replicas x{ws}",
+                   "parallelism": f"replicas x{ws}", "step_group": STEP_GROUP,
                    "l2": "image inputs 1.6 GB per batch > 126 MB L2; no flush needed"},
         "delta_t": dT("image"), "fill": fill("image"),
         "overrun_frac": sum(r["image"]["overrun"] for r in results) / max(1e-12, sum(r["image"]["used"] for r in results)),

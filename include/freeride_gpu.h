@@ -55,6 +55,12 @@ typedef struct fr_preempt {
 typedef struct fr_img_plan fr_img_plan;
 enum fr_img_path { FR_IMG_PATH_GENERAL = 0, FR_IMG_PATH_TMA_2X = 1 };
 int fr_img_plan_create(int32_t sw, int32_t sh, int32_t dw, int32_t dh, fr_img_plan** out);
+/* Consecutive exact-2x launches on this plan may overlap (programmatic
+ * dependent launch: a launch's CTAs start as soon as every CTA of the previous
+ * one has taken its last row).  Only for callers whose launches read inputs
+ * that the immediately preceding kernel on the stream did not produce (the
+ * built-in image task: frames materialised at InitSideTask). */
+int fr_img_plan_set_overlap(fr_img_plan* plan, int32_t overlap);
 int fr_img_plan_destroy(fr_img_plan* plan);
 int fr_img_plan_path(const fr_img_plan* plan, int32_t* path);
 /* n images: src [n][sh][sw][3] u8, dst [n][dh][dw][3] u8, wm [dh][dw][4] u8
@@ -322,6 +328,10 @@ typedef struct fr_harness_config {
    * observed within grace_ns -> pause-timeout kill (framework_enforce). */
   double memory_headroom_gib;
   int64_t grace_ns;           /* <= 0: 100 ms (LimitConfig::grace_period = 100 ticks of 1 ms) */
+  int32_t step_group;         /* <= 1: timing events around every step; G > 1: up to G
+                                 consecutive iterative steps between one pair of events
+                                 (each still admitted by the gate), so they run back to
+                                 back; timelines and reprofile then see step groups */
 } fr_harness_config;
 
 /* All durations in ns ticks (tick_seconds = 1e-9). */

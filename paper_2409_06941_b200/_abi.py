@@ -438,6 +438,7 @@ GPU_PROTOTYPES = {
     "fr_clock_probe": (C.c_int, [vp, i64, vp]),
     "fr_memcpy": (C.c_int, [vp, vp, i64]),
     "fr_img_plan_create": (C.c_int, [i32, i32, i32, i32, P(vp)]),
+    "fr_img_plan_set_overlap": (C.c_int, [vp, i32]),
     "fr_img_plan_destroy": (C.c_int, [vp]),
     "fr_img_plan_path": (C.c_int, [vp, P(i32)]),
     "fr_img_resize_watermark": (C.c_int, [vp, vp, vp, vp, i32, vp]),
@@ -542,7 +543,7 @@ class HarnessConfigC(Struct):
         ("gpu_memory_total", dbl), ("weight_mem", dbl), ("activation_mem", dbl),
         ("fp_ticks_override", i64), ("bp_ticks_override", i64),
         ("profile_epochs", i32), ("transport", i32),
-        ("memory_headroom_gib", dbl), ("grace_ns", i64),
+        ("memory_headroom_gib", dbl), ("grace_ns", i64), ("step_group", i32),
     ]
 
 

@@ -188,10 +188,17 @@ __global__ void __launch_bounds__(kImgThreads, CPS)
   __syncthreads();
 
   uint32_t k = 0;
+  bool triggered = false;
   for (;; ++k) {
     const int s = static_cast<int>(k % S);
     const uint32_t row = row_of[s];  // written >= S-1 barriers ago (or before the first)
     if (row >= rows) break;          // rows are grabbed in increasing order: all done
+    if (!PREEMPT && !triggered && row_of[(s + S - 1) % S] >= rows) {
+      // this CTA takes no further row: let a programmatic dependent launch
+      // (the next step on the stream) start its CTAs on the SMs we free
+      asm volatile("griddepcontrol.launch_dependents;");
+      triggered = true;
+    }
     const uint32_t y = y_of[s];
     // the elected thread's next row: the atomic's round trip overlaps this
     // row's compute instead of delaying the refill after the barrier
@@ -332,13 +339,17 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 
 }  // namespace
 
+constexpr uint32_t kImgCtrSlots = 64;
+
 struct fr_img_plan {
   int sw = 0, sh = 0, dw = 0, dh = 0;
   int stages = kImgStages, ctas_per_sm = kImgCtasPerSm;  // TMA path pipeline shape
   int path = FR_IMG_PATH_GENERAL;
   int32_t* d_tab = nullptr;
   void* d_wm = nullptr;  // plan-owned prepared watermark for fr_img_resize_watermark
-  uint32_t* d_ctr = nullptr;  // dynamic row scheduler {next row, CTAs done}; one stream at a time
+  uint32_t* d_ctr = nullptr;  // dynamic row scheduler {next row, CTAs done} x kImgCtrSlots; one stream at a time
+  mutable uint32_t launches = 0;  // TMA launches so far: slot = launches % kImgCtrSlots
+  bool overlap = false;           // fr_img_plan_set_overlap: consecutive launches may overlap
   int smem = 0;
   int sms = 0;
   size_t prepared_bytes() const {
@@ -400,8 +411,8 @@ int fr_img_plan_create(int32_t sw, int32_t sh, int32_t dw, int32_t dh, fr_img_pl
       e = cudaMemcpy(plan->d_tab, tab.data(), tab.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
   }
   if (e == cudaSuccess) e = cudaMalloc(&plan->d_wm, plan->prepared_bytes());
-  if (e == cudaSuccess) e = cudaMalloc(&plan->d_ctr, 2 * sizeof(uint32_t));
-  if (e == cudaSuccess) e = cudaMemset(plan->d_ctr, 0, 2 * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMalloc(&plan->d_ctr, 2 * kImgCtrSlots * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMemset(plan->d_ctr, 0, 2 * kImgCtrSlots * sizeof(uint32_t));
   if (e != cudaSuccess) {
     if (plan->d_tab) cudaFree(plan->d_tab);
     if (plan->d_wm) cudaFree(plan->d_wm);
@@ -410,6 +421,12 @@ int fr_img_plan_create(int32_t sw, int32_t sh, int32_t dw, int32_t dh, fr_img_pl
     return frcapi::cuda_status(e, "image plan setup");
   }
   *out = plan;
+  return FR_OK;
+}
+
+int fr_img_plan_set_overlap(fr_img_plan* plan, int32_t overlap) {
+  if (!plan) return frcapi::fail(FR_ERR_ARGUMENT, "null plan");
+  plan->overlap = overlap != 0;
   return FR_OK;
 }
 
@@ -463,9 +480,28 @@ int fr_img_resize_watermark_prepared(const fr_img_plan* plan, const uint8_t* src
     if (rows >= (int64_t{1} << 31)) return frcapi::fail(FR_ERR_UNSUPPORTED, "too many rows in one step");
     const int grid = static_cast<int>(std::min<int64_t>(rows, int64_t(plan->sms) * plan->ctas_per_sm));
     auto k = plan->stages == 2 ? img_resize2x_wm_tma<2, false, 3> : img_resize2x_wm_tma<3, false, 2>;
-    k<<<grid, kImgThreads, plan->smem, s>>>(
-        src, dst, static_cast<const uint4*>(prepared), plan->dw, plan->dh, static_cast<uint32_t>(rows), plan->d_ctr,
-        nullptr, 0u, 0u);
+    // Consecutive steps overlap their tail and head (programmatic dependent
+    // launch: a launch's CTAs start once every CTA of the previous one took
+    // its last row).  Steps touch different frames; the row counters rotate
+    // through kImgCtrSlots slots, so overlapping launches never share one.
+    uint32_t* ctr = plan->d_ctr + 2 * (plan->launches++ % kImgCtrSlots);
+    static const int pdl_env = [] {
+      const char* e = std::getenv("FR_IMG_PDL");  // experiment override: 0 / 1
+      return e ? std::atoi(e) : -1;
+    }();
+    const bool pdl = pdl_env >= 0 ? pdl_env != 0 : plan->overlap;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kImgThreads);
+    cfg.dynamicSmemBytes = plan->smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    FR_CUDA_TRY(cudaLaunchKernelEx(&cfg, k, src, dst, static_cast<const uint4*>(prepared), plan->dw, plan->dh,
+                                   static_cast<uint32_t>(rows), ctr, static_cast<const uint32_t*>(nullptr), 0u, 0u));
   } else {
     const int64_t total = static_cast<int64_t>(n) * plan->dw * plan->dh;
     img_resize_wm_general<<<grid_for(total, 256, 8), 256, 0, s>>>(

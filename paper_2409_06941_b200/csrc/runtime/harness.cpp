@@ -134,9 +134,12 @@ struct Task {
   }
 };
 
+// One timed record: `n` consecutive RunNextStep calls of `task` between the
+// events a and b (n > 1 with cfg.step_group: no event between the steps).
 struct StepRec {
   cudaEvent_t a, b;
   Task* task;
+  int n = 1;
 };
 
 // Peer-linked pipeline mailbox (transport 1): one device allocation per
@@ -374,7 +377,7 @@ struct fr_harness {
                                   : t.prof.est_per_step_duration.value_or(0.0);
   }
 
-  std::vector<Task*> step_task;  // task of each step of the last run
+  std::vector<Task*> step_task;  // task of each step of the last run (groups: equal slices)
 
   TaskView lookup(const std::string& id) const {
     auto it = tasks.find(id);
@@ -562,7 +565,20 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
   double dispatch_ns = 0;
   std::int64_t next_slot = 0;
   double units = 0;
-  const int depth = std::max(1, cfg.max_inflight_steps);
+  // Step groups: up to G consecutive steps of a task go out between one pair
+  // of timing events.  An event between two kernels serialises them (the next
+  // launch waits for the event), which costs ~2-3 us per step and defeats a
+  // kernel's programmatic dependent launch; grouped steps run back to back.
+  const int group = std::max(1, cfg.step_group);
+  const int depth = std::max(std::max(1, cfg.max_inflight_steps), group > 1 ? 2 * group : 1);
+  std::int64_t inflight_steps = 0;  // dispatched, not yet completed (all records)
+  std::int64_t open_rec = -1;       // record still collecting steps (no end event yet)
+  auto close_group = [&] {
+    if (open_rec < 0) return;
+    ck(cudaEventRecord(steps[static_cast<std::size_t>(open_rec)].b, side), "record");
+    inflight.push_back(static_cast<std::size_t>(open_rec));
+    open_rec = -1;
+  };
 
   auto task_of = [&](const std::string& id) -> Task& { return *tasks.at(id); };
   // imperative work is counted by the workload itself (rows, pixels, ...)
@@ -592,17 +608,19 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
       if (q == cudaErrorNotReady) break;
       ck(q, "step event");
       Task* st = steps[inflight.front()].task;
+      const int n = steps[inflight.front()].n;
       inflight.pop_front();
-      ++completed;
-      if (!st->imperative()) units += st->vt.work_units_per_step;  // the completing step's own task
-      st->rt.steps_completed++;  // counted at step end (task.hpp:55); imperative: kernels
+      inflight_steps -= n;
+      completed += n;
+      if (!st->imperative()) units += n * st->vt.work_units_per_step;  // the completing steps' own task
+      st->rt.steps_completed += n;  // counted at step end (task.hpp:55); imperative: kernels
       // Re-anchor the projection: the next queued step started when this one
       // ended (~now), so drift from mis-estimated step times cannot build up.
       if (!inflight.empty() && !st->imperative()) {
         const double est = gate_est(*st);
         proj_end_dev = std::max<std::int64_t>(
             proj_end_dev, dev_now() + static_cast<std::int64_t>(std::llround(est / kTick)) *
-                                          static_cast<std::int64_t>(inflight.size()));
+                                          inflight_steps);
       }
       if (running && !running->imperative()) {
         int32_t done = 0;
@@ -767,6 +785,7 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
         ck(cudaEventRecord(r.b, side), "record");
         steps.push_back(r);
         inflight.push_back(steps.size() - 1);
+        ++inflight_steps;
         ++launched;
         dispatch_ns += static_cast<double>(host_ns() - h0);
         if (oom(*r.task)) break;
@@ -774,7 +793,7 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
       // 3b. iterative dispatch: the program-directed gate at the projected start time
       while (running && !running->imperative() && !pause_pending && !gate_closed &&
              running->rt.state == SideTaskState::Running &&
-             static_cast<int>(inflight.size()) < depth) {
+             inflight_steps < depth) {
         const std::int64_t h0 = host_ns();
         const std::int64_t now = h0 + clock_off;
         const std::int64_t start = std::max(now + launch_lat, proj_end_dev);
@@ -785,21 +804,30 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
           gate_closed = true;  // yield until the next transition
           break;
         }
-        StepRec r{ev(), ev(), running};
-        ck(cudaEventRecord(r.a, side), "record");
+        const bool extend = open_rec >= 0 && steps[static_cast<std::size_t>(open_rec)].task == running &&
+                            steps[static_cast<std::size_t>(open_rec)].n < group;
+        if (!extend) {
+          close_group();
+          steps.push_back(StepRec{ev(), ev(), running, 0});
+          open_rec = static_cast<std::int64_t>(steps.size()) - 1;
+          ck(cudaEventRecord(steps.back().a, side), "record");
+        }
         {
           PoolScope ps(device, running->pool);
           hook(running->vt.run_next_step(running->user, side), "run_next_step");
         }
-        ck(cudaEventRecord(r.b, side), "record");
+        StepRec& r = steps[static_cast<std::size_t>(open_rec)];
+        ++r.n;
+        Task* rt = r.task;
+        if (r.n >= group) close_group();
         apply_transition(running->rt, TransitionKind::RunNextStep, start);
-        steps.push_back(r);
-        inflight.push_back(steps.size() - 1);
+        ++inflight_steps;
         proj_end_dev = d.step_end;
         ++launched;
         dispatch_ns += static_cast<double>(host_ns() - h0);
-        if (oom(*r.task)) break;
+        if (oom(*rt)) break;
       }
+      close_group();  // nothing else may enter the side stream inside a group
       // framework-enforced limit: a pause not observed within the grace
       // period is a Kill (limits.cpp:21-26): the task's cancel hook stops its
       // in-flight kernels (cooperative ones exit at once), then it is stopped
@@ -860,10 +888,14 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
     prev_end = eev[e].end;
   }
   step_task.clear();
-  for (const StepRec& r : steps) {
-    step_se.push_back(elapsed_s(run_start, r.a));
-    step_se.push_back(elapsed_s(run_start, r.b));
-    step_task.push_back(r.task);
+  for (const StepRec& r : steps) {  // a group of n back-to-back steps: n equal slices
+    const double a = elapsed_s(run_start, r.a), b = elapsed_s(run_start, r.b);
+    const int n = std::max(1, r.n);
+    for (int i = 0; i < n; ++i) {
+      step_se.push_back(a + (b - a) * i / n);
+      step_se.push_back(a + (b - a) * (i + 1) / n);
+      step_task.push_back(r.task);
+    }
   }
   const double makespan = elapsed_s(run_start, eev[static_cast<std::size_t>(epochs) - 1].end);
   double bubble_total = 0, used = 0, step_total = 0, worst = 0;

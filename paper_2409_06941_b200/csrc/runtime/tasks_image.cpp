@@ -77,8 +77,11 @@ int release(ImageTask* t, cudaStream_t s) {
 
 int img_create(void* u) {
   auto* t = static_cast<ImageTask*>(u);
-  if (!t->plan) return fr_img_plan_create(t->cfg.sw, t->cfg.sh, t->cfg.dw, t->cfg.dh, &t->plan);
-  return FR_OK;
+  if (t->plan) return FR_OK;
+  int rc = fr_img_plan_create(t->cfg.sw, t->cfg.sh, t->cfg.dw, t->cfg.dh, &t->plan);
+  // resident frames are produced at Init, never by the kernel before a step
+  if (rc == FR_OK && !t->cfg.host_io) rc = fr_img_plan_set_overlap(t->plan, 1);
+  return rc;
 }
 
 int host_frames(ImageTask* t, cudaStream_t s);

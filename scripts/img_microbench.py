@@ -27,6 +27,35 @@ def main():
             sl = slice(i * per_step, (i + 1) * per_step)
             plan.run_prepared(src[sl], dst[sl], wmp, stream=s)
     s.synchronize()
+    if len(sys.argv) > 3 and sys.argv[3] == "chain1":   # one event between consecutive steps
+        n = reps * steps
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(n + 1)]
+        ev[0].record(s)
+        for k in range(n):
+            i = k % steps
+            plan.run_prepared(src[i * per_step:(i + 1) * per_step], dst[i * per_step:(i + 1) * per_step], wmp,
+                              stream=s)
+            ev[k + 1].record(s)
+        s.synchronize()
+        ts = sorted(ev[k].elapsed_time(ev[k + 1]) * 1e-3 for k in range(n))
+        med = ts[len(ts) // 2]
+        alg = per_step * (24883200 + 6220800) + 16588800
+        print(json.dumps({"per_step": per_step, "mode": "chain1", "median_s": med, "alg_GBps": alg / med / 1e9}))
+        return
+    if len(sys.argv) > 3 and sys.argv[3] == "chain":   # steps back to back, events only around each batch pass
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+        for a, b in ev:
+            a.record(s)
+            for i in range(steps):
+                sl = slice(i * per_step, (i + 1) * per_step)
+                plan.run_prepared(src[sl], dst[sl], wmp, stream=s)
+            b.record(s)
+        s.synchronize()
+        ts = sorted(a.elapsed_time(b) * 1e-3 / steps for a, b in ev)
+        med = ts[len(ts) // 2]
+        alg = per_step * (24883200 + 6220800) + 16588800
+        print(json.dumps({"per_step": per_step, "mode": "chain", "median_s": med, "alg_GBps": alg / med / 1e9}))
+        return
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps * steps)]
     k = 0
     for _ in range(reps):
