@@ -340,7 +340,8 @@ def ours(args):
         try:   # a failure here (e.g. a peer link timing out) must not cost the replica numbers
             linked = D.linked_harvest(
                 lambda: gpu.ImageTask(batch=BATCH, images_per_step=IMAGES_PER_STEP, **FRAMES),
-                shape, num_micro_batches=max(MICRO_BATCHES, ws), epochs=K, warmup=W, task_name="image")
+                shape, num_micro_batches=max(MICRO_BATCHES, ws), epochs=K, warmup=W, task_name="image",
+                step_group=STEP_GROUP)
             linked["shape"] = shape
         except Exception as e:  # noqa: BLE001 -- reported in the JSON line
             print(f"[bench] rank {rank}: linked pipeline failed: {e!r}", file=sys.stderr, flush=True)
