@@ -320,7 +320,7 @@ def ours(args):
     c5 = None
     if not args.no_c5:
         h = gpu.Harness(num_stages=8, num_micro_batches=8, stage=3, layers=LAYERS_6B // 8, hidden=HIDDEN_6B,
-                        tokens=8192, ffn_mult=4)
+                        tokens=8192, ffn_mult=4, step_group=STEP_GROUP)
         prof = h.profile()
         r = harvest(h, "image", gpu.ImageTask(batch=BATCH, images_per_step=IMAGES_PER_STEP, **FRAMES), K, W)
         h.close()
