@@ -155,6 +155,10 @@ int fr_sgd_group_by_user(fr_sgd_problem* p, int64_t window_edges, void* stream);
  * across each run of equal u -- correct for any order, fast when runs are
  * long), 0 = per-edge.  For callers that lay their ratings out themselves. */
 int fr_sgd_problem_set_kernel(fr_sgd_problem* p, int32_t by_user);
+/* Consecutive user-grouped steps may overlap (programmatic dependent launch:
+ * a step's CTAs start while the previous step's last segments drain -- more
+ * Hogwild concurrency, nothing else).  The built-in task sets it. */
+int fr_sgd_problem_set_overlap(fr_sgd_problem* p, int32_t overlap);
 /* K4: *d_acc (device fp64) += sum of squared errors over [e_begin, e_end) */
 int fr_sgd_sqerr(const fr_sgd_problem* p, int64_t e_begin, int64_t e_end, double* d_acc,
                  void* stream);

@@ -526,6 +526,7 @@ GPU_PROTOTYPES.update({
     "fr_sgd_step": (C.c_int, [vp, i64, i64, C.c_float, C.c_float, vp]),
     "fr_sgd_group_by_user": (C.c_int, [vp, i64, vp]),
     "fr_sgd_problem_set_kernel": (C.c_int, [vp, i32]),
+    "fr_sgd_problem_set_overlap": (C.c_int, [vp, i32]),
     "fr_sgd_sqerr": (C.c_int, [vp, i64, i64, vp, vp]),
     "fr_sgd_rmse": (C.c_int, [vp, vp, P(dbl)]),
     "fr_sgd_buffers": (C.c_int, [vp, P(vp), P(vp), P(vp), P(vp), P(i32), P(i64), P(i32)]),

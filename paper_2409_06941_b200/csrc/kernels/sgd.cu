@@ -257,6 +257,8 @@ __global__ void __maxnreg__(SGD_MAXNREG) sgd_user_kernel(
     mu0 = mu1; mv0 = mv1; mr0 = mr1;
     mu1 = mu2; mv1 = mv2; mr1 = mr2;
   }
+  // segment done: a programmatic dependent launch (the next step) may start
+  asm volatile("griddepcontrol.launch_dependents;");
   if (cu >= 0)
     apply(&L4[static_cast<int64_t>(cu) * LN + sub], make_float4(a.x - a0.x, a.y - a0.y, a.z - a0.z, a.w - a0.w));
 }
@@ -422,6 +424,7 @@ struct fr_sgd_problem {
   double* acc = nullptr;
   int sms = 148;
   bool grouped = false;  // edges stable-sorted by u (fr_sgd_group_by_user)
+  bool overlap = false;  // fr_sgd_problem_set_overlap: consecutive steps may overlap (Hogwild)
   int64_t max_deg = 0;   // largest number of ratings touching one vertex (u or v side)
 };
 
@@ -515,7 +518,21 @@ void launch_user_step(fr_sgd_problem* p, int64_t a, int64_t b, float eta, float 
   const int64_t seg = ((n + groups - 1) / groups + D - 1) / D * D;
   const int64_t used = (n + seg - 1) / seg;
   const int grid = static_cast<int>((used * LN + kSgdThreads - 1) / kSgdThreads);
-  sgd_user_kernel<K, D><<<grid, kSgdThreads, 0, s>>>(p->u, p->v, p->r, p->L, a, b, seg, eta, lam);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kSgdThreads);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  static const int overlap_env = [] {
+    const char* e = std::getenv("FR_SGD_OVERLAP");  // A/B override: 0 / 1
+    return e ? std::atoi(e) : -1;
+  }();
+  cfg.numAttrs = (overlap_env >= 0 ? overlap_env != 0 : p->overlap) ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, sgd_user_kernel<K, D>, static_cast<const int32_t*>(p->u), static_cast<const int32_t*>(p->v),
+                     static_cast<const float*>(p->r), p->L, a, b, seg, eta, lam);
 }
 
 template <int K>
@@ -758,6 +775,12 @@ int fr_sgd_group_by_user(fr_sgd_problem* p, int64_t window_edges, void* stream) 
   return FR_OK;
 }
 
+int fr_sgd_problem_set_overlap(fr_sgd_problem* p, int32_t overlap) {
+  if (!p) return frcapi::fail(FR_ERR_ARGUMENT, "null problem");
+  p->overlap = overlap != 0;
+  return FR_OK;
+}
+
 int fr_sgd_problem_set_kernel(fr_sgd_problem* p, int32_t by_user) {
   if (!p) return frcapi::fail(FR_ERR_ARGUMENT, "null problem");
   p->grouped = by_user != 0;
@@ -898,6 +921,9 @@ int fr_sgd_task_create_from_problem(const fr_sgd_task_config* c, fr_sgd_problem*
   } else {
     rc = sgd_task_create(t);
   }
+  // the task's steps follow each other (Hogwild: a step may start while the
+  // previous one's last segments drain)
+  if (rc == FR_OK) rc = fr_sgd_problem_set_overlap(t->p, 1);
   if (rc != FR_OK) {
     delete t;
     return rc;
