@@ -9,8 +9,9 @@ import torch  # noqa: E402
 
 from paper_2409_06941_b200 import gpu  # noqa: E402
 
-h = gpu.Harness(num_stages=4, num_micro_batches=4, stage=1, layers=6, hidden=2048, tokens=8192)
-h.submit("image", gpu.ImageTask(batch=64, images_per_step=8), profile_steps=16)
+# the bench's configuration: 16 frames per step, step groups of 3
+h = gpu.Harness(num_stages=4, num_micro_batches=4, stage=1, layers=6, hidden=2048, tokens=8192, step_group=3)
+h.submit("image", gpu.ImageTask(batch=64, images_per_step=16), profile_steps=16)
 h.run(3, True)
 h.reprofile("image")
 torch.cuda.synchronize()
