@@ -344,6 +344,9 @@ __global__ void __maxnreg__(kPrThreads >= 1024 ? 56 : 40) pr_pull_kernel(PrArgs 
   __shared__ int scnt[kMaxSlots];
   const float* hot = reinterpret_cast<const float*>(hot4);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // launched as a programmatic dependent of the previous iteration: the CTA
+  // is resident early, but reads c_in only once that grid completed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   {
     const float4* src = reinterpret_cast<const float4*>(a.c_in);
     for (int i = tid; i < (a.hot >> 2); i += kPrThreads) hot4[i] = __ldg(&src[i]);
@@ -403,6 +406,7 @@ __global__ void __maxnreg__(kPrThreads >= 1024 ? 56 : 40) pr_pull_kernel(PrArgs 
     x = px;
     y = py;
   }
+  asm volatile("griddepcontrol.launch_dependents;");
   if (a.do_tail) {
     for (int32_t i = a.bstart[0] + blockIdx.x * kPrThreads + tid; i < a.V; i += gridDim.x * kPrThreads)
       store(a, i, __ldg(&a.rowc[i]), __ldg(&a.rinv[i]), 0.0);
@@ -422,6 +426,14 @@ int grid_for(int64_t work, int threads, int per_sm) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t want = (work + threads - 1) / threads;
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(sms) * per_sm)));
+}
+
+bool pr_pdl() {
+  static const bool v = [] {
+    const char* e = std::getenv("FR_PR_PDL");  // A/B override
+    return !e || std::atoi(e) != 0;
+  }();
+  return v;
 }
 
 int split_edges() {
@@ -830,7 +842,17 @@ int fr_pr_step(fr_pr_state* st, int32_t iters, float damping, void* stream) {
     a.c_in = st->c[st->cur];
     a.c_out = st->c[st->cur ^ 1];
     a.do_tail = st->tail_pending > 0;
-    kern<<<std::min(g->sms * cfg.ctas_per_sm, kMaxCtas), cfg.threads, smem, s>>>(a);
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(std::min(g->sms * cfg.ctas_per_sm, kMaxCtas));
+    lc.blockDim = dim3(cfg.threads);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;  // safe: the kernel waits before reading
+    lc.attrs = at;
+    lc.numAttrs = pr_pdl() ? 1 : 0;
+    FR_CUDA_TRY(cudaLaunchKernelEx(&lc, kern, a));
     if (st->tail_pending > 0) --st->tail_pending;
     st->cur ^= 1;
     st->iterations++;
