@@ -13,7 +13,7 @@ Headline workload (BASELINE.json configs[1]): the image resize + watermark
 side task (64 synthetic 4K RGB frames -> 1080p, RGBA watermark, 32 frames per
 RunNextStep).  The same run also measures configs[0] (PageRank, RMAT-20,
 two pull iterations per step), configs[2] (Graph-SGD, Orkut shape, rank
-16, 2^21 edges per step), configs[3] (mixed, 3.6B-shaped stages) and the
+16, 2^22 edges per step), configs[3] (mixed, 3.6B-shaped stages) and the
 image task through the imperative interface (device-preempted workload)
 under "workloads".
 
@@ -58,7 +58,8 @@ E2E_IMAGES_PER_STEP = 1
 E2E_RING = int(os.environ.get("FR_E2E_RING", "128"))   # device staging slots: the copy engines run ahead of the steps
 OUT_PX = FRAMES["dw"] * FRAMES["dh"]
 PR = dict(scale=20, edge_factor=16, seed=1, iters_per_step=2)
-SGD = dict(V=3072441, E=117185083, k=16, edge_seed=2, init_seed=3, edges_per_step=1 << 21)
+SGD = dict(V=3072441, E=117185083, k=16, edge_seed=2, init_seed=3,
+           edges_per_step=int(os.environ.get("FR_SGD_EDGES_PER_STEP", str(1 << 22))))
 METRIC = "side-task px/s per bubble-sec at <=1% pipeline dT (image 4K->1080p+watermark); HBM GB/s vs peak"
 UNIT = "px/bubble-s"
 WORKLOAD = ("image resize+watermark side task (64x 3840x2160 RGB -> 1920x1080, RGBA watermark), "
@@ -413,10 +414,10 @@ def emit(args, results, ws, names, csr):
                      "roofline": roof("pagerank", "pr_pull_kernel (2 launches of 1 iteration per step, in-pipeline); "
                                       "working set L2-resident: latency-bound gathers, not HBM"),
                      "cpu_baseline": cpu_pagerank(args.cpu_seconds / 2, csr) if csr is not None else None},
-        "sgd": {"config": "configs[2]: Orkut shape V=3,072,441 E=117,185,083 k=16, 2^21 edges/step, "
+        "sgd": {"config": f"configs[2]: Orkut shape V=3,072,441 E=117,185,083 k=16, {SGD['edges_per_step']} edges/step, "
                           "by-user layout (fr_sgd_group_by_user)",
                 "value": rate("sgd"), "unit": "edges/bubble-s", "dT": dT("sgd"), "fill": fill("sgd"),
-                "roofline": dict(roof("sgd", "sgd_user_kernel<16> (2^21 edges/launch, in-pipeline; "
+                "roofline": dict(roof("sgd", f"sgd_user_kernel<16> ({SGD['edges_per_step']} edges/launch, in-pipeline; "
                                              "alg bytes 12 + 128 per edge + 128 per L_u load; item blocks keep "
                                              "L_v in L2, so part of them never reaches DRAM)") or {},
                                  traffic=70.7 * SGD["edges_per_step"],
