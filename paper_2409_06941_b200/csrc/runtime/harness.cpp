@@ -177,6 +177,9 @@ struct fr_harness {
   std::uint32_t* flag = nullptr;   // mapped
   std::uint64_t* stamp_dev = nullptr;
   std::uint32_t* flag_dev = nullptr;
+  std::uint32_t* pgate = nullptr;      // host-mapped gate of the standalone step profile
+  std::uint32_t* pgate_dev = nullptr;
+  std::uint32_t pgate_seq = 0;
   // transport 1 (peer-linked pipeline)
   Mailbox mbox, prev_mbox, next_mbox;
   std::size_t mbox_bytes = 0, msg_bytes = 0;
@@ -222,6 +225,7 @@ struct fr_harness {
     if (ring) cudaFreeHost(ring);
     if (stamp) cudaFreeHost(stamp);
     if (flag) cudaFreeHost(flag);
+    if (pgate) cudaFreeHost(pgate);
     if (ctl) cudaFree(ctl);
     if (mbox.base) cudaFree(mbox.base);
     if (train) cudaStreamDestroy(train);
@@ -982,6 +986,9 @@ int fr_harness_create(const fr_harness_config* cfg, fr_harness** out) {
     ck(cudaHostAlloc(reinterpret_cast<void**>(&h->stamp), 64, cudaHostAllocMapped), "stamp");
     ck(cudaHostAlloc(reinterpret_cast<void**>(&h->flag), 64, cudaHostAllocMapped), "flag");
     *h->flag = 0;
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&h->pgate), 64, cudaHostAllocMapped), "profile gate");
+    *h->pgate = 0;
+    ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->pgate_dev), h->pgate, 0), "profile gate dev");
     ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->stamp_dev), h->stamp, 0), "stamp dev");
     ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->flag_dev), h->flag, 0), "flag dev");
     ck(cudaMalloc(&h->ctl, sizeof(TimelineCtl)), "ctl");
@@ -1126,10 +1133,22 @@ int fr_harness_submit(fr_harness* h, const char* task_id, const fr_side_task_vta
     for (int i = 0; i < (imperative ? 0 : 2); ++i) hook(vt->run_next_step(user, h->side), "run_next_step");
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs;
     for (int i = 0; i < n; ++i) {
+      // The side stream is held by a flag wait until the hook has returned:
+      // a hook that stalls the host (a cudaMallocAsync growing its pool
+      // maps memory for 0.4-23 ms) must not be timed as GPU step time --
+      // an inflated estimate closes the gate for every bubble.
+      LinkWaitArgs w{};
+      w.ctl = h->ctl;
+      w.slot_start = w.slot_end = -1;
+      w.flag = h->pgate_dev;
+      w.seq = ++h->pgate_seq;
+      w.timeout_ns = 5'000'000'000ull;
+      launch_link_wait(w, h->side);
       cudaEvent_t a = h->ev(), b = h->ev();
       ck(cudaEventRecord(a, h->side), "record");
       hook(vt->run_next_step(user, h->side), "run_next_step");
       ck(cudaEventRecord(b, h->side), "record");
+      __atomic_store_n(h->pgate, w.seq, __ATOMIC_RELEASE);
       ck(cudaEventSynchronize(b), "profile step");  // standalone: one step at a time
       evs.push_back({a, b});
     }
