@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(kImgThreads, CPS)
                         uint32_t* __restrict__ counters, const uint32_t* __restrict__ stop_word,
                         uint32_t token, uint32_t budget) {
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ uint32_t row_of[S], y_of[S];
+  __shared__ uint32_t row_of[S], y_of[S], next_of[S];
   const uint32_t src_row = 6u * static_cast<uint32_t>(dw);  // one source row, RGB
   const uint32_t out_row = 3u * static_cast<uint32_t>(dw);
   const uint32_t a_src = (2u * src_row + 127u) & ~127u;
@@ -193,16 +193,11 @@ __global__ void __launch_bounds__(kImgThreads, CPS)
     const int s = static_cast<int>(k % S);
     const uint32_t row = row_of[s];  // written >= S-1 barriers ago (or before the first)
     if (row >= rows) break;          // rows are grabbed in increasing order: all done
-    if (!PREEMPT && !triggered && row_of[(s + S - 1) % S] >= rows) {
-      // this CTA takes no further row: let a programmatic dependent launch
-      // (the next step on the stream) start its CTAs on the SMs we free
-      asm volatile("griddepcontrol.launch_dependents;");
-      triggered = true;
-    }
     const uint32_t y = y_of[s];
     // the elected thread's next row: the atomic's round trip overlaps this
     // row's compute instead of delaying the refill after the barrier
     const uint32_t next_row = tid == 0 ? take() : 0u;
+    if (tid == 0) next_of[s] = next_row;  // read after this row's barrier; rewritten S rows later
     uint8_t* st = smem + s * stage_bytes;
     const uint8_t* ra = st;
     const uint8_t* rb = st + src_row;
@@ -224,6 +219,12 @@ __global__ void __launch_bounds__(kImgThreads, CPS)
     // that last read it (issued S-1 rows ago) must have drained.
     if (tid == 0 && k + 1 >= S) frk::bulk_wait_read<S - 2>();
     __syncthreads();
+    if (!PREEMPT && !triggered && next_of[s] >= rows) {
+      // this CTA takes no further row: let a programmatic dependent launch
+      // (the next step on the stream) start its CTAs on the SMs we free
+      asm volatile("griddepcontrol.launch_dependents;");
+      triggered = true;
+    }
     if (tid == 0) {
       frk::bulk_s2g(dst + static_cast<uint64_t>(row) * out_row, orow, out_row, pol_stream);
       frk::bulk_commit();

@@ -72,6 +72,10 @@ class ImagePlan:
         check(glib().fr_img_plan_create(sw, sh, dw, dh, C.byref(h)))
         self._h = h
 
+    def set_overlap(self, on: bool = True):
+        """consecutive exact-2x launches may overlap (fr_img_plan_set_overlap)"""
+        check(glib().fr_img_plan_set_overlap(self._h, int(bool(on))))
+
     @property
     def path(self) -> int:
         out = C.c_int32()

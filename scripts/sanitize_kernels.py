@@ -19,6 +19,11 @@ wm = gpu.img_generate_watermark(320, 180, seed=2)
 dst = torch.empty((3, 180, 320, 3), dtype=torch.uint8, device="cuda")
 plan.run(src, dst, wm, stream=s)
 prep = plan.prepare(wm, stream=s)
+# overlapping consecutive launches (programmatic dependent launch, rotating counters)
+plan.set_overlap(True)
+for i in range(3):
+    plan.run_prepared(src[i:i + 1], dst[i:i + 1], prep, stream=s)
+plan.set_overlap(False)
 ctr = torch.zeros(8, dtype=torch.int32, device="cuda")
 plan.run_preemptible(src, dst, prep, ctr, max_rows=700, stream=s)
 gen = gpu.ImagePlan(300, 200, 170, 90)
@@ -47,8 +52,10 @@ p = gpu.SgdProblem(V=5000, E=40000, k=16, edge_seed=6, init_seed=7)
 p.step(0, 40000, stream=s)
 p.rmse()
 pu = gpu.SgdProblem(V=5000, E=40000, k=16, edge_seed=6, init_seed=7, by_user=True, window=4096)
+gpu.check(gpu.glib().fr_sgd_problem_set_overlap(pu._h, 1))   # overlapping consecutive steps
 pu.step(0, 17, stream=s)
-pu.step(17, 40000, stream=s)
+pu.step(17, 20000, stream=s)
+pu.step(20000, 40000, stream=s)
 pu.rmse()
 pb = gpu.SgdProblem(V=140000, E=300000, k=128, edge_seed=6, init_seed=7, by_user=True, window=65536)
 pb.step(0, 65536, stream=s)
