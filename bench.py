@@ -10,7 +10,7 @@ SURVEY.md §7); with --gpus N each rank is an independent replica (no
 collective on the data path) -> scaling "weak".
 
 Headline workload (BASELINE.json configs[1]): the image resize + watermark
-side task (64 synthetic 4K RGB frames -> 1080p, RGBA watermark, 32 frames per
+side task (64 synthetic 4K RGB frames -> 1080p, RGBA watermark, 16 frames per
 RunNextStep).  The same run also measures configs[0] (PageRank, RMAT-20,
 two pull iterations per step), configs[2] (Graph-SGD, Orkut shape, rank
 16, 2^22 edges per step), configs[3] (mixed, 3.6B-shaped stages) and the
@@ -52,7 +52,7 @@ SHAPE_36B = dict(layers=9, hidden=2880, tokens=8192, ffn_mult=4)    # nanoGPT-3.
 LAYERS_6B, HIDDEN_6B = 32, 4096                                       # nanoGPT-6B (configs[4])
 FRAMES = dict(sw=3840, sh=2160, dw=1920, dh=1080)
 BATCH = 64
-IMAGES_PER_STEP = int(os.environ.get("FR_IMAGES_PER_STEP", "32"))   # ~190 us steps (step size vs fill vs ΔT)
+IMAGES_PER_STEP = int(os.environ.get("FR_IMAGES_PER_STEP", "16"))   # ~95 us steps (step size vs fill vs ΔT)
 STEP_GROUP = int(os.environ.get("FR_STEP_GROUP", "3"))   # steps between one pair of timing events
 E2E_IMAGES_PER_STEP = 1
 E2E_RING = int(os.environ.get("FR_E2E_RING", "128"))   # device staging slots: the copy engines run ahead of the steps
