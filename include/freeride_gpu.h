@@ -57,9 +57,12 @@ enum fr_img_path { FR_IMG_PATH_GENERAL = 0, FR_IMG_PATH_TMA_2X = 1 };
 int fr_img_plan_create(int32_t sw, int32_t sh, int32_t dw, int32_t dh, fr_img_plan** out);
 /* Consecutive exact-2x launches on this plan may overlap (programmatic
  * dependent launch: a launch's CTAs start as soon as every CTA of the previous
- * one has taken its last row).  Only for callers whose launches read inputs
- * that the immediately preceding kernel on the stream did not produce (the
- * built-in image task: frames materialised at InitSideTask). */
+ * one has taken its last row).  Only a launch that directly follows another
+ * exact-2x step of this plan on the same stream is made a dependent; the
+ * watermark preparation, a preemptible launch or a call of this function
+ * restart the chain.  The caller promises not to enqueue a producer of a
+ * step's frames between two such steps (the built-in image task: frames
+ * materialised at InitSideTask, which also prepares the watermark). */
 int fr_img_plan_set_overlap(fr_img_plan* plan, int32_t overlap);
 int fr_img_plan_destroy(fr_img_plan* plan);
 int fr_img_plan_path(const fr_img_plan* plan, int32_t* path);
@@ -157,7 +160,12 @@ int fr_sgd_group_by_user(fr_sgd_problem* p, int64_t window_edges, void* stream);
 int fr_sgd_problem_set_kernel(fr_sgd_problem* p, int32_t by_user);
 /* Consecutive user-grouped steps may overlap (programmatic dependent launch:
  * a step's CTAs start while the previous step's last segments drain -- more
- * Hogwild concurrency, nothing else).  The built-in task sets it. */
+ * Hogwild concurrency, nothing else).  Only a step that directly follows
+ * another user-grouped step of this problem on the same stream is made a
+ * dependent: fr_sgd_reinit, fr_sgd_group_by_user, fr_sgd_sqerr/rmse, a
+ * per-edge step or a call of this function restart the chain.  The caller
+ * promises not to write the problem's buffers between two such steps.  The
+ * built-in task sets it. */
 int fr_sgd_problem_set_overlap(fr_sgd_problem* p, int32_t overlap);
 /* K4: *d_acc (device fp64) += sum of squared errors over [e_begin, e_end) */
 int fr_sgd_sqerr(const fr_sgd_problem* p, int64_t e_begin, int64_t e_end, double* d_acc,
@@ -286,6 +294,8 @@ typedef struct fr_sgd_task_config {
   float lambda;           /* 0.05 */
   int64_t total_steps;    /* <= 0: unbounded */
   int32_t layout;         /* FR_SGD_LAYOUT_COO (generated order) or FR_SGD_LAYOUT_BY_USER */
+  int32_t total_epochs;   /* > 0: stop after exactly this many passes over the edges (the
+                             step that ends the last epoch is cut there); <= 0: unbounded */
 } fr_sgd_task_config;
 #define FR_SGD_LAYOUT_COO 0
 #define FR_SGD_LAYOUT_BY_USER 1

@@ -513,7 +513,7 @@ GPU_PROTOTYPES.update({
 class SgdTaskConfigC(Struct):
     _fields_ = [("V", i32), ("k", i32), ("E", i64), ("edge_seed", u64), ("init_seed", u64),
                 ("edges_per_step", i64), ("eta", C.c_float), ("lambda_", C.c_float),
-                ("total_steps", i64), ("layout", i32)]
+                ("total_steps", i64), ("layout", i32), ("total_epochs", i32)]
 
 
 SGD_LAYOUT_COO, SGD_LAYOUT_BY_USER = 0, 1

@@ -148,9 +148,12 @@ int fr_build_schedule(const fr_pipeline_config* cfg, fr_op_event* ops, int64_t c
 int fr_extract_bubbles(const fr_pipeline_config* cfg, const fr_op_event* ops, int64_t n_ops,
                        const fr_tick* spans, fr_bubble* out, int64_t cap, int64_t* n_out) {
   if (!cfg || !n_out) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  if (n_ops < 0 || cap < 0) return frcapi::fail(FR_ERR_VALIDATION, "counts must be >= 0", n_ops < 0 ? "n_ops" : "cap");
+  if ((n_ops > 0 && !ops) || !spans || (cap > 0 && !out)) return frcapi::fail(FR_ERR_ARGUMENT, "null buffer");
   return frcapi::guard([&]() -> int {
     ScheduleTrace t;
     t.config = to_cfg(cfg);
+    t.config.validate();  // num_epochs >= 1 bounds the reads of spans
     t.ops.reserve(static_cast<std::size_t>(n_ops));
     for (int64_t i = 0; i < n_ops; ++i) t.ops.push_back(op_in(ops[i]));
     for (int e = 0; e < cfg->num_epochs; ++e) t.epoch_spans.push_back({spans[2 * e], spans[2 * e + 1]});
@@ -164,6 +167,7 @@ int fr_extract_bubbles(const fr_pipeline_config* cfg, const fr_op_event* ops, in
 
 int fr_bubble_rate(int32_t p, const fr_op_event* ops, int64_t n_ops, const fr_bubble* b,
                    int64_t nb, double* rate) {
+  if (!rate || (n_ops > 0 && !ops) || (nb > 0 && !b)) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
   return frcapi::guard([&]() -> int {
     std::vector<OpEvent> o;
     for (int64_t i = 0; i < n_ops; ++i) o.push_back(op_in(ops[i]));

@@ -351,6 +351,13 @@ struct fr_img_plan {
   uint32_t* d_ctr = nullptr;  // dynamic row scheduler {next row, CTAs done} x kImgCtrSlots; one stream at a time
   mutable uint32_t launches = 0;  // TMA launches so far: slot = launches % kImgCtrSlots
   bool overlap = false;           // fr_img_plan_set_overlap: consecutive launches may overlap
+  // A launch is a programmatic dependent only directly behind another
+  // exact-2x step of this plan on the same stream (nothing else of the plan
+  // in between): the watermark preparation, a preemptible launch or a new
+  // overlap setting break the chain, so the next step is fully serialised
+  // behind whatever produced its inputs.
+  mutable bool chained = false;
+  mutable cudaStream_t chain_stream = nullptr;
   int smem = 0;
   int sms = 0;
   size_t prepared_bytes() const {
@@ -428,6 +435,7 @@ int fr_img_plan_create(int32_t sw, int32_t sh, int32_t dw, int32_t dh, fr_img_pl
 int fr_img_plan_set_overlap(fr_img_plan* plan, int32_t overlap) {
   if (!plan) return frcapi::fail(FR_ERR_ARGUMENT, "null plan");
   plan->overlap = overlap != 0;
+  plan->chained = false;
   return FR_OK;
 }
 
@@ -456,6 +464,7 @@ int fr_img_prepare_watermark(const fr_img_plan* plan, const uint8_t* wm_rgba, vo
                              void* stream) {
   if (!plan || !wm_rgba || !prepared) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
   auto s = static_cast<cudaStream_t>(stream);
+  plan->chained = false;
   if (plan->path == FR_IMG_PATH_TMA_2X) {
     if (!aligned16(prepared)) return frcapi::fail(FR_ERR_UNSUPPORTED, "prepared watermark must be 16-byte aligned");
     const int64_t total = static_cast<int64_t>(plan->dh) * (plan->dw >> 3) * 4;
@@ -490,7 +499,9 @@ int fr_img_resize_watermark_prepared(const fr_img_plan* plan, const uint8_t* src
       const char* e = std::getenv("FR_IMG_PDL");  // experiment override: 0 / 1
       return e ? std::atoi(e) : -1;
     }();
-    const bool pdl = pdl_env >= 0 ? pdl_env != 0 : plan->overlap;
+    const bool pdl = (pdl_env >= 0 ? pdl_env != 0 : plan->overlap) && plan->chained && plan->chain_stream == s;
+    plan->chained = true;
+    plan->chain_stream = s;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kImgThreads);
@@ -535,6 +546,7 @@ int fr_img_resize_watermark_preemptible(const fr_img_plan* plan, const uint8_t* 
   const uint32_t* word = preempt && preempt->stop_word ? preempt->stop_word : counters + 5;
   const uint32_t token = preempt && preempt->stop_word ? preempt->token : 0xFFFFFFFFu;
   auto k = plan->stages == 2 ? img_resize2x_wm_tma<2, true, 3> : img_resize2x_wm_tma<3, true, 2>;
+  plan->chained = false;
   k<<<grid, kImgThreads, plan->smem, static_cast<cudaStream_t>(stream)>>>(
       src, dst, static_cast<const uint4*>(prepared), plan->dw, plan->dh, static_cast<uint32_t>(rows),
       counters, word, token, static_cast<uint32_t>(max_rows));

@@ -425,6 +425,13 @@ struct fr_sgd_problem {
   int sms = 148;
   bool grouped = false;  // edges stable-sorted by u (fr_sgd_group_by_user)
   bool overlap = false;  // fr_sgd_problem_set_overlap: consecutive steps may overlap (Hogwild)
+  // Programmatic dependent launch is only safe behind another user step of
+  // this problem: any other launch that writes (init, re-layout) or reads
+  // (sqerr) the problem's buffers breaks the chain, so the next step runs
+  // fully serialised behind it.
+  mutable bool chained = false;
+  mutable cudaStream_t chain_stream = nullptr;
+  void break_chain() const { chained = false; }
   int64_t max_deg = 0;   // largest number of ratings touching one vertex (u or v side)
 };
 
@@ -530,7 +537,10 @@ void launch_user_step(fr_sgd_problem* p, int64_t a, int64_t b, float eta, float 
     const char* e = std::getenv("FR_SGD_OVERLAP");  // A/B override: 0 / 1
     return e ? std::atoi(e) : -1;
   }();
-  cfg.numAttrs = (overlap_env >= 0 ? overlap_env != 0 : p->overlap) ? 1 : 0;
+  const bool want = overlap_env >= 0 ? overlap_env != 0 : p->overlap;
+  cfg.numAttrs = (want && p->chained && p->chain_stream == s) ? 1 : 0;
+  p->chained = true;
+  p->chain_stream = s;
   cudaLaunchKernelEx(&cfg, sgd_user_kernel<K, D>, static_cast<const int32_t*>(p->u), static_cast<const int32_t*>(p->v),
                      static_cast<const float*>(p->r), p->L, a, b, seg, eta, lam);
 }
@@ -645,6 +655,7 @@ int fr_sgd_reinit(fr_sgd_problem* p, uint64_t init_seed, void* stream) {
   if (!p) return frcapi::fail(FR_ERR_ARGUMENT, "null problem");
   const int64_t n = static_cast<int64_t>(p->V) * p->K;
   const float scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(p->K))) * (1.0f / 16777216.0f);
+  p->break_chain();
   sgd_init_kernel<<<grid_for(n, 256, 16), 256, 0, static_cast<cudaStream_t>(stream)>>>(n, scale, init_seed, p->L);
   FR_CUDA_LAUNCHED("sgd_init");
   return FR_OK;
@@ -667,6 +678,7 @@ int fr_sgd_step(fr_sgd_problem* p, int64_t e_begin, int64_t e_end, float eta, fl
     FR_CUDA_LAUNCHED("sgd_user_step");
     return FR_OK;
   }
+  p->break_chain();
   switch (p->K) {
     case 4: launch_step<4>(p, e_begin, e_end, eta, lambda, s); break;
     case 8: launch_step<8>(p, e_begin, e_end, eta, lambda, s); break;
@@ -687,6 +699,7 @@ int fr_sgd_group_by_user(fr_sgd_problem* p, int64_t window_edges, void* stream) 
     return FR_OK;
   }
   if (p->E > INT32_MAX) return frcapi::fail(FR_ERR_VALIDATION, "grouping needs E < 2^31", "E");
+  p->break_chain();
   auto s = static_cast<cudaStream_t>(stream);
   const int n = static_cast<int>(p->E);
   const int32_t P = sgd_item_blocks(p->V, p->K);
@@ -778,6 +791,7 @@ int fr_sgd_group_by_user(fr_sgd_problem* p, int64_t window_edges, void* stream) 
 int fr_sgd_problem_set_overlap(fr_sgd_problem* p, int32_t overlap) {
   if (!p) return frcapi::fail(FR_ERR_ARGUMENT, "null problem");
   p->overlap = overlap != 0;
+  p->break_chain();
   return FR_OK;
 }
 
@@ -793,6 +807,7 @@ int fr_sgd_sqerr(const fr_sgd_problem* p, int64_t e_begin, int64_t e_end, double
     return frcapi::fail(FR_ERR_VALIDATION, "edge range outside [0, E]", "edges");
   if (e_begin == e_end) return FR_OK;
   auto s = static_cast<cudaStream_t>(stream);
+  p->break_chain();
   switch (p->K) {
     case 4: launch_sqerr<4>(p, e_begin, e_end, d_acc, s); break;
     case 8: launch_sqerr<8>(p, e_begin, e_end, d_acc, s); break;
@@ -845,6 +860,8 @@ struct SgdTask {
   fr_sgd_task_config cfg{};
   fr_sgd_problem* p = nullptr;
   int64_t cursor = 0, epochs = 0;
+  int64_t launched = 0;   // steps since InitSideTask
+  int64_t last_step = 0;  // total_epochs: the step that ended the last epoch (1-based)
 };
 
 int sgd_task_create(void* u) {
@@ -861,13 +878,17 @@ int sgd_task_init(void* u, void* stream) {
   auto* t = static_cast<SgdTask*>(u);
   t->cursor = 0;
   t->epochs = 0;
+  t->launched = 0;
+  t->last_step = 0;
   return fr_sgd_reinit(t->p, t->cfg.init_seed, stream);
 }
 
 int sgd_task_step(void* u, void* stream) {
   auto* t = static_cast<SgdTask*>(u);
   int64_t left = t->cfg.edges_per_step;
-  while (left > 0) {
+  ++t->launched;
+  const bool bounded = t->cfg.total_epochs > 0;
+  while (left > 0 && !(bounded && t->epochs >= t->cfg.total_epochs)) {
     const int64_t n = std::min<int64_t>(left, t->p->E - t->cursor);
     const int rc = fr_sgd_step(t->p, t->cursor, t->cursor + n, t->cfg.eta, t->cfg.lambda, stream);
     if (rc != FR_OK) return rc;
@@ -876,6 +897,7 @@ int sgd_task_step(void* u, void* stream) {
     if (t->cursor == t->p->E) {
       t->cursor = 0;
       t->epochs++;
+      if (bounded && t->epochs == t->cfg.total_epochs) t->last_step = t->launched;
     }
   }
   return FR_OK;
@@ -883,7 +905,8 @@ int sgd_task_step(void* u, void* stream) {
 
 int sgd_task_finished(void* u, int64_t done, int32_t* out) {
   auto* t = static_cast<SgdTask*>(u);
-  *out = t->cfg.total_steps > 0 && done >= t->cfg.total_steps;
+  *out = (t->cfg.total_steps > 0 && done >= t->cfg.total_steps) ||
+         (t->last_step > 0 && done >= t->last_step);
   return FR_OK;
 }
 

@@ -733,7 +733,12 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
     }
     // 1. bubble signals from the device
     volatile RingSlot* sl = ring + (static_cast<std::uint64_t>(next_slot) & (kRingSlots - 1));
-    if (next_slot < n_events && sl->seq == static_cast<std::uint32_t>(next_slot + 1)) {
+    // acquire: the payload (code, t_ns) is read only after the published seq
+    // (the device writes it behind a system-scope fence); on a weakly ordered
+    // host (aarch64) plain loads could pair a stale payload with a fresh seq
+    if (next_slot < n_events &&
+        __atomic_load_n(const_cast<std::uint32_t*>(&sl->seq), __ATOMIC_ACQUIRE) ==
+            static_cast<std::uint32_t>(next_slot + 1)) {
       const std::uint32_t code = sl->code;
       const auto t_dev = static_cast<std::int64_t>(sl->t_ns);
       const std::int64_t seen = host_ns();

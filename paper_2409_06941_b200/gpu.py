@@ -373,6 +373,11 @@ class SgdProblem:
     def reinit(self, seed=3, stream=None):
         check(glib().fr_sgd_reinit(self._h, seed, _stream(stream)))
 
+    def set_overlap(self, on: bool = True):
+        """consecutive user-grouped steps on one stream may overlap
+        (fr_sgd_problem_set_overlap; the built-in task's setting)"""
+        check(glib().fr_sgd_problem_set_overlap(self._h, int(bool(on))))
+
     def step(self, e_begin, e_end, eta=0.01, lam=0.05, stream=None):
         check(glib().fr_sgd_step(self._h, e_begin, e_end, eta, lam, _stream(stream)))
 
@@ -405,7 +410,7 @@ class SgdTask:
 
     def __init__(self, V=3072441, E=117185083, k=16, edge_seed=2, init_seed=3,
                  edges_per_step=1 << 21, eta=0.01, lam=0.05, total_steps=0, by_user=True,
-                 problem: "SgdProblem | None" = None):
+                 problem: "SgdProblem | None" = None, total_epochs=0):
         """problem=: harvest over the caller's ratings (SgdProblem.from_edges); the
         task takes the problem over (fr_sgd_task_create_from_problem)"""
         if problem is not None:
@@ -413,7 +418,8 @@ class SgdTask:
         self.cfg = A.SgdTaskConfigC(V=V, k=k, E=E, edge_seed=edge_seed, init_seed=init_seed,
                                     edges_per_step=edges_per_step, eta=eta, lambda_=lam,
                                     total_steps=total_steps,
-                                    layout=A.SGD_LAYOUT_BY_USER if by_user else A.SGD_LAYOUT_COO)
+                                    layout=A.SGD_LAYOUT_BY_USER if by_user else A.SGD_LAYOUT_COO,
+                                    total_epochs=total_epochs)
         self.vt = A.SideTaskVTableC()
         self.user = C.c_void_p()
         if problem is None:

@@ -235,3 +235,77 @@ def test_task_over_caller_ratings_in_bubbles(g):
     assert p2.rmse() < r0
     h.close()
 
+
+
+# ---- the benchmarked Graph-SGD path (bench.py SGD: by-user layout, rounds of
+# 2^22 edges, overlapping PDL steps, step groups of 3) at the Orkut shape for
+# SURVEY §8(d) C3's 5 epochs, against the sequential oracle in the same layout
+BENCH_STEP = 1 << 22
+ORKUT = (3072441, 117185083)
+
+
+@pytest.fixture(scope="module")
+def orkut_oracle_rmse(sidetask_oracle):
+    """RMSE of the sequential oracle after each of 5 epochs (by-user layout, rounds of 2^22 edges)"""
+    V, E = ORKUT
+    u, v, r = sidetask_oracle.sgd_group_by_user(V, *sidetask_oracle.sgd_edges(V, E, seed=2), window=BENCH_STEP)
+    L = sidetask_oracle.sgd_init(V, 16, seed=3)
+    out = []
+    for _ in range(5):
+        sidetask_oracle.sgd_epoch(u, v, r, L, ETA, LAM, nthreads=1)
+        out.append(sidetask_oracle.sgd_rmse(u, v, r, L))
+    return out
+
+
+def test_overlapped_task_steps_match_oracle_orkut(g, orkut_oracle_rmse):
+    """standalone: the task's stepping (2^22-edge steps straddling epochs,
+    fr_sgd_problem_set_overlap(1), back to back on one low-priority stream)
+    for exactly 5 epochs: |dRMSE| <= 1e-3 vs the sequential oracle at every
+    epoch from the second on (epoch 1: the by-user outlier)"""
+    import torch
+    V, E = ORKUT
+    p = g.SgdProblem(V=V, E=E, k=16, edge_seed=2, init_seed=3, by_user=True, window=BENCH_STEP)
+    p.set_overlap(True)
+    s = g.low_priority_stream()
+    cur, ep, got = 0, 0, []
+    while ep < 5:
+        left = BENCH_STEP
+        while left > 0 and ep < 5:
+            n = min(left, E - cur)
+            p.step(cur, cur + n, ETA, LAM, stream=s)
+            cur, left = cur + n, left - n
+            if cur == E:
+                cur, ep = 0, ep + 1
+                torch.cuda.current_stream().wait_stream(s)
+                got.append(p.rmse())   # breaks the PDL chain: the next step waits for it
+    print("overlapped orkut", got, orkut_oracle_rmse)
+    for e in range(1, 5):
+        assert abs(got[e] - orkut_oracle_rmse[e]) <= 1e-3, (e, got[e], orkut_oracle_rmse[e])
+    assert abs(got[0] - orkut_oracle_rmse[0]) <= 4e-3
+
+
+def test_sgd_task_in_bubbles_bench_settings_orkut(g, orkut_oracle_rmse):
+    """the in-bubble task exactly as bench.py runs it (stage of the
+    nanoGPT-1.2B-shaped 4-stage pipeline, step groups of 3, 2^22-edge
+    overlapping steps) until it completes 5 epochs: RMSE within 1e-3 of the
+    sequential oracle after 5 epochs"""
+    V, E = ORKUT
+    h = g.Harness(num_stages=4, num_micro_batches=4, stage=0, layers=6, hidden=2048, tokens=8192,
+                  ffn_mult=4, step_group=3, profile_epochs=1, profile_reps=2)
+    task = g.SgdTask(V=V, E=E, k=16, edges_per_step=BENCH_STEP, total_epochs=5)
+    ok, _ = h.submit("sgd", task, profile_steps=8)
+    assert ok
+    steps = 0
+    for _ in range(30):
+        r = h.run(2, True)
+        steps += r["steps_completed"]
+        if h.task_status("sgd")["disposition"] == "completed":
+            break
+    st = h.task_status("sgd")
+    assert st["disposition"] == "completed", (st, steps)
+    prob, epochs = task.problem()
+    assert epochs == 5
+    got = prob.rmse()
+    print("in-bubble orkut", steps, got, orkut_oracle_rmse[4])
+    assert abs(got - orkut_oracle_rmse[4]) <= 1e-3, (got, orkut_oracle_rmse[4])
+    h.close()
