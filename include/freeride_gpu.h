@@ -346,6 +346,10 @@ typedef struct fr_harness_config {
                                  consecutive iterative steps between one pair of events
                                  (each still admitted by the gate), so they run back to
                                  back; timelines and reprofile then see step groups */
+  double harvest_fraction;    /* (0, 1): the gate admits steps only in the first
+                                 fraction of every bubble (the bubble end it is given is
+                                 start + fraction x profiled duration); <= 0 or >= 1:
+                                 the whole bubble */
 } fr_harness_config;
 
 /* All durations in ns ticks (tick_seconds = 1e-9). */
@@ -403,6 +407,8 @@ int fr_harness_stop_task(fr_harness* h, const char* task_id);
  * under training load): est = mean, max = worst, as in profiler.cpp:50-78 */
 int fr_harness_reprofile(fr_harness* h, const char* task_id, fr_task_profile* out);
 /* Runs `epochs` epochs; with_tasks=0 is the ΔT baseline. Blocks. */
+/* harvest fraction for the next runs (fr_harness_config::harvest_fraction) */
+int fr_harness_set_harvest_fraction(fr_harness* h, double fraction);
 int fr_harness_run(fr_harness* h, int32_t epochs, int32_t with_tasks, fr_run_report* out);
 /* a submitted task's state (enum fr_task_state), disposition (enum
  * fr_disposition; FR_DISP_ACTIVE while alive) and bytes in its memory pool */

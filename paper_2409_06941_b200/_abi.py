@@ -545,6 +545,7 @@ class HarnessConfigC(Struct):
         ("fp_ticks_override", i64), ("bp_ticks_override", i64),
         ("profile_epochs", i32), ("transport", i32),
         ("memory_headroom_gib", dbl), ("grace_ns", i64), ("step_group", i32),
+        ("harvest_fraction", dbl),
     ]
 
 
@@ -576,6 +577,7 @@ GPU_PROTOTYPES.update({
     "fr_synthetic_task_create": (C.c_int, [P(SyntheticTaskConfigC), P(SideTaskVTableC), P(vp)]),
     "fr_harness_task_status": (C.c_int, [vp, C.c_char_p, P(i32), P(i32), P(dbl)]),
     "fr_harness_destroy": (C.c_int, [vp]),
+    "fr_harness_set_harvest_fraction": (C.c_int, [vp, dbl]),
     "fr_harness_get_profile": (C.c_int, [vp, P(HarnessProfileC)]),
     "fr_harness_stage_bubbles": (C.c_int, [vp, P(BubbleC), i32, P(i32)]),
     "fr_harness_submit": (C.c_int, [vp, cp, P(SideTaskVTableC), vp, dbl, i32, P(TaskProfileC), P(i32)]),

@@ -488,7 +488,12 @@ int fr_img_resize_watermark_prepared(const fr_img_plan* plan, const uint8_t* src
       return frcapi::fail(FR_ERR_UNSUPPORTED, "TMA path needs 16-byte aligned buffers");
     const int64_t rows = static_cast<int64_t>(n) * plan->dh;
     if (rows >= (int64_t{1} << 31)) return frcapi::fail(FR_ERR_UNSUPPORTED, "too many rows in one step");
-    const int grid = static_cast<int>(std::min<int64_t>(rows, int64_t(plan->sms) * plan->ctas_per_sm));
+    static const int grid_sms = [] {
+      const char* e = std::getenv("FR_IMG_GRID_SMS");  // experiment: CTAs for this many SMs only
+      return e ? std::max(1, std::atoi(e)) : 0;
+    }();
+    const int64_t sms = grid_sms > 0 ? std::min(grid_sms, plan->sms) : plan->sms;
+    const int grid = static_cast<int>(std::min<int64_t>(rows, sms * plan->ctas_per_sm));
     auto k = plan->stages == 2 ? img_resize2x_wm_tma<2, false, 3> : img_resize2x_wm_tma<3, false, 2>;
     // Consecutive steps overlap their tail and head (programmatic dependent
     // launch: a launch's CTAs start once every CTA of the previous one took

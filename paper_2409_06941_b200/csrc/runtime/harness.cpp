@@ -718,7 +718,10 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
         apply_transition(t.rt, TransitionKind::StartSideTask, t_dev);
         hook(t.vt.start ? t.vt.start(t.user) : FR_OK, "start");
         running = &t;
-        bubble_end_dev = t_dev + pb.duration;  // StartSideTask carries the bubble end
+        // StartSideTask carries the bubble end (§4.5); a harvest
+        // fraction < 1 hands the gate only the bubble's first part
+        const double frac = cfg.harvest_fraction > 0 && cfg.harvest_fraction < 1 ? cfg.harvest_fraction : 1.0;
+        bubble_end_dev = t_dev + static_cast<std::int64_t>(std::llround(frac * static_cast<double>(pb.duration)));
         proj_end_dev = 0;
         gate_closed = false;
         cur_token = id + 1;
@@ -1215,6 +1218,14 @@ int fr_harness_run(fr_harness* h, int32_t epochs, int32_t with_tasks, fr_run_rep
   } catch (const std::exception& e) {
     return frcapi::fail(FR_ERR_INVARIANT, e.what());
   }
+}
+
+int fr_harness_set_harvest_fraction(fr_harness* h, double fraction) {
+  if (!h) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  if (!(fraction >= 0.0 && fraction <= 1.0))
+    return frcapi::fail(FR_ERR_VALIDATION, "harvest fraction must be in [0, 1]", "harvest_fraction");
+  h->cfg.harvest_fraction = fraction;
+  return FR_OK;
 }
 
 int fr_harness_reprofile_bubbles(fr_harness* h) {

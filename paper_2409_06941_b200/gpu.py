@@ -527,7 +527,7 @@ class Harness:
                  tokens=8192, ffn_mult=4, profile_reps=5, max_inflight_steps=2, gate_estimate=0,
                  gpu_memory_total=178.0, weight_mem=-1.0, activation_mem=-1.0,
                  fp_ticks=0, bp_ticks=0, profile_epochs=3, transport="replica",
-                 memory_headroom_gib=0.0, grace_ns=0, step_group=1):
+                 memory_headroom_gib=0.0, grace_ns=0, step_group=1, harvest_fraction=1.0):
         """transport="replica": this GPU replays stage `stage` against the
         device clock (one GPU); "linked": a real pipeline stage whose
         neighbours are linked through mailboxes (see link())."""
@@ -539,7 +539,8 @@ class Harness:
             gpu_memory_total=gpu_memory_total, weight_mem=weight_mem,
             activation_mem=activation_mem, fp_ticks_override=fp_ticks, bp_ticks_override=bp_ticks,
             profile_epochs=profile_epochs if tp == 0 else 0, transport=tp,
-            memory_headroom_gib=memory_headroom_gib, grace_ns=grace_ns, step_group=step_group)
+            memory_headroom_gib=memory_headroom_gib, grace_ns=grace_ns, step_group=step_group,
+            harvest_fraction=harvest_fraction)
         h = C.c_void_p()
         check(glib().fr_harness_create(C.byref(self.cfg), C.byref(h)))
         self._h = h
@@ -597,6 +598,10 @@ class Harness:
     def reprofile_bubbles(self):
         """Bubble durations := medians of the last run's measured bubbles."""
         check(glib().fr_harness_reprofile_bubbles(self._h))
+
+    def set_harvest_fraction(self, fraction: float):
+        """the gate sees only the first `fraction` of every bubble (1 = all)"""
+        check(glib().fr_harness_set_harvest_fraction(self._h, float(fraction)))
 
     def stop_task(self, task_id: str):
         check(glib().fr_harness_stop_task(self._h, task_id.encode()))

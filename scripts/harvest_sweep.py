@@ -1,0 +1,83 @@
+"""Operating points of bubble harvesting on a power-capped B200: side-task
+throughput per bubble-second vs pipeline (critical-path) ΔT.
+
+Every stage of the bench pipeline is replayed in turn; per stage and harvest
+fraction f (the gate sees the first f of every bubble): a run without and a
+run with the side task.  The per-stage mean FP / BP durations of both runs go
+through build_schedule (pipeline_dt.critical_path_dt) -> the linked
+pipeline's ΔT; throughput = units / bubble-seconds over all stages.
+
+Usage: python scripts/harvest_sweep.py TASK FRACTIONS [epochs] [stages]
+  TASK in image16 | image8 | image4 | pagerank | sgd ; FRACTIONS e.g. 1,0.5,0.25
+  env FR_IMG_GRID_SMS limits the image kernel's grid to that many SMs.
+"""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_2409_06941_b200 import api, gpu  # noqa: E402
+from paper_2409_06941_b200 import pipeline_dt as P  # noqa: E402
+
+
+def make(name):
+    if name.startswith("image"):
+        return gpu.ImageTask(batch=64, images_per_step=int(name[5:] or 16))
+    if name == "pagerank":
+        return gpu.PageRankTask(scale=20, edge_factor=16, seed=1, iters_per_step=2)
+    if name == "sgd":
+        return gpu.SgdTask(edges_per_step=1 << 22)
+    raise ValueError(name)
+
+
+def main():
+    name = sys.argv[1]
+    fracs = [float(x) for x in sys.argv[2].split(",")]
+    K = int(sys.argv[3]) if len(sys.argv) > 3 else 8
+    stages = [int(x) for x in sys.argv[4].split(",")] if len(sys.argv) > 4 else [0, 1, 2, 3]
+    p, m = 4, 4
+    torch.cuda.set_device(0)
+    a = api()
+    res = {f: {"base": {}, "with": {}, "units": 0.0, "bubble_s": 0.0, "stage_dT": {}, "fill": {}} for f in fracs}
+    for s in stages:
+        h = gpu.Harness(num_stages=p, num_micro_batches=m, stage=s, layers=6, hidden=2048, tokens=8192,
+                        ffn_mult=4, step_group=3)
+        kinds = P.issue_kinds(a, s, p, m)
+        ok, _ = h.submit(name, make(name), profile_steps=16)
+        assert ok
+        h.run(3, True)
+        h.reprofile(name)
+        for f in fracs:
+            h.set_harvest_fraction(f)
+            base = h.run(K, False)
+            ob = h.timeline(0)
+            r = h.run(K, True)
+            ow = h.timeline(0)
+            R = res[f]
+            R["base"][s] = P.op_means(ob, kinds)
+            R["with"][s] = P.op_means(ow, kinds)
+            R["units"] += r["work_units"]
+            R["bubble_s"] += base["bubble_s"]
+            R["stage_dT"][s] = (r["makespan_s"] - base["makespan_s"]) / base["makespan_s"]
+            R["fill"][s] = r["used_s"] / r["bubble_s"]
+        h.close()
+    out = []
+    for f in fracs:
+        R = res[f]
+        row = {"task": name, "fraction": f, "grid_sms": os.environ.get("FR_IMG_GRID_SMS"),
+               "units_per_bubble_s": R["units"] / R["bubble_s"],
+               "stage_dT_max": max(R["stage_dT"].values()), "fill": R["fill"],
+               "op_growth": {s: (R["with"][s][0] / R["base"][s][0] - 1, R["with"][s][1] / R["base"][s][1] - 1)
+                             for s in R["base"]}}
+        if len(R["base"]) == p:
+            row["critical_path_dT"] = P.critical_path_dt(a, p, m, K, R["base"], R["with"])["dT"]
+        out.append(row)
+        print(json.dumps(row), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -260,8 +260,10 @@ def orkut_oracle_rmse(sidetask_oracle):
 def test_overlapped_task_steps_match_oracle_orkut(g, orkut_oracle_rmse):
     """standalone: the task's stepping (2^22-edge steps straddling epochs,
     fr_sgd_problem_set_overlap(1), back to back on one low-priority stream)
-    for exactly 5 epochs: |dRMSE| <= 1e-3 vs the sequential oracle at every
-    epoch from the second on (epoch 1: the by-user outlier)"""
+    for exactly 5 epochs: |dRMSE| <= 1e-3 vs the sequential oracle after
+    every epoch (measured <= 5e-5: with rounds of 2^22 edges a round holds
+    about one 64-edge piece of any user, so the epoch-1 by-user outlier of
+    small windows does not arise)"""
     import torch
     V, E = ORKUT
     p = g.SgdProblem(V=V, E=E, k=16, edge_seed=2, init_seed=3, by_user=True, window=BENCH_STEP)
@@ -279,9 +281,8 @@ def test_overlapped_task_steps_match_oracle_orkut(g, orkut_oracle_rmse):
                 torch.cuda.current_stream().wait_stream(s)
                 got.append(p.rmse())   # breaks the PDL chain: the next step waits for it
     print("overlapped orkut", got, orkut_oracle_rmse)
-    for e in range(1, 5):
+    for e in range(5):
         assert abs(got[e] - orkut_oracle_rmse[e]) <= 1e-3, (e, got[e], orkut_oracle_rmse[e])
-    assert abs(got[0] - orkut_oracle_rmse[0]) <= 4e-3
 
 
 def test_sgd_task_in_bubbles_bench_settings_orkut(g, orkut_oracle_rmse):
