@@ -64,6 +64,10 @@ int fr_img_plan_create(int32_t sw, int32_t sh, int32_t dw, int32_t dh, fr_img_pl
  * step's frames between two such steps (the built-in image task: frames
  * materialised at InitSideTask, which also prepares the watermark). */
 int fr_img_plan_set_overlap(fr_img_plan* plan, int32_t overlap);
+/* launches of this plan occupy at most `sms` SMs (0 = all): the grid is
+ * sized for that many SMs (rows are handed out dynamically, so any grid is
+ * correct) */
+int fr_img_plan_set_max_sms(fr_img_plan* plan, int32_t sms);
 int fr_img_plan_destroy(fr_img_plan* plan);
 int fr_img_plan_path(const fr_img_plan* plan, int32_t* path);
 /* n images: src [n][sh][sw][3] u8, dst [n][dh][dw][3] u8, wm [dh][dw][4] u8
@@ -167,6 +171,8 @@ int fr_sgd_problem_set_kernel(fr_sgd_problem* p, int32_t by_user);
  * promises not to write the problem's buffers between two such steps.  The
  * built-in task sets it. */
 int fr_sgd_problem_set_overlap(fr_sgd_problem* p, int32_t overlap);
+/* steps occupy at most `sms` SMs (0 = all): fewer lane groups in flight */
+int fr_sgd_problem_set_max_sms(fr_sgd_problem* p, int32_t sms);
 /* K4: *d_acc (device fp64) += sum of squared errors over [e_begin, e_end) */
 int fr_sgd_sqerr(const fr_sgd_problem* p, int64_t e_begin, int64_t e_end, double* d_acc,
                  void* stream);
@@ -216,6 +222,13 @@ typedef struct fr_side_task_vtable {
    * kernels poll) without synchronising.  The worker then drains the task's
    * stream, calls stop and releases the task's memory pool. */
   int (*cancel)(void* user);
+  /* SM budget (optional): from now on the task's kernels occupy at most `sms`
+   * SMs (0 = all).  On a power-capped B200 every joule a side task spends in
+   * a bubble is taken from the boost the pipeline's GEMMs get from their idle
+   * bubbles; the same bytes moved by fewer SMs cost far less power, so the
+   * harness bounds the side task's SMs to hold the pipeline's ΔT (DESIGN.md
+   * §5c).  The harness calls it before profiling and on every change. */
+  int (*set_sm_budget)(void* user, int32_t sms);
 } fr_side_task_vtable;
 
 /* Built-in side tasks (kernels above) behind the vtable. */
@@ -260,6 +273,8 @@ typedef struct fr_synthetic_task_config {
   int64_t total_steps;          /* <= 0: unbounded */
   int32_t cooperative;
   int32_t reserved;
+  int64_t init_ns;              /* InitSideTask: a GPU spin this long (0: none) -- an init
+                                   that outlasts its bubble trips the init guard */
 } fr_synthetic_task_config;
 int fr_synthetic_task_create(const fr_synthetic_task_config* cfg, fr_side_task_vtable* vt,
                              void** user);
@@ -350,6 +365,11 @@ typedef struct fr_harness_config {
                                  fraction of every bubble (the bubble end it is given is
                                  start + fraction x profiled duration); <= 0 or >= 1:
                                  the whole bubble */
+  int64_t reclamation_delay_ns; /* LimitConfig::reclamation_delay (limits.hpp:12): a killed
+                                   task's pool pages go back to the device this long after
+                                   the kill (<= 0: at once) */
+  int32_t side_sms;           /* SM budget of the side tasks' kernels (set_sm_budget;
+                                 0 = all SMs) */
 } fr_harness_config;
 
 /* All durations in ns ticks (tick_seconds = 1e-9). */
@@ -384,6 +404,8 @@ typedef struct fr_run_report {
   int64_t kills;                /* tasks killed in this run (both reasons) */
   int64_t kills_oom;            /* check_memory OomKill (limits.hpp:20) */
   int64_t kills_pause_timeout;  /* framework_enforce Kill (limits.hpp:34) */
+  int64_t kills_init_timeout;   /* ArmInitGuard fired with InitSideTask still running
+                                   (manager.hpp:58, KillReason::InitTimeout) */
 } fr_run_report;
 
 int fr_harness_create(const fr_harness_config* cfg, fr_harness** out);
@@ -406,14 +428,64 @@ int fr_harness_stop_task(fr_harness* h, const char* task_id);
 /* profile_task from the task's steps in the last run (measured in bubbles,
  * under training load): est = mean, max = worst, as in profiler.cpp:50-78 */
 int fr_harness_reprofile(fr_harness* h, const char* task_id, fr_task_profile* out);
-/* Runs `epochs` epochs; with_tasks=0 is the ΔT baseline. Blocks. */
 /* harvest fraction for the next runs (fr_harness_config::harvest_fraction) */
 int fr_harness_set_harvest_fraction(fr_harness* h, double fraction);
+/* side-task SM budget for the next runs (fr_harness_config::side_sms); the
+ * tasks' step estimates change with it: re-profile (fr_harness_reprofile)
+ * after a run at the new budget */
+int fr_harness_set_side_sms(fr_harness* h, int32_t sms);
+/* Runs `epochs` epochs; with_tasks=0 is the ΔT baseline. Blocks. */
 int fr_harness_run(fr_harness* h, int32_t epochs, int32_t with_tasks, fr_run_report* out);
 /* a submitted task's state (enum fr_task_state), disposition (enum
  * fr_disposition; FR_DISP_ACTIVE while alive) and bytes in its memory pool */
 int fr_harness_task_status(const fr_harness* h, const char* task_id, int32_t* state,
                            int32_t* disposition, double* memory_used_gib);
+/* bytes the task's pool holds: in use, and reserved (kept mapped until the
+ * task is stopped / killed and its reclamation delay has passed) */
+int fr_harness_task_memory(const fr_harness* h, const char* task_id, double* used_gib,
+                           double* reserved_gib);
+/* The last run with tasks as the reference's parity object (RunTrace,
+ * engine.hpp:75-92), recorded on the GPU: this stage's ops (CUDA events),
+ * its bubbles, submits / assigns, every transition the worker applied, Init
+ * and Step activities, kills and dispositions, in ns from the run's start
+ * (ticks of 1e-9 s).  `measured` is set: fr_run_trace_check then skips the
+ * simulated-only invariants (configured op durations, absent stages, op /
+ * side-kernel exclusivity) and allows `tolerance` ns between the host-clock
+ * transition stamps and the device-event activity times.  Caller destroys
+ * it with fr_run_trace_destroy. */
+int fr_harness_run_trace(const fr_harness* h, fr_run_trace** out);
+/* Every program-directed gate decision of the last run (iterative_run,
+ * task.cpp:89-100), in order: the inputs the worker gave it and its answer,
+ * so the decisions can be replayed through the reference's function. */
+typedef struct fr_gate_record {
+  fr_tick now;          /* projected device start of the step, ns from run start */
+  fr_tick bubble_end;   /* bubble end handed over at StartSideTask, ns from run start */
+  double est_seconds;   /* the profiled estimate (GateEstimate) */
+  fr_tick step_ticks;   /* actual_step_ticks argument (= the estimate in ticks) */
+  int32_t run;          /* 1: admitted (RunNextStep dispatched) */
+  int32_t signal;       /* index into the signal log of the BubbleStarted that started it */
+  fr_tick step_end;     /* IterativeDecision::step_end */
+  char task[FR_TASK_ID_MAX];
+} fr_gate_record;
+/* Every Alg. 2 call of the last run (on_bubble_started / on_bubble_ended,
+ * manager.cpp:37-70), in call order, with the view of the task it looked up
+ * and the actions it returned. */
+typedef struct fr_signal_record {
+  fr_tick t;            /* signal time (device clock), ns from run start */
+  int32_t kind;         /* 0 BubbleStarted, 1 BubbleEnded */
+  int32_t epoch;
+  int32_t bubble;       /* index into fr_harness_stage_bubbles */
+  int32_t looked_up;    /* 1: the manager consulted `task` (view below) */
+  fr_tick duration;     /* profiled bubble duration carried by BubbleStarted */
+  int32_t view_state;   /* enum fr_task_state of `task` at the call */
+  int32_t view_initializing;
+  int32_t n_actions;
+  int32_t actions[4];   /* ManagerActionKind codes, in order */
+  int32_t deferred;     /* 1: a BubbleStarted held until the previous pause landed */
+  char task[FR_TASK_ID_MAX];
+} fr_signal_record;
+int fr_harness_gate_log(const fr_harness* h, fr_gate_record* out, int64_t cap, int64_t* n);
+int fr_harness_signal_log(const fr_harness* h, fr_signal_record* out, int64_t cap, int64_t* n);
 /* raw timelines of the last run, seconds from run start, (start, end) pairs */
 int fr_harness_timeline(const fr_harness* h, int32_t which /*0 ops,1 bubbles,2 steps*/,
                         double* start_end, int64_t cap, int64_t* n);

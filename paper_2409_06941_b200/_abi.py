@@ -467,13 +467,14 @@ class SideTaskVTableC(Struct):
         ("run_gpu_workload", C.CFUNCTYPE(C.c_int, vp, vp, vp)),
         ("work_done", C.CFUNCTYPE(C.c_int, vp, vp, P(C.c_double))),
         ("cancel", C.CFUNCTYPE(C.c_int, vp)),
+        ("set_sm_budget", C.CFUNCTYPE(C.c_int, vp, i32)),
     ]
 
 
 class SyntheticTaskConfigC(Struct):
     _fields_ = [("step_ns", i64), ("profile_step_ns", i64), ("memory_demand_gib", C.c_double),
                 ("leak_gib_per_step", C.c_double), ("total_steps", i64), ("cooperative", i32),
-                ("reserved", i32)]
+                ("reserved", i32), ("init_ns", i64)]
 
 
 class PreemptC(Struct):
@@ -545,7 +546,7 @@ class HarnessConfigC(Struct):
         ("fp_ticks_override", i64), ("bp_ticks_override", i64),
         ("profile_epochs", i32), ("transport", i32),
         ("memory_headroom_gib", dbl), ("grace_ns", i64), ("step_group", i32),
-        ("harvest_fraction", dbl),
+        ("harvest_fraction", dbl), ("reclamation_delay_ns", i64), ("side_sms", i32),
     ]
 
 
@@ -557,6 +558,17 @@ class HarnessProfileC(Struct):
     ]
 
 
+class GateRecordC(Struct):
+    _fields_ = [("now", tick), ("bubble_end", tick), ("est_seconds", dbl), ("step_ticks", tick),
+                ("run", i32), ("signal", i32), ("step_end", tick), ("task", C.c_char * 64)]
+
+
+class SignalRecordC(Struct):
+    _fields_ = [("t", tick), ("kind", i32), ("epoch", i32), ("bubble", i32), ("looked_up", i32),
+                ("duration", tick), ("view_state", i32), ("view_initializing", i32), ("n_actions", i32),
+                ("actions", i32 * 4), ("deferred", i32), ("task", C.c_char * 64)]
+
+
 class RunReportC(Struct):
     _fields_ = [
         ("epochs", i32), ("with_tasks", i32),
@@ -564,7 +576,7 @@ class RunReportC(Struct):
         ("work_units", dbl), ("steps_launched", i64), ("steps_completed", i64),
         ("dispatch_host_us", dbl), ("max_step_overrun_s", dbl),
         ("breakdown", StageBreakdownC), ("pauses", i64), ("kills", i64),
-        ("kills_oom", i64), ("kills_pause_timeout", i64),
+        ("kills_oom", i64), ("kills_pause_timeout", i64), ("kills_init_timeout", i64),
     ]
 
 
@@ -578,6 +590,13 @@ GPU_PROTOTYPES.update({
     "fr_harness_task_status": (C.c_int, [vp, C.c_char_p, P(i32), P(i32), P(dbl)]),
     "fr_harness_destroy": (C.c_int, [vp]),
     "fr_harness_set_harvest_fraction": (C.c_int, [vp, dbl]),
+    "fr_harness_set_side_sms": (C.c_int, [vp, i32]),
+    "fr_harness_task_memory": (C.c_int, [vp, cp, P(dbl), P(dbl)]),
+    "fr_harness_run_trace": (C.c_int, [vp, P(vp)]),
+    "fr_harness_gate_log": (C.c_int, [vp, P(GateRecordC), i64, P(i64)]),
+    "fr_harness_signal_log": (C.c_int, [vp, P(SignalRecordC), i64, P(i64)]),
+    "fr_img_plan_set_max_sms": (C.c_int, [vp, i32]),
+    "fr_sgd_problem_set_max_sms": (C.c_int, [vp, i32]),
     "fr_harness_get_profile": (C.c_int, [vp, P(HarnessProfileC)]),
     "fr_harness_stage_bubbles": (C.c_int, [vp, P(BubbleC), i32, P(i32)]),
     "fr_harness_submit": (C.c_int, [vp, cp, P(SideTaskVTableC), vp, dbl, i32, P(TaskProfileC), P(i32)]),

@@ -472,6 +472,11 @@ class BubbleSim:
                                                            profile_steps, int(gate_max)))
         h = C.c_void_p()
         self._check(self.lib.fr_run_experiment(C.byref(ec), int(with_tasks), seed, C.byref(h)))
+        return self.trace_dict(h, check, trace_path)
+
+    def trace_dict(self, h, check: bool = False, trace_path: Optional[str] = None) -> dict:
+        """An fr_run_trace handle (simulated, or recorded on the GPU by
+        fr_harness_run_trace) as run_experiment's dict; destroys the handle."""
         try:
             n = A.RunTraceCountsC()
             self._check(self.lib.fr_run_trace_get_counts(h, C.byref(n)))

@@ -11,9 +11,7 @@
 
 using namespace freeride;
 
-struct fr_run_trace {
-  RunTrace t;
-};
+#include "run_trace.hpp"
 
 namespace {
 

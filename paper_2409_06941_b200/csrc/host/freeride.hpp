@@ -398,6 +398,12 @@ struct RunTrace {  // engine.hpp:75-92
   std::vector<DispositionRecord> dispositions;
   std::vector<TaskProfile> profiles;
   Tick makespan = 0;
+  // A trace recorded on the GPU (fr_harness_run_trace) rather than simulated:
+  // op durations are measured, only the stages in it ran, side-task kernels
+  // may co-run with an op (a step's tail past its bubble), and times from the
+  // host / device-clock domains agree to within `tolerance` ticks.
+  bool measured = false;
+  Tick tolerance = 0;
 };
 
 // engine.hpp:97-98 -- the reference declares it and never implements it; the

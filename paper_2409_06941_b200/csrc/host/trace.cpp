@@ -88,6 +88,10 @@ void write_trace_jsonl(const RunTrace& tr, std::ostream& out) {
   meta.set("with_tasks", Value::boolean(tr.with_tasks));
   Value& pf = meta.set("profiles", Value::array());
   for (const TaskProfile& p : tr.profiles) pf.push(profile_json(p));
+  if (tr.measured) {  // only in GPU traces: simulated traces stay byte-identical
+    meta.set("measured", Value::boolean(true));
+    meta.set("tolerance", Value::integer(tr.tolerance));
+  }
   out << json::dump(meta) << '\n';
 
   std::vector<Rec> recs;
@@ -200,6 +204,8 @@ RunTrace read_trace_jsonl(std::istream& in) {
         tp.profiled_steps = static_cast<int>(json::get_int(json::need(p, "profiled_steps", path), path));
         tr.profiles.push_back(tp);
       }
+      if (const Value* m = v.find("measured")) tr.measured = json::get_bool(*m, path + ".measured");
+      if (const Value* t = v.find("tolerance")) tr.tolerance = json::get_int(*t, path + ".tolerance");
       meta = true;
       continue;
     }

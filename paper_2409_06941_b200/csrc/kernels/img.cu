@@ -360,6 +360,8 @@ struct fr_img_plan {
   mutable cudaStream_t chain_stream = nullptr;
   int smem = 0;
   int sms = 0;
+  int max_sms = 0;  // fr_img_plan_set_max_sms: grid sized for this many SMs (0 = all)
+  int64_t grid_sms() const { return max_sms > 0 ? std::min(max_sms, sms) : sms; }
   size_t prepared_bytes() const {
     return path == FR_IMG_PATH_TMA_2X ? static_cast<size_t>(dw) * dh * 8 : static_cast<size_t>(dw) * dh * 4;
   }
@@ -439,6 +441,13 @@ int fr_img_plan_set_overlap(fr_img_plan* plan, int32_t overlap) {
   return FR_OK;
 }
 
+int fr_img_plan_set_max_sms(fr_img_plan* plan, int32_t sms) {
+  if (!plan) return frcapi::fail(FR_ERR_ARGUMENT, "null plan");
+  if (sms < 0) return frcapi::fail(FR_ERR_VALIDATION, "sms must be >= 0", "sms");
+  plan->max_sms = sms;
+  return FR_OK;
+}
+
 int fr_img_plan_destroy(fr_img_plan* plan) {
   if (!plan) return FR_OK;
   if (plan->d_tab) cudaFree(plan->d_tab);
@@ -488,12 +497,7 @@ int fr_img_resize_watermark_prepared(const fr_img_plan* plan, const uint8_t* src
       return frcapi::fail(FR_ERR_UNSUPPORTED, "TMA path needs 16-byte aligned buffers");
     const int64_t rows = static_cast<int64_t>(n) * plan->dh;
     if (rows >= (int64_t{1} << 31)) return frcapi::fail(FR_ERR_UNSUPPORTED, "too many rows in one step");
-    static const int grid_sms = [] {
-      const char* e = std::getenv("FR_IMG_GRID_SMS");  // experiment: CTAs for this many SMs only
-      return e ? std::max(1, std::atoi(e)) : 0;
-    }();
-    const int64_t sms = grid_sms > 0 ? std::min(grid_sms, plan->sms) : plan->sms;
-    const int grid = static_cast<int>(std::min<int64_t>(rows, sms * plan->ctas_per_sm));
+    const int grid = static_cast<int>(std::min<int64_t>(rows, plan->grid_sms() * plan->ctas_per_sm));
     auto k = plan->stages == 2 ? img_resize2x_wm_tma<2, false, 3> : img_resize2x_wm_tma<3, false, 2>;
     // Consecutive steps overlap their tail and head (programmatic dependent
     // launch: a launch's CTAs start once every CTA of the previous one took
@@ -546,7 +550,7 @@ int fr_img_resize_watermark_preemptible(const fr_img_plan* plan, const uint8_t* 
   if (max_rows < 0 || max_rows >= (int64_t{1} << 31))
     return frcapi::fail(FR_ERR_VALIDATION, "max_rows in [0, 2^31)", "max_rows");
   if (max_rows == 0) return FR_OK;
-  const int grid = static_cast<int>(std::min<int64_t>(max_rows, int64_t(plan->sms) * plan->ctas_per_sm));
+  const int grid = static_cast<int>(std::min<int64_t>(max_rows, plan->grid_sms() * plan->ctas_per_sm));
   // no preempt: a stop word that never fires (counters[5] stays 0 < token)
   const uint32_t* word = preempt && preempt->stop_word ? preempt->stop_word : counters + 5;
   const uint32_t token = preempt && preempt->stop_word ? preempt->token : 0xFFFFFFFFu;

@@ -423,6 +423,8 @@ struct fr_sgd_problem {
   float* L = nullptr;
   double* acc = nullptr;
   int sms = 148;
+  int max_sms = 0;  // fr_sgd_problem_set_max_sms (0 = all)
+  int64_t grid_sms() const { return max_sms > 0 ? std::min(max_sms, sms) : sms; }
   bool grouped = false;  // edges stable-sorted by u (fr_sgd_group_by_user)
   bool overlap = false;  // fr_sgd_problem_set_overlap: consecutive steps may overlap (Hogwild)
   // Programmatic dependent launch is only safe behind another user step of
@@ -499,7 +501,7 @@ void launch_step(fr_sgd_problem* p, int64_t a, int64_t b, float eta, float lam, 
   const int64_t groups = (b - a + kSgdEpi - 1) / kSgdEpi;
   const int64_t cap_groups = std::max<int64_t>(1, std::min(int64_t(p->V) / div, hub_cap(p)) / kSgdEpi);
   const int64_t want = (std::min(groups, cap_groups) * Row<K>::kLanes + kSgdThreads - 1) / kSgdThreads;
-  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(p->sms) * per_sm)));
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, p->grid_sms() * per_sm)));
   sgd_step_kernel<K><<<grid, kSgdThreads, 0, s>>>(p->u, p->v, p->r, p->L, a, b, eta, lam);
 }
 
@@ -520,7 +522,7 @@ void launch_user_step(fr_sgd_problem* p, int64_t a, int64_t b, float eta, float 
   }();
   const int64_t n = b - a;
   const int64_t cap_groups = std::max<int64_t>(1, std::min(int64_t(p->V) / div, hub_cap(p)) / D);
-  const int64_t max_groups = int64_t(p->sms) * per_sm * kSgdThreads / LN;
+  const int64_t max_groups = p->grid_sms() * per_sm * kSgdThreads / LN;
   const int64_t groups = std::min({(n + D - 1) / D, cap_groups, max_groups});
   const int64_t seg = ((n + groups - 1) / groups + D - 1) / D * D;
   const int64_t used = (n + seg - 1) / seg;
@@ -795,6 +797,13 @@ int fr_sgd_problem_set_overlap(fr_sgd_problem* p, int32_t overlap) {
   return FR_OK;
 }
 
+int fr_sgd_problem_set_max_sms(fr_sgd_problem* p, int32_t sms) {
+  if (!p) return frcapi::fail(FR_ERR_ARGUMENT, "null problem");
+  if (sms < 0) return frcapi::fail(FR_ERR_VALIDATION, "sms must be >= 0", "sms");
+  p->max_sms = sms;
+  return FR_OK;
+}
+
 int fr_sgd_problem_set_kernel(fr_sgd_problem* p, int32_t by_user) {
   if (!p) return frcapi::fail(FR_ERR_ARGUMENT, "null problem");
   p->grouped = by_user != 0;
@@ -910,6 +919,10 @@ int sgd_task_finished(void* u, int64_t done, int32_t* out) {
   return FR_OK;
 }
 
+int sgd_task_sm_budget(void* u, int32_t sms) {
+  return fr_sgd_problem_set_max_sms(static_cast<SgdTask*>(u)->p, sms);
+}
+
 void sgd_task_destroy(void* u) {
   auto* t = static_cast<SgdTask*>(u);
   cudaDeviceSynchronize();
@@ -958,6 +971,7 @@ int fr_sgd_task_create_from_problem(const fr_sgd_task_config* c, fr_sgd_problem*
   vt->run_next_step = sgd_task_step;
   vt->finished = sgd_task_finished;
   vt->destroy = sgd_task_destroy;
+  vt->set_sm_budget = sgd_task_sm_budget;
   vt->work_units_per_step = static_cast<double>(c->edges_per_step);  // edges
   *user = t;
   return FR_OK;

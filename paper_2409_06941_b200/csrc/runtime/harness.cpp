@@ -44,6 +44,7 @@
 #include "capi_util.hpp"
 #include "freeride_gpu.h"
 #include "host/freeride.hpp"
+#include "run_trace.hpp"
 #include "runtime/standin.hpp"
 #include "runtime/timeline.cuh"
 
@@ -200,6 +201,48 @@ struct fr_harness {
 
   std::vector<WorkerState> workers;      // this process serves one worker
   std::map<std::string, std::unique_ptr<Task>> tasks;
+
+  // The last run's decision records (device ns, absolute; converted to ns
+  // from the run start -- ctl->run0_ns -- on export).
+  struct SignalRec {
+    std::int64_t t = 0;
+    int kind = 0;  // 0 started, 1 ended
+    std::uint32_t id = 0;
+    std::int64_t duration = 0;
+    bool looked_up = false, deferred = false;
+    std::string task;
+    TaskView view;
+    std::vector<ManagerAction> acts;
+  };
+  struct GateRec {
+    std::int64_t now = 0, bubble_end = 0, step_end = 0;
+    double est = 0;
+    std::int64_t est_ticks = 0;
+    bool run = false;
+    int signal = -1;
+    std::string task;
+  };
+  std::vector<SignalRec> sig_log;
+  std::vector<GateRec> gate_log;
+  std::vector<TransitionRecord> tr_log;
+  std::vector<KillRecord> kill_log;
+  std::map<std::string, SideTaskState> run_start_state;
+  std::vector<std::pair<std::string, std::pair<double, double>>> init_log;  // event seconds
+  std::int64_t run0_dev = 0;
+  bool last_with_tasks = false;
+  int last_epochs = 0;
+  // reclamation_delay: killed tasks whose pool pages are still held, and when they go
+  std::vector<std::pair<Task*, std::int64_t>> reclaim;
+  void reclaim_due(std::int64_t now) {
+    for (auto it = reclaim.begin(); it != reclaim.end();) {
+      if (now >= it->second) {
+        if (it->first->pool) cudaMemPoolTrimTo(it->first->pool, 0);
+        it = reclaim.erase(it);
+      } else {
+        ++it;
+      }
+    }
+  }
 
   // last run
   std::vector<double> op_se, bubble_se, step_se;
@@ -406,6 +449,15 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
   if (cfg.transport == 1 && !linked)
     throw std::runtime_error("peer-linked harness: call fr_harness_link before running");
   pool_used = 0;
+  sig_log.clear();
+  gate_log.clear();
+  tr_log.clear();
+  kill_log.clear();
+  init_log.clear();
+  run_start_state.clear();
+  for (const auto& kv : tasks) run_start_state[kv.first] = kv.second->rt.state;
+  last_with_tasks = with_tasks;
+  last_epochs = epochs;
   std::memset(ring, 0, sizeof(RingSlot) * kRingSlots);
   ck(cudaMemset(&ctl->end_seq, 0, 2 * sizeof(std::uint32_t)), "end_seq / link_timeouts reset");
   // the wait kernels' L1/shared split: max-L1 only if every task wants it
@@ -420,6 +472,7 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
   }
   set_wait_kernel_carveout(all_l1 ? cudaSharedmemCarveoutMaxL1 : cudaSharedmemCarveoutMaxShared);
   calibrate();
+  reclaim_due(dev_now());
   // this harness's streams only: a device-wide sync would wait on a linked
   // neighbour's dependency spin in the same process (deadlock)
   ck(cudaStreamSynchronize(train), "pre-run sync");
@@ -556,7 +609,51 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
 
   // ---- the worker: Alg. 2 + iterative interface, in real time
   WorkerState& ws = workers[0];
-  const auto view = [this](const std::string& id) { return lookup(id); };
+  // Alg. 2's task lookup, remembering what it showed the manager (signal log)
+  std::string seen_id;
+  TaskView seen_view;
+  bool looked = false;
+  const auto view = [&](const std::string& id) {
+    TaskView v = lookup(id);
+    if (!looked) {
+      looked = true;
+      seen_id = id;
+      seen_view = v;
+    }
+    return v;
+  };
+  // every transition the worker applies, stamped (device ns) for the run
+  // trace.  Stamps are the decision's device time (a BubbleStarted's signal
+  // time, a step's projected start, a pause's drain) made non-decreasing per
+  // task, so the trace's time order is the order they were applied in (a
+  // BubbleStarted held while a pause drained is applied after that pause).
+  std::map<std::string, std::int64_t> last_stamp;
+  const auto trans = [&](Task& t, TransitionKind k, std::int64_t now) {
+    auto it = last_stamp.find(t.id);
+    if (it != last_stamp.end()) now = std::max(now, it->second);
+    last_stamp[t.id] = now;
+    apply_transition(t.rt, k, now);
+    tr_log.push_back(TransitionRecord{now, t.id, k, cfg.stage});
+  };
+  const auto log_signal = [&](std::int64_t t, int kind, std::uint32_t id, std::int64_t dur, bool deferred,
+                              const std::vector<ManagerAction>& acts) {
+    SignalRec r;
+    r.t = t;
+    r.kind = kind;
+    r.id = id;
+    r.duration = dur;
+    r.deferred = deferred;
+    r.looked_up = looked;
+    r.task = looked ? seen_id : std::string();
+    r.view = seen_view;
+    r.acts = acts;
+    sig_log.push_back(std::move(r));
+    looked = false;
+  };
+  int cur_signal = -1;                 // the BubbleStarted that started the running task
+  Task* guard_task = nullptr;          // ArmInitGuard (manager.hpp:58): init in flight at a bubble end
+  std::int64_t guard_due = 0;
+  const Tick grace = cfg.grace_ns > 0 ? cfg.grace_ns : kGraceTicks;
   std::vector<StepRec> steps;
   std::deque<std::size_t> inflight;  // indices into steps
   std::vector<std::pair<std::int64_t, std::int64_t>> init_spans;
@@ -595,7 +692,7 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
     }
   std::uint32_t cur_token = 0;  // bubble-end token the running imperative workload stops at
   auto stop_task = [&](Task& t, Tick now) {
-    apply_transition(t.rt, TransitionKind::StopSideTask, now);
+    trans(t, TransitionKind::StopSideTask, now);
     {
       PoolScope ps(device, t.pool);
       hook(t.vt.stop ? t.vt.stop(t.user) : FR_OK, "stop");
@@ -604,7 +701,7 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
     if (ws.current_task && *ws.current_task == t.id) ws.current_task.reset();  // Appendix B rule 8
     if (running == &t) running = nullptr;
   };
-  std::int64_t kills_oom = 0, kills_timeout = 0;
+  std::int64_t kills_oom = 0, kills_timeout = 0, kills_init = 0;
   std::function<void(Task&, Disposition)> kill;  // defined below (needs drain_completions)
   auto drain_completions = [&] {
     while (!inflight.empty()) {
@@ -636,16 +733,26 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
   // Framework-enforced kill (limits.cpp:13-26): cancel the task's in-flight
   // work (its cancel hook), drain its stream, StopSideTask, release its pool.
   kill = [&](Task& t, Disposition d) {
+    const std::int64_t t_kill = dev_now();
+    kill_log.push_back(KillRecord{t_kill, t.id, cfg.stage,
+                                  d == Disposition::KilledOom ? KillReason::Oom
+                                  : d == Disposition::KilledPauseTimeout ? KillReason::PauseTimeout
+                                                                         : KillReason::InitTimeout});
     if (t.vt.cancel) hook(t.vt.cancel(t.user), "cancel");
     ck(cudaStreamSynchronize(side), "kill drain");
     drain_completions();
     if (t.rt.state != SideTaskState::Stopped) {
-      apply_transition(t.rt, TransitionKind::StopSideTask, dev_now());
+      trans(t, TransitionKind::StopSideTask, t_kill);
       PoolScope ps(device, t.pool);
       hook(t.vt.stop ? t.vt.stop(t.user) : FR_OK, "stop");
     }
     ck(cudaStreamSynchronize(side), "kill release");
-    if (t.pool) cudaMemPoolTrimTo(t.pool, 0);
+    // memory goes back after LimitConfig::reclamation_delay (limits.hpp:12)
+    if (cfg.reclamation_delay_ns > 0)
+      reclaim.emplace_back(&t, t_kill + cfg.reclamation_delay_ns);
+    else if (t.pool)
+      cudaMemPoolTrimTo(t.pool, 0);
+    if (guard_task == &t) guard_task = nullptr;
     t.disp = d;
     t.initializing = false;
     if (ws.current_task && *ws.current_task == t.id) ws.current_task.reset();  // Appendix B rule 8
@@ -654,7 +761,7 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
     pause_pending = false;
     gate_closed = false;
     ++kills;
-    ++(d == Disposition::KilledOom ? kills_oom : kills_timeout);
+    ++(d == Disposition::KilledOom ? kills_oom : d == Disposition::KilledPauseTimeout ? kills_timeout : kills_init);
   };
   auto oom = [&](Task& t) {  // check_memory (limits.cpp:13-15), strict exceedance
     if (check_memory(t.used_gib(), t.mem_limit) == MemCheck::OomKill) {
@@ -668,7 +775,7 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
     pause_pending = false;
     if (running && running->rt.state == SideTaskState::Running) {
       const Tick now = dev_now();
-      apply_transition(running->rt, TransitionKind::PauseSideTask, now);
+      trans(*running, TransitionKind::PauseSideTask, now);
       hook(running->vt.pause ? running->vt.pause(running->user) : FR_OK, "pause");
       ++pauses;
     }
@@ -682,8 +789,9 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
       if (q == cudaErrorNotReady) continue;
       ck(q, "init event");
       t.initializing = false;
-      apply_transition(t.rt, TransitionKind::InitSideTask, dev_now());
+      trans(t, TransitionKind::InitSideTask, dev_now());
       t.rt.assigned_worker = 0;
+      if (guard_task == &t) guard_task = nullptr;  // the init landed before the guard fired
     }
   };
 
@@ -691,12 +799,15 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
   bool deferred_start = false;
   std::int64_t deferred_t = 0;
   std::uint32_t deferred_id = 0;
-  auto start_bubble = [&](std::int64_t t_dev, std::uint32_t id) {
+  auto start_bubble = [&](std::int64_t t_dev, std::uint32_t id, bool deferred) {
     const Bubble& pb = bubbles[id % kBubbleIds];
     Bubble b = pb;
     b.epoch = static_cast<int>(id / kBubbleIds);
     b.start = t_dev;
-    for (const ManagerAction& act : on_bubble_started(ws, b, view)) {
+    looked = false;
+    const std::vector<ManagerAction> acts = on_bubble_started(ws, b, view);
+    log_signal(t_dev, 0, id, pb.duration, deferred, acts);
+    for (const ManagerAction& act : acts) {
       Task& t = task_of(act.task_id);
       if (act.kind == ManagerActionKind::IssueInit) {
         if (!t.init_a) {
@@ -715,7 +826,8 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
         t.init_recorded = true;
         oom(t);
       } else if (act.kind == ManagerActionKind::IssueStart) {
-        apply_transition(t.rt, TransitionKind::StartSideTask, t_dev);
+        trans(t, TransitionKind::StartSideTask, t_dev);
+        cur_signal = static_cast<int>(sig_log.size()) - 1;
         hook(t.vt.start ? t.vt.start(t.user) : FR_OK, "start");
         running = &t;
         // StartSideTask carries the bubble end (§4.5); a harvest
@@ -756,23 +868,32 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
         deferred_t = t_dev;
         deferred_id = id;
       } else if (with_tasks && kind == kEvBubbleStart) {
-        start_bubble(t_dev, id);
+        start_bubble(t_dev, id, false);
       } else if (with_tasks && kind == kEvBubbleEnd && deferred_start) {
         deferred_start = false;  // the held bubble ended before the pause landed
-        on_bubble_ended(ws, t_dev, view);
+        looked = false;
+        log_signal(t_dev, 1, id, 0, true, on_bubble_ended(ws, t_dev, view));
       } else if (with_tasks && kind == kEvBubbleEnd) {
-        for (const ManagerAction& act : on_bubble_ended(ws, t_dev, view)) {
+        looked = false;
+        const std::vector<ManagerAction> acts = on_bubble_ended(ws, t_dev, view);
+        log_signal(t_dev, 1, id, 0, false, acts);
+        for (const ManagerAction& act : acts) {
           if (act.kind == ManagerActionKind::IssuePause) {
             pause_pending = true;
             kill_judged = false;
             pause_issued_dev = t_dev;
+          } else if (act.kind == ManagerActionKind::ArmInitGuard) {
+            // engine rule: at issue + grace the init
+            // must have landed, else KilledInitTimeout
+            guard_task = &task_of(act.task_id);
+            guard_due = t_dev + grace;
           }
         }
       }
     }
     if (with_tasks && deferred_start && !pause_pending) {
       deferred_start = false;
-      start_bubble(deferred_t, deferred_id);
+      start_bubble(deferred_t, deferred_id, true);
     }
     if (!with_tasks && next_slot >= n_events) break;
     // 2. step completions, init completion, pause drains
@@ -812,6 +933,18 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
         const double est = gate_est(*running);
         const Tick est_ticks = static_cast<Tick>(std::llround(est / kTick));
         const IterativeDecision d = iterative_run(running->rt, bubble_end_dev, start, est, kTick, est_ticks);
+        {
+          GateRec g;
+          g.now = start;
+          g.bubble_end = bubble_end_dev;
+          g.est = est;
+          g.est_ticks = est_ticks;
+          g.run = d.run;
+          g.step_end = d.step_end;
+          g.signal = cur_signal;
+          g.task = running->id;
+          gate_log.push_back(std::move(g));
+        }
         if (!d.run) {
           gate_closed = true;  // yield until the next transition
           break;
@@ -832,7 +965,7 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
         ++r.n;
         Task* rt = r.task;
         if (r.n >= group) close_group();
-        apply_transition(running->rt, TransitionKind::RunNextStep, start);
+        trans(*running, TransitionKind::RunNextStep, start);
         ++inflight_steps;
         proj_end_dev = d.step_end;
         ++launched;
@@ -844,13 +977,23 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
       // period is a Kill (limits.cpp:21-26): the task's cancel hook stops its
       // in-flight kernels (cooperative ones exit at once), then it is stopped
       // and its memory pool released.
+      // the init guard: InitSideTask still running one grace period after the
+      // bubble it was issued in ended -> KilledInitTimeout (engine.hpp:16)
+      if (guard_task) {
+        finish_init();
+        if (guard_task && guard_task->initializing && dev_now() >= guard_due) {
+          Task* g = guard_task;
+          guard_task = nullptr;
+          kill(*g, Disposition::KilledInitTimeout);
+        }
+      }
+      if (!reclaim.empty()) reclaim_due(dev_now());
       if (pause_pending && !kill_judged && running &&
-          framework_enforce(running->rt.last_paused, pause_issued_dev, dev_now(),
-                            cfg.grace_ns > 0 ? cfg.grace_ns : kGraceTicks) == Enforce::Kill) {
+          framework_enforce(running->rt.last_paused, pause_issued_dev, dev_now(), grace) == Enforce::Kill) {
         kill_judged = true;
         kill(*running, Disposition::KilledPauseTimeout);
       }
-      if (next_slot >= n_events && inflight.empty() && !pause_pending) break;
+      if (next_slot >= n_events && inflight.empty() && !pause_pending && !guard_task) break;
     }
   }
   trainer.join();
@@ -867,6 +1010,11 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
     if (timeouts)
       throw std::runtime_error("peer-linked pipeline: " + std::to_string(timeouts) +
                                " dependency waits timed out (a neighbour stage never signalled)");
+  }
+  {
+    std::uint64_t r0 = 0;
+    ck(cudaMemcpy(&r0, &ctl->run0_ns, sizeof(r0), cudaMemcpyDeviceToHost), "run0");
+    run0_dev = static_cast<std::int64_t>(r0);
   }
   for (auto& [t, before] : work_before) {
     double u = before;
@@ -936,6 +1084,7 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
       const double a = elapsed_s(run_start, kv.second->init_a);
       const double b = elapsed_s(run_start, kv.second->init_b);
       if (b > 0) bi.activities.push_back(ActivityRecord{tick_of(std::max(0.0, a)), tick_of(b), kv.first, 0, ActivityKind::Init, false});
+      if (b > 0) init_log.push_back({kv.first, {std::max(0.0, a), b}});
       if (std::getenv("FR_HARNESS_TRACE"))
         std::fprintf(stderr, "[harness] %s InitSideTask on device %.3f..%.3f ms after run start (hook %.0f us on host)\n",
                      kv.first.c_str(), a * 1e3, b * 1e3, kv.second->init_host_us);
@@ -963,6 +1112,7 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
   rep->kills = kills;
   rep->kills_oom = kills_oom;
   rep->kills_pause_timeout = kills_timeout;
+  rep->kills_init_timeout = kills_init;
   last_side_steps = launched;
   last_train_ops = static_cast<std::int64_t>(epochs) * nops;
   epoch_base += static_cast<std::uint32_t>(epochs);
@@ -1135,6 +1285,7 @@ int fr_harness_submit(fr_harness* h, const char* task_id, const fr_side_task_vta
     std::uint64_t keep = UINT64_MAX;  // cache freed memory inside the pool (no device sync on reuse)
     cudaMemPoolSetAttribute(t->pool, cudaMemPoolAttrReleaseThreshold, &keep);
     PoolScope ps(h->device, t->pool);
+    if (vt->set_sm_budget) hook(vt->set_sm_budget(user, std::max(0, h->cfg.side_sms)), "set_sm_budget");
     hook(vt->create ? vt->create(user) : FR_OK, "create");
     hook(vt->init(user, h->side), "init");
     const int n = imperative ? 0 : std::max(1, profile_steps);
@@ -1228,6 +1379,33 @@ int fr_harness_set_harvest_fraction(fr_harness* h, double fraction) {
   return FR_OK;
 }
 
+int fr_harness_set_side_sms(fr_harness* h, int32_t sms) {
+  if (!h) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  if (sms < 0) return frcapi::fail(FR_ERR_VALIDATION, "side_sms must be >= 0", "side_sms");
+  h->cfg.side_sms = sms;
+  for (auto& kv : h->tasks)
+    if (kv.second->vt.set_sm_budget) {
+      const int rc = kv.second->vt.set_sm_budget(kv.second->user, sms);
+      if (rc != FR_OK) return rc;
+    }
+  return FR_OK;
+}
+
+int fr_harness_task_memory(const fr_harness* h, const char* task_id, double* used_gib, double* reserved_gib) {
+  if (!h || !task_id) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  auto it = h->tasks.find(task_id);
+  if (it == h->tasks.end()) return frcapi::fail(FR_ERR_NOT_FOUND, "unknown task");
+  const Task& t = *it->second;
+  std::size_t used = 0, reserved = 0;
+  if (t.pool) {
+    cudaMemPoolGetAttribute(t.pool, cudaMemPoolAttrUsedMemCurrent, &used);
+    cudaMemPoolGetAttribute(t.pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+  }
+  if (used_gib) *used_gib = static_cast<double>(used) / kGiB;
+  if (reserved_gib) *reserved_gib = static_cast<double>(reserved) / kGiB;
+  return FR_OK;
+}
+
 int fr_harness_reprofile_bubbles(fr_harness* h) {
   if (!h) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
   if (h->bubbles_from_last_run() == 0)
@@ -1285,6 +1463,122 @@ int fr_harness_task_status(const fr_harness* h, const char* task_id, int32_t* st
   if (state) *state = static_cast<int32_t>(t.rt.state);
   if (disposition) *disposition = static_cast<int32_t>(t.disp);
   if (memory_used_gib) *memory_used_gib = t.used_gib();
+  return FR_OK;
+}
+
+int fr_harness_run_trace(const fr_harness* h, fr_run_trace** out) {
+  if (!h || !out) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  if (!h->last_with_tasks || h->last_epochs < 1)
+    return frcapi::fail(FR_ERR_VALIDATION, "the last run had no side tasks", "run");
+  return frcapi::guard([&]() -> int {
+    auto tr = std::make_unique<fr_run_trace>();
+    RunTrace& r = tr->t;
+    const int s = h->cfg.stage;
+    const auto tick_of = [](double sec) { return static_cast<Tick>(std::llround(sec / kTick)); };
+    const auto rel = [h](std::int64_t t_dev) { return static_cast<Tick>(t_dev - h->run0_dev); };
+    r.measured = true;
+    r.tolerance = 20'000;  // host-clock stamps vs device events (calibrated offset + polling)
+    r.with_tasks = true;
+    ExperimentConfig& ec = r.config;
+    ec.pipeline = h->pcfg;
+    ec.pipeline.num_epochs = h->last_epochs;
+    ec.limits.grace_period = h->cfg.grace_ns > 0 ? h->cfg.grace_ns : kGraceTicks;
+    ec.limits.memory_headroom = std::max(0.0, h->cfg.memory_headroom_gib);
+    ec.limits.reclamation_delay = std::max<std::int64_t>(0, h->cfg.reclamation_delay_ns);
+    ec.runtime.check_overhead = 0;
+    ec.runtime.gate_estimate = h->cfg.gate_estimate == 1 ? GateEstimate::Max : GateEstimate::Mean;
+    std::map<std::string, std::int64_t> steps;
+    for (const auto& kv : h->tasks) {
+      const Task& t = *kv.second;
+      SideTaskSpec spec = t.rt.spec;
+      spec.per_step_duration = static_cast<Tick>(std::llround(t.prof.est_per_step_duration.value_or(0.0) / kTick));
+      ec.tasks.push_back(spec);
+      r.profiles.push_back(t.prof);
+      r.submits.push_back(AssignRecord{0, t.id, -1});
+      r.assigns.push_back(AssignRecord{0, t.id, s});
+      // the transitions that brought the task to its state at the run start
+      auto it = h->run_start_state.find(t.id);
+      const SideTaskState st0 = it == h->run_start_state.end() ? SideTaskState::Created : it->second;
+      std::vector<TransitionKind> pre;
+      if (st0 != SideTaskState::Submitted) pre.push_back(TransitionKind::CreateSideTask);
+      if (st0 == SideTaskState::Paused || st0 == SideTaskState::Running) pre.push_back(TransitionKind::InitSideTask);
+      if (st0 == SideTaskState::Running) pre.push_back(TransitionKind::StartSideTask);
+      if (st0 == SideTaskState::Stopped) pre.push_back(TransitionKind::StopSideTask);
+      for (TransitionKind k : pre) r.transitions.push_back(TransitionRecord{0, t.id, k, s});
+    }
+    for (const TransitionRecord& x : h->tr_log)
+      r.transitions.push_back(TransitionRecord{rel(x.t), x.task, x.kind, x.worker});
+    std::stable_sort(r.transitions.begin(), r.transitions.end(),
+                     [](const TransitionRecord& a, const TransitionRecord& b) { return a.t < b.t; });
+    const std::size_t nops = h->ops.size();
+    for (std::size_t i = 0; i < h->op_se.size() / 2; ++i) {
+      const OpEvent& o = h->ops[i % nops];
+      r.ops.push_back(OpEvent{s, o.kind, o.micro_batch, static_cast<int>(i / nops), tick_of(h->op_se[2 * i]),
+                              tick_of(h->op_se[2 * i + 1])});
+    }
+    const std::size_t nb = h->bubbles.size();
+    for (std::size_t k = 0; nb && k < h->bubble_se.size() / 2; ++k) {
+      const Tick a = tick_of(h->bubble_se[2 * k]), b = tick_of(h->bubble_se[2 * k + 1]);
+      r.bubbles.push_back(Bubble{s, static_cast<int>(k / nb), a, b - a, h->avail, h->bubbles[k % nb].btype});
+    }
+    for (const auto& [id, se] : h->init_log)
+      r.activities.push_back(ActivityRecord{tick_of(se.first), tick_of(se.second), id, s, ActivityKind::Init, false});
+    for (std::size_t i = 0; i < h->step_task.size(); ++i) {
+      const Task* t = h->step_task[i];
+      r.activities.push_back(ActivityRecord{tick_of(h->step_se[2 * i]), tick_of(h->step_se[2 * i + 1]), t->id, s,
+                                            t->imperative() ? ActivityKind::Kernel : ActivityKind::Step, false});
+      ++steps[t->id];
+    }
+    for (const KillRecord& k : h->kill_log) r.kills.push_back(KillRecord{rel(k.t), k.task, k.worker, k.reason});
+    for (const auto& kv : h->tasks)
+      r.dispositions.push_back(DispositionRecord{kv.first, kv.second->disp, steps[kv.first], s});
+    for (const OpEvent& o : r.ops) r.makespan = std::max(r.makespan, o.end);
+    *out = tr.release();
+    return FR_OK;
+  });
+}
+
+int fr_harness_gate_log(const fr_harness* h, fr_gate_record* out, int64_t cap, int64_t* n) {
+  if (!h || !n) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  *n = static_cast<int64_t>(h->gate_log.size());
+  if (*n > cap) return frcapi::fail(FR_ERR_CAPACITY, "gate record buffer too small");
+  for (std::size_t i = 0; i < h->gate_log.size(); ++i) {
+    const auto& g = h->gate_log[i];
+    fr_gate_record& o = out[i];
+    std::memset(&o, 0, sizeof(o));
+    o.now = g.now - h->run0_dev;
+    o.bubble_end = g.bubble_end - h->run0_dev;
+    o.est_seconds = g.est;
+    o.step_ticks = g.est_ticks;
+    o.run = g.run;
+    o.signal = g.signal;
+    o.step_end = g.run ? g.step_end - h->run0_dev : 0;
+    frcapi::copy_id(o.task, g.task);
+  }
+  return FR_OK;
+}
+
+int fr_harness_signal_log(const fr_harness* h, fr_signal_record* out, int64_t cap, int64_t* n) {
+  if (!h || !n) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  *n = static_cast<int64_t>(h->sig_log.size());
+  if (*n > cap) return frcapi::fail(FR_ERR_CAPACITY, "signal record buffer too small");
+  for (std::size_t i = 0; i < h->sig_log.size(); ++i) {
+    const auto& g = h->sig_log[i];
+    fr_signal_record& o = out[i];
+    std::memset(&o, 0, sizeof(o));
+    o.t = g.t - h->run0_dev;
+    o.kind = g.kind;
+    o.epoch = static_cast<int32_t>(g.id / kBubbleIds);
+    o.bubble = static_cast<int32_t>(g.id % kBubbleIds);
+    o.looked_up = g.looked_up;
+    o.duration = g.duration;
+    o.view_state = static_cast<int32_t>(g.view.state);
+    o.view_initializing = g.view.initializing;
+    o.n_actions = static_cast<int32_t>(std::min<std::size_t>(4, g.acts.size()));
+    for (int k = 0; k < o.n_actions; ++k) o.actions[k] = static_cast<int32_t>(g.acts[static_cast<std::size_t>(k)].kind);
+    o.deferred = g.deferred;
+    frcapi::copy_id(o.task, g.task);
+  }
   return FR_OK;
 }
 

@@ -42,6 +42,7 @@ struct ImageTask {
   int64_t cursor = 0;
   int64_t steps = 0;
   cudaStream_t last = nullptr;
+  int32_t max_sms = 0;  // set_sm_budget
 
   std::size_t src_img() const { return static_cast<std::size_t>(cfg.sw) * cfg.sh * 3; }
   std::size_t dst_img() const { return static_cast<std::size_t>(cfg.dw) * cfg.dh * 3; }
@@ -79,6 +80,7 @@ int img_create(void* u) {
   auto* t = static_cast<ImageTask*>(u);
   if (t->plan) return FR_OK;
   int rc = fr_img_plan_create(t->cfg.sw, t->cfg.sh, t->cfg.dw, t->cfg.dh, &t->plan);
+  if (rc == FR_OK) rc = fr_img_plan_set_max_sms(t->plan, t->max_sms);
   // resident frames are produced at Init, never by the kernel before a step
   if (rc == FR_OK && !t->cfg.host_io) rc = fr_img_plan_set_overlap(t->plan, 1);
   return rc;
@@ -216,6 +218,12 @@ int img_stop(void* u) {
   return release(t, t->last);
 }
 
+int img_sm_budget(void* u, int32_t sms) {
+  auto* t = static_cast<ImageTask*>(u);
+  t->max_sms = sms;
+  return t->plan ? fr_img_plan_set_max_sms(t->plan, sms) : FR_OK;
+}
+
 int img_finished(void* u, int64_t done, int32_t* out) {
   auto* t = static_cast<ImageTask*>(u);
   *out = t->cfg.total_steps > 0 && done >= t->cfg.total_steps;
@@ -272,6 +280,7 @@ int fr_image_task_create(const fr_image_task_config* c, fr_side_task_vtable* vt,
   vt->stop = img_stop;
   vt->finished = img_finished;
   vt->destroy = img_destroy;
+  vt->set_sm_budget = img_sm_budget;
   vt->work_units_per_step = double(c->images_per_step) * c->dw * c->dh;  // output pixels
   if (c->interface_kind == FR_IMPERATIVE) {
     vt->interface_kind = FR_IMPERATIVE;

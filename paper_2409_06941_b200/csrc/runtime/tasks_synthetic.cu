@@ -56,8 +56,14 @@ int syn_init(void* u, void* stream) {
   auto s = static_cast<cudaStream_t>(stream);
   t->last = s;
   *t->cancel = 0;
-  if (t->cfg.memory_demand_gib > 0)
-    return cu(cudaMallocAsync(&t->demand, gib_bytes(t->cfg.memory_demand_gib), s), "demand");
+  if (t->cfg.memory_demand_gib > 0) {
+    const int rc = cu(cudaMallocAsync(&t->demand, gib_bytes(t->cfg.memory_demand_gib), s), "demand");
+    if (rc != FR_OK) return rc;
+  }
+  if (t->cfg.init_ns > 0) {
+    spin_kernel<<<1, 32, 0, s>>>(t->cfg.init_ns, t->cfg.cooperative ? t->cancel_dev : nullptr);
+    return cu(cudaGetLastError(), "init spin");
+  }
   return FR_OK;
 }
 
@@ -115,6 +121,7 @@ extern "C" int fr_synthetic_task_create(const fr_synthetic_task_config* c, fr_si
                                         void** user) {
   if (!c || !vt || !user) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
   if (c->step_ns < 1) return frcapi::fail(FR_ERR_VALIDATION, "step_ns must be >= 1", "step_ns");
+  if (c->init_ns < 0) return frcapi::fail(FR_ERR_VALIDATION, "init_ns must be >= 0", "init_ns");
   if (c->memory_demand_gib < 0 || c->leak_gib_per_step < 0)
     return frcapi::fail(FR_ERR_VALIDATION, "memory sizes must be >= 0", "memory_demand");
   auto* t = new (std::nothrow) SynthTask;

@@ -26,6 +26,7 @@ __global__ void gap_kernel(GapArgs a) {
   if (a.mode == 2) {  // the run's first epoch starts now
     base = now;
     a.ctl->base_ns = base;
+    a.ctl->run0_ns = now;
   }
   if (a.slot_start >= 0) publish(a.ring, a.ring_mask, a.slot_start, a.code_start, now);
   std::uint64_t target;
@@ -61,7 +62,7 @@ __device__ __forceinline__ std::uint32_t ld_acquire_sys(const std::uint32_t* p) 
 // done), spin until the neighbour's flag reaches seq, BubbleEnded.
 __global__ void link_wait_kernel(LinkWaitArgs a) {
   const std::uint64_t now = frk::globaltimer_ns();
-  if (a.mode == 2) a.ctl->base_ns = now;
+  if (a.mode == 2) a.ctl->base_ns = a.ctl->run0_ns = now;
   if (a.slot_start >= 0) publish(a.ring, a.ring_mask, a.slot_start, a.code_start, now);
   if (a.flag) {
     // a watchdog, not a protocol step: a neighbour that never signals (a

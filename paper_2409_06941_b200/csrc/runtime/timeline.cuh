@@ -31,7 +31,7 @@ struct TimelineCtl {
   std::uint64_t last_ns;
   std::uint32_t end_seq;   // token of the last bubble that ended (imperative preemption)
   std::uint32_t link_timeouts;  // linked waits that gave up (neighbour never signalled)
-  std::uint32_t pad[2];
+  std::uint64_t run0_ns;        // the run's first gap (device clock): origin of the run's records
 };
 
 struct GapArgs {

@@ -76,6 +76,10 @@ class ImagePlan:
         """consecutive exact-2x launches may overlap (fr_img_plan_set_overlap)"""
         check(glib().fr_img_plan_set_overlap(self._h, int(bool(on))))
 
+    def set_max_sms(self, sms: int):
+        """launches occupy at most `sms` SMs (0 = all; fr_img_plan_set_max_sms)"""
+        check(glib().fr_img_plan_set_max_sms(self._h, int(sms)))
+
     @property
     def path(self) -> int:
         out = C.c_int32()
@@ -211,11 +215,12 @@ class SyntheticTask:
     that overruns its bubbles (Fig. 9 scenarios)."""
 
     def __init__(self, step_ns=200_000, profile_step_ns=0, memory_demand_gib=0.25,
-                 leak_gib_per_step=0.0, total_steps=0, cooperative=True):
+                 leak_gib_per_step=0.0, total_steps=0, cooperative=True, init_ns=0):
         self.cfg = A.SyntheticTaskConfigC(step_ns=step_ns, profile_step_ns=profile_step_ns,
                                           memory_demand_gib=memory_demand_gib,
                                           leak_gib_per_step=leak_gib_per_step,
-                                          total_steps=total_steps, cooperative=int(cooperative))
+                                          total_steps=total_steps, cooperative=int(cooperative),
+                                          init_ns=init_ns)
         self.vt = A.SideTaskVTableC()
         self.user = C.c_void_p()
         check(glib().fr_synthetic_task_create(C.byref(self.cfg), C.byref(self.vt), C.byref(self.user)))
@@ -373,6 +378,10 @@ class SgdProblem:
     def reinit(self, seed=3, stream=None):
         check(glib().fr_sgd_reinit(self._h, seed, _stream(stream)))
 
+    def set_max_sms(self, sms: int):
+        """steps occupy at most `sms` SMs (0 = all; fr_sgd_problem_set_max_sms)"""
+        check(glib().fr_sgd_problem_set_max_sms(self._h, int(sms)))
+
     def set_overlap(self, on: bool = True):
         """consecutive user-grouped steps on one stream may overlap
         (fr_sgd_problem_set_overlap; the built-in task's setting)"""
@@ -527,7 +536,8 @@ class Harness:
                  tokens=8192, ffn_mult=4, profile_reps=5, max_inflight_steps=2, gate_estimate=0,
                  gpu_memory_total=178.0, weight_mem=-1.0, activation_mem=-1.0,
                  fp_ticks=0, bp_ticks=0, profile_epochs=3, transport="replica",
-                 memory_headroom_gib=0.0, grace_ns=0, step_group=1, harvest_fraction=1.0):
+                 memory_headroom_gib=0.0, grace_ns=0, step_group=1, harvest_fraction=1.0,
+                 reclamation_delay_ns=0, side_sms=0):
         """transport="replica": this GPU replays stage `stage` against the
         device clock (one GPU); "linked": a real pipeline stage whose
         neighbours are linked through mailboxes (see link())."""
@@ -540,7 +550,8 @@ class Harness:
             activation_mem=activation_mem, fp_ticks_override=fp_ticks, bp_ticks_override=bp_ticks,
             profile_epochs=profile_epochs if tp == 0 else 0, transport=tp,
             memory_headroom_gib=memory_headroom_gib, grace_ns=grace_ns, step_group=step_group,
-            harvest_fraction=harvest_fraction)
+            harvest_fraction=harvest_fraction, reclamation_delay_ns=reclamation_delay_ns,
+            side_sms=side_sms)
         h = C.c_void_p()
         check(glib().fr_harness_create(C.byref(self.cfg), C.byref(h)))
         self._h = h
@@ -612,6 +623,42 @@ class Harness:
         d = r.as_dict()
         d["breakdown"] = r.breakdown.as_dict()
         return d
+
+    def set_side_sms(self, sms: int):
+        """SM budget of the side tasks' kernels (0 = all); re-profile after a run"""
+        check(glib().fr_harness_set_side_sms(self._h, int(sms)))
+
+    def task_memory(self, task_id: str) -> dict:
+        used, reserved = C.c_double(), C.c_double()
+        check(glib().fr_harness_task_memory(self._h, task_id.encode(), C.byref(used), C.byref(reserved)))
+        return {"used_gib": used.value, "reserved_gib": reserved.value}
+
+    def run_trace(self, check_trace: bool = True, trace_path=None) -> dict:
+        """The last run with tasks as a RunTrace (fr_harness_run_trace): the
+        simulated engine's dict layout, plus "violations" (fr_run_trace_check)"""
+        from . import api
+        h = C.c_void_p()
+        check(glib().fr_harness_run_trace(self._h, C.byref(h)))
+        return api().trace_dict(h, check_trace, trace_path)
+
+    def gate_log(self):
+        n = C.c_int64()
+        glib().fr_harness_gate_log(self._h, None, 0, C.byref(n))
+        buf = (A.GateRecordC * max(1, n.value))()
+        check(glib().fr_harness_gate_log(self._h, buf, n.value, C.byref(n)))
+        return [buf[i].as_dict() for i in range(n.value)]
+
+    def signal_log(self):
+        n = C.c_int64()
+        glib().fr_harness_signal_log(self._h, None, 0, C.byref(n))
+        buf = (A.SignalRecordC * max(1, n.value))()
+        check(glib().fr_harness_signal_log(self._h, buf, n.value, C.byref(n)))
+        out = []
+        for i in range(n.value):
+            d = buf[i].as_dict()
+            d["actions"] = [buf[i].actions[k] for k in range(buf[i].n_actions)]
+            out.append(d)
+        return out
 
     def timeline(self, which: int):
         n = C.c_int64()
