@@ -1002,8 +1002,12 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
   ck(cudaStreamSynchronize(side), "side sync");
   drain_completions();
   finish_init();
-  for (auto& kv : tasks)  // StopSideTask freed the task's memory: give the pages back
-    if (kv.second->rt.state == SideTaskState::Stopped && kv.second->pool) cudaMemPoolTrimTo(kv.second->pool, 0);
+  for (auto& kv : tasks) {  // StopSideTask freed the task's memory: give the pages back
+    const bool held = std::any_of(reclaim.begin(), reclaim.end(),
+                                  [&](const auto& x) { return x.first == kv.second.get(); });
+    if (kv.second->rt.state == SideTaskState::Stopped && kv.second->pool && !held)
+      cudaMemPoolTrimTo(kv.second->pool, 0);
+  }
   if (cfg.transport == 1) {
     std::uint32_t timeouts = 0;
     ck(cudaMemcpy(&timeouts, &ctl->link_timeouts, sizeof(timeouts), cudaMemcpyDeviceToHost), "timeouts");
