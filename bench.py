@@ -11,11 +11,21 @@ collective on the data path) -> scaling "weak".
 
 Headline workload (BASELINE.json configs[1]): the image resize + watermark
 side task (64 synthetic 4K RGB frames -> 1080p, RGBA watermark, 16 frames per
-RunNextStep).  The same run also measures configs[0] (PageRank, RMAT-20,
+RunNextStep), run on an SM budget (IMG_SMS) that holds the pipeline's ΔT
+under 1 %: on a power-capped B200 every joule a side task spends in a bubble
+is taken from the boost the pipeline's GEMMs get out of their idle bubbles,
+and the same bytes moved by fewer SMs cost far less power (DESIGN.md §5c;
+"image_full_gpu" under workloads is the same task on all 148 SMs).  The same run also measures configs[0] (PageRank, RMAT-20,
 two pull iterations per step), configs[2] (Graph-SGD, Orkut shape, rank
 16, 2^22 edges per step), configs[3] (mixed, 3.6B-shaped stages) and the
 image task through the imperative interface (device-preempted workload)
 under "workloads".
+
+ΔT is the PIPELINE's: the per-stage FP / BP op durations measured with and
+without the side task go through build_schedule (the reference's 1F1B DAG)
+and the makespan growth is reported (`delta_t`, paper_2409_06941_b200/
+pipeline_dt.py); the per-stage replica makespan growths are reported beside
+it (`delta_t_stage_max`).
 
 A bench *step* is one training iteration (epoch) of all 4 stages with the
 side task harvesting its bubbles.  Per stage and workload: the bubble
@@ -53,6 +63,11 @@ LAYERS_6B, HIDDEN_6B = 32, 4096                                       # nanoGPT-
 FRAMES = dict(sw=3840, sh=2160, dw=1920, dh=1080)
 BATCH = 64
 IMAGES_PER_STEP = int(os.environ.get("FR_IMAGES_PER_STEP", "16"))   # ~95 us steps (step size vs fill vs ΔT)
+# side-task SM budgets that keep the pipeline ΔT <= 1 % (DESIGN.md §5c,
+# scripts/harvest_sweep.py); 0 = all SMs.  PageRank is L2-resident and cheap
+# in power: it keeps every SM.
+IMG_SMS = int(os.environ.get("FR_IMG_SMS", "37"))
+SGD_SMS = int(os.environ.get("FR_SGD_SMS", "48"))
 STEP_GROUP = int(os.environ.get("FR_STEP_GROUP", "3"))   # steps between one pair of timing events
 E2E_IMAGES_PER_STEP = 1
 E2E_RING = int(os.environ.get("FR_E2E_RING", "128"))   # device staging slots: the copy engines run ahead of the steps
@@ -180,8 +195,26 @@ def cpu_sgd(seconds, edges=1 << 24):
                                      f"by-user layout), Hogwild OpenMP on {os.cpu_count()} host threads"}
 
 
+def cpu_info():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
 # ---------------------------------------------------------------- harvest
-def harvest(h, name, task, K, W):
+def harvest(h, name, task, K, W, sms=0, kinds=None):
+    """submit + warm-up + ΔT baseline + timed harvest on one stage replica;
+    `sms`: the side task's SM budget; `kinds`: the stage's issue-order op
+    kinds, for the per-stage mean FP / BP op durations of both runs"""
+    from paper_2409_06941_b200 import pipeline_dt as PD
+    h.set_side_sms(sms)
     ok, tprof = h.submit(name, task, profile_steps=32)
     if not ok:
         raise RuntimeError(f"{name}: rejected by Alg. 1")
@@ -197,11 +230,14 @@ def harvest(h, name, task, K, W):
         print(f"bench: {name} ran no step in {3 * max(W, 1)} warm-up epochs "
               f"({h.task_status(name)}); keeping the standalone profile", file=sys.stderr)
     base = h.run(K, False)
+    ops_base = PD.op_means(h.timeline(0), kinds) if kinds else None
     r = h.run(K, True)
+    ops_with = PD.op_means(h.timeline(0), kinds) if kinds else None
     durs = [b - a for a, b in h.timeline(2)]
     side, train = h.launches()
     h.stop_task(name)
     return {"base": base, "with": r, "durs": durs, "side": side, "train_ops": train,
+            "ops_base": ops_base, "ops_with": ops_with, "sms": sms,
             "units_per_step": task.units_per_step, "bytes_per_step": task.bytes_per_step,
             "h2d": task.h2d_per_step, "d2h": task.d2h_per_step, "est_step_s": tprof["est_per_step_duration"]}
 
@@ -224,7 +260,11 @@ def ours(args):
     from paper_2409_06941_b200 import gpu
     gpu.glib()
     K, W = args.steps, args.warmup
-    names = ["image", "image_imperative", "pagerank", "sgd"] + ([] if args.no_e2e else ["image_e2e"])
+    from paper_2409_06941_b200 import api as host_api
+    from paper_2409_06941_b200 import pipeline_dt as PD
+    A = host_api()
+    names = ["image", "image_full_gpu", "image_imperative", "pagerank", "sgd"] + ([] if args.no_e2e else ["image_e2e"])
+    sms_of = {"image": IMG_SMS, "image_imperative": IMG_SMS, "image_e2e": IMG_SMS, "sgd": SGD_SMS}
     runs = {n: [] for n in names}
     stage_prof = []
     if dist:
@@ -235,8 +275,9 @@ def ours(args):
             h = gpu.Harness(num_stages=STAGES, num_micro_batches=MICRO_BATCHES, stage=s, step_group=STEP_GROUP,
                             **SHAPE)
             stage_prof.append(h.profile())
+            kinds = PD.issue_kinds(A, s, STAGES, MICRO_BATCHES)
             for n in names:
-                if n == "image":
+                if n in ("image", "image_full_gpu"):
                     task = gpu.ImageTask(batch=BATCH, images_per_step=IMAGES_PER_STEP, **FRAMES)
                 elif n == "image_imperative":
                     task = gpu.ImageTask(batch=BATCH, images_per_step=IMAGES_PER_STEP, imperative=True, **FRAMES)
@@ -247,7 +288,7 @@ def ours(args):
                     task = gpu.PageRankTask(**PR)
                 else:
                     task = gpu.SgdTask(**SGD)
-                runs[n].append(harvest(h, n, task, K, W))
+                runs[n].append(harvest(h, n, task, K, W, sms=sms_of.get(n, 0), kinds=kinds))
             h.close()
     torch.cuda.synchronize()
     if dist:
@@ -258,77 +299,100 @@ def ours(args):
                     bubble_s=sum(r["base"]["bubble_s"] for r in rs),
                     t_no=sum(r["base"]["makespan_s"] for r in rs),
                     t_with=sum(r["with"]["makespan_s"] for r in rs),
+                    stage_dT=[(r["with"]["makespan_s"] - r["base"]["makespan_s"]) / r["base"]["makespan_s"] for r in rs],
+                    ops_base={i: r["ops_base"] for i, r in enumerate(rs)},
+                    ops_with={i: r["ops_with"] for i, r in enumerate(rs)},
                     used=sum(r["with"]["used_s"] for r in rs),
                     bubble_with=sum(r["with"]["bubble_s"] for r in rs),
                     overrun=sum(r["with"]["overrun_s"] for r in rs),
                     pauses=sum(r["with"]["pauses"] for r in rs),
                     steps=sum(r["with"]["steps_completed"] for r in rs),
                     launches=sum(r["side"] for r in rs),
+                    sms=rs[0]["sms"],
                     mean_step_s=statistics.fmean(d for r in rs for d in r["durs"]) if any(r["durs"] for r in rs) else None,
                     bytes_per_step=rs[0]["bytes_per_step"], units_per_step=rs[0]["units_per_step"],
                     h2d=sum(r["h2d"] * r["with"]["steps_completed"] for r in rs),
                     d2h=sum(r["d2h"] * r["with"]["steps_completed"] for r in rs))
 
+    def pipe_dt(rs, p, m, epochs):
+        """the linked pipeline's ΔT from the replicas' op durations (pipeline_dt)"""
+        base = {r_["stage"]: r_["ops_base"] for r_ in rs}
+        with_ = {r_["stage"]: r_["ops_with"] for r_ in rs}
+        return PD.critical_path_dt(A, p, m, epochs, base, with_)
+
     local_res = {n: agg(runs[n]) for n in names}
+    for n in names:
+        local_res[n]["pipeline"] = pipe_dt([dict(r_, stage=i) for i, r_ in enumerate(runs[n])], STAGES,
+                                           MICRO_BATCHES, K)
     local_res["clocks"] = clk.summary()
     local_res["gap_kernels"] = sum(r["train_ops"] // (2 * MICRO_BATCHES) * (2 * MICRO_BATCHES + 1)
                                    for r in runs["image"])
     local_res["stages"] = [{"stage": s, "fp_ms": p["fp_ticks"] / 1e6, "bp_ms": p["bp_ticks"] / 1e6,
                             "fp_tflops": p["fp_tflops"], "bp_tflops": p["bp_tflops"],
                             "bubble_ms_per_epoch": p["stage_bubble_ticks"] / 1e6,
-                            "dT_image": (runs["image"][s]["with"]["makespan_s"] - runs["image"][s]["base"]["makespan_s"])
-                            / runs["image"][s]["base"]["makespan_s"],
+                            "dT": {n: local_res[n]["stage_dT"][s] for n in names},
+                            "op_growth_image": local_res["image"]["pipeline"]["op_growth"][s],
                             "fill_image": runs["image"][s]["with"]["used_s"] / runs["image"][s]["with"]["bubble_s"],
                             "breakdown_image": runs["image"][s]["with"]["breakdown"]}
                            for s, p in enumerate(stage_prof)]
     # configs[3]: mixed side tasks over a 3.6B-shaped pipeline, placed by Alg. 1
     mixed = None
     if not args.no_mixed:
-        from paper_2409_06941_b200 import api as host_api
-        a = host_api()
         probe = gpu.Harness(num_stages=STAGES, num_micro_batches=MICRO_BATCHES, stage=0,
                             profile_epochs=0, profile_reps=1, **SHAPE_36B)
         avail = [probe.profile()["available_memory"]]
         probe.close()
-        specs = [("pagerank", lambda: gpu.PageRankTask(**PR)), ("sgd", lambda: gpu.SgdTask(**SGD)),
-                 ("image", lambda: gpu.ImageTask(batch=BATCH, images_per_step=IMAGES_PER_STEP, **FRAMES)),
-                 ("pagerank2", lambda: gpu.PageRankTask(**PR))]
+        specs = [("pagerank", lambda: gpu.PageRankTask(**PR), 0), ("sgd", lambda: gpu.SgdTask(**SGD), SGD_SMS),
+                 ("image", lambda: gpu.ImageTask(batch=BATCH, images_per_step=IMAGES_PER_STEP, **FRAMES), IMG_SMS),
+                 ("pagerank2", lambda: gpu.PageRankTask(**PR), 0)]
         from paper_2409_06941_b200.bubblesim import TaskProfile
         mem = {"pagerank": 0.3, "pagerank2": 0.3, "sgd": 1.6, "image": 2.2}
-        wstates = a.workers([avail[0]] * STAGES)   # replica: every stage sees its own GPU's memory
+        wstates = A.workers([avail[0]] * STAGES)   # replica: every stage sees its own GPU's memory
         placement = {}
-        for name, _ in specs:
-            o = a.submit_task(TaskProfile(name, 1e-4, 1e-4, mem[name], 32), wstates)
+        for name, _, _ in specs:
+            o = A.submit_task(TaskProfile(name, 1e-4, 1e-4, mem[name], 32), wstates)
             placement[name] = o.worker_id if o.assigned else None
         mixed = {"placement": placement, "stages": []}
-        for name, make in specs:
+        mruns = []
+        for name, make, sms in specs:
             s = placement[name]
             if s is None:
                 continue
             h = gpu.Harness(num_stages=STAGES, num_micro_batches=MICRO_BATCHES, stage=s, step_group=STEP_GROUP,
                             **SHAPE_36B)
-            r = harvest(h, name, make(), K, W)
+            r = harvest(h, name, make(), K, W, sms=sms, kinds=PD.issue_kinds(A, s, STAGES, MICRO_BATCHES))
             h.close()
+            mruns.append(dict(r, stage=s))
             mixed["stages"].append({"stage": s, "task": name, "units_per_bubble_s": r["with"]["work_units"] / r["base"]["bubble_s"],
-                                    "unit": "px" if name == "image" else "edges",
+                                    "unit": "px" if name == "image" else "edges", "side_sms": sms,
                                     "dT": (r["with"]["makespan_s"] - r["base"]["makespan_s"]) / r["base"]["makespan_s"],
                                     "fill": r["with"]["used_s"] / r["with"]["bubble_s"]})
-        mixed["dT_max"] = max(x["dT"] for x in mixed["stages"])
+        mixed["dT_stage_max"] = max(x["dT"] for x in mixed["stages"])
+        if len({r_["stage"] for r_ in mruns}) == STAGES:
+            mixed["dT_pipeline"] = pipe_dt(mruns, STAGES, MICRO_BATCHES, K)["dT"]
         mixed["fill_mean"] = statistics.fmean(x["fill"] for x in mixed["stages"])
     local_res["mixed"] = mixed
-    # configs[4] at N = 1: one stage of the 8-stage, m = 8 pipeline of
-    # nanoGPT-6B-shaped stages (32/8 layers of h = 4096 each), replayed
+    # configs[4] at N = 1: every stage of the 8-stage, m = 8 pipeline of
+    # nanoGPT-6B-shaped stages (32/8 layers of h = 4096 each) replayed in turn
     c5 = None
     if not args.no_c5:
-        h = gpu.Harness(num_stages=8, num_micro_batches=8, stage=3, layers=LAYERS_6B // 8, hidden=HIDDEN_6B,
-                        tokens=8192, ffn_mult=4, step_group=STEP_GROUP)
-        prof = h.profile()
-        r = harvest(h, "image", gpu.ImageTask(batch=BATCH, images_per_step=IMAGES_PER_STEP, **FRAMES), K, W)
-        h.close()
+        K5 = min(K, 4)
+        c5runs, prof = [], None
+        for s in range(8):
+            h = gpu.Harness(num_stages=8, num_micro_batches=8, stage=s, layers=LAYERS_6B // 8, hidden=HIDDEN_6B,
+                            tokens=8192, ffn_mult=4, step_group=STEP_GROUP, profile_epochs=2)
+            prof = prof or h.profile()
+            r = harvest(h, "image", gpu.ImageTask(batch=BATCH, images_per_step=IMAGES_PER_STEP, **FRAMES), K5, W,
+                        sms=IMG_SMS, kinds=PD.issue_kinds(A, s, 8, 8))
+            h.close()
+            c5runs.append(dict(r, stage=s))
+        pipe = pipe_dt(c5runs, 8, 8, K5)
         c5 = {"bubble_rate": prof["bubble_rate"], "fp_ms": prof["fp_ticks"] / 1e6, "bp_ms": prof["bp_ticks"] / 1e6,
-              "units_per_bubble_s": r["with"]["work_units"] / r["base"]["bubble_s"],
-              "dT": (r["with"]["makespan_s"] - r["base"]["makespan_s"]) / r["base"]["makespan_s"],
-              "fill": r["with"]["used_s"] / r["with"]["bubble_s"]}
+              "epochs": K5, "side_sms": IMG_SMS,
+              "units_per_bubble_s": sum(r_["with"]["work_units"] for r_ in c5runs) / sum(r_["base"]["bubble_s"] for r_ in c5runs),
+              "dT_pipeline": pipe["dT"],
+              "dT_stage_max": max((r_["with"]["makespan_s"] - r_["base"]["makespan_s"]) / r_["base"]["makespan_s"] for r_ in c5runs),
+              "fill": sum(r_["with"]["used_s"] for r_ in c5runs) / sum(r_["with"]["bubble_s"] for r_ in c5runs)}
     local_res["c5"] = c5
     # configs[4] / SURVEY §8(e): with N > 1 GPUs, additionally a REAL N-stage
     # pipeline (6B-shaped stages, rank s = stage s) whose activations and
@@ -342,7 +406,7 @@ def ours(args):
             linked = D.linked_harvest(
                 lambda: gpu.ImageTask(batch=BATCH, images_per_step=IMAGES_PER_STEP, **FRAMES),
                 shape, num_micro_batches=max(MICRO_BATCHES, ws), epochs=K, warmup=W, task_name="image",
-                step_group=STEP_GROUP)
+                step_group=STEP_GROUP, side_sms=IMG_SMS)
             linked["shape"] = shape
         except Exception as e:  # noqa: BLE001 -- reported in the JSON line
             print(f"[bench] rank {rank}: linked pipeline failed: {e!r}", file=sys.stderr, flush=True)
@@ -378,8 +442,16 @@ def emit(args, results, ws, names, csr):
         return sum(r[n]["units"] for r in results) / max(r[n]["bubble_s"] for r in results)
 
     def dT(n):
-        t_no = max(r[n]["t_no"] for r in results)
-        return (max(r[n]["t_with"] for r in results) - t_no) / t_no
+        """the pipeline's ΔT (build_schedule over the measured op durations), max over ranks"""
+        return max(r[n]["pipeline"]["dT"] for r in results)
+
+    def dT_stages(n):
+        return max(x for r in results for x in r[n]["stage_dT"])
+
+    def dT_fields(n):
+        return {"dT": dT(n), "dT_stage_max": dT_stages(n),
+                "dT_stages": results[0][n]["stage_dT"], "side_sms": results[0][n]["sms"] or 148,
+                "dT_budget_met": dT(n) <= 0.01}
 
     def fill(n):
         return sum(r[n]["used"] for r in results) / sum(r[n]["bubble_with"] for r in results)
@@ -399,24 +471,26 @@ def emit(args, results, ws, names, csr):
     image_roof = roof("image", f"img_resize2x_wm_tma ({IMAGES_PER_STEP} frames/launch, in-pipeline)")
     image_roof["traffic"] = traffic
     cpu = cpu_image(args.cpu_seconds) if not args.no_cpu else None
+    if cpu:
+        cpu.update(cpu_info())
     e2e = None
     if "image_e2e" in names:
         e2e = {"value": rate("image_e2e"), "unit": UNIT,
                "h2d_bytes_per_step": sum(r["image_e2e"]["h2d"] for r in results) / (K * STAGES),
                "d2h_bytes_per_step": sum(r["image_e2e"]["d2h"] for r in results) / (K * STAGES),
-               "dT": dT("image_e2e"), "fill": fill("image_e2e"),
+               **dT_fields("image_e2e"), "fill": fill("image_e2e"),
                "path": f"fr_image_task host_io=1: pinned host frames -> {E2E_RING}-slot device ring filled by the "
                        "copy engines ahead of the steps (also while the pipeline computes) -> K5 -> D2H per frame"}
     workloads = {
         "pagerank": {"config": "configs[0]: RMAT scale 20 (edge factor 16, seed 1), pull, d=0.85, 2 iterations/step",
-                     "value": rate("pagerank"), "unit": "edges/bubble-s", "dT": dT("pagerank"),
+                     "value": rate("pagerank"), "unit": "edges/bubble-s", **dT_fields("pagerank"),
                      "fill": fill("pagerank"),
                      "roofline": roof("pagerank", "pr_pull_kernel (2 launches of 1 iteration per step, in-pipeline); "
                                       "working set L2-resident: latency-bound gathers, not HBM"),
                      "cpu_baseline": cpu_pagerank(args.cpu_seconds / 2, csr) if csr is not None else None},
         "sgd": {"config": f"configs[2]: Orkut shape V=3,072,441 E=117,185,083 k=16, {SGD['edges_per_step']} edges/step, "
                           "by-user layout (fr_sgd_group_by_user)",
-                "value": rate("sgd"), "unit": "edges/bubble-s", "dT": dT("sgd"), "fill": fill("sgd"),
+                "value": rate("sgd"), "unit": "edges/bubble-s", **dT_fields("sgd"), "fill": fill("sgd"),
                 "roofline": dict(roof("sgd", f"sgd_user_kernel<16> ({SGD['edges_per_step']} edges/launch, in-pipeline; "
                                              "alg bytes 12 + 128 per edge + 128 per L_u load; item blocks keep "
                                              "L_v in L2, so part of them never reaches DRAM)") or {},
@@ -428,13 +502,19 @@ def emit(args, results, ws, names, csr):
     workloads["image_imperative"] = {
         "config": "configs[1] through the imperative interface (RunGpuWorkload): one preemptible K5 "
                   "workload per bubble over the 64-frame batch, paused on the device per output row",
-        "value": rate("image_imperative"), "unit": UNIT, "dT": dT("image_imperative"),
+        "value": rate("image_imperative"), "unit": UNIT, **dT_fields("image_imperative"),
         "fill": fill("image_imperative"),
         "overrun_per_pause_us": sum(r["image_imperative"]["overrun"] for r in results)
         / max(1, sum(r["image_imperative"]["pauses"] for r in results)) * 1e6,
         "alg_GBps_in_bubbles": imp["units"] / OUT_PX * (FRAMES["sw"] * FRAMES["sh"] * 3 + OUT_PX * 3)
         / max(1e-12, imp["used"] + imp["overrun"]) / 1e9,
         "workload_launches": imp["launches"]}
+    workloads["image_full_gpu"] = {
+        "config": "configs[1] with the side task on all 148 SMs: the most px per bubble-second, but the "
+                  "power its HBM streaming draws slows every GEMM of the pipeline (DESIGN.md §5c)",
+        "value": rate("image_full_gpu"), "unit": UNIT, **dT_fields("image_full_gpu"), "fill": fill("image_full_gpu"),
+        "roofline": roof("image_full_gpu", f"img_resize2x_wm_tma ({IMAGES_PER_STEP} frames/launch, 148 SMs, "
+                                           "in-pipeline)")}
     launches = sum(r[n]["launches"] for r in results for n in names) + sum(r["gap_kernels"] for r in results)
     line = {
         "metric": METRIC, "value": rate("image"), "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": W,
@@ -444,9 +524,13 @@ def emit(args, results, ws, names, csr):
         "config": {"workload": WORKLOAD, "stages": STAGES, "micro_batches": MICRO_BATCHES, "stage_shape": SHAPE,
                    "frames": BATCH, "images_per_step": IMAGES_PER_STEP,
                    "step": "one 1F1B epoch of all 4 stages (replayed) with the side task",
-                   "parallelism": f"replicas x{ws}", "step_group": STEP_GROUP,
+                   "parallelism": f"replicas x{ws}", "step_group": STEP_GROUP, "side_sms": IMG_SMS or 148,
                    "l2": "image inputs 1.6 GB per batch > 126 MB L2; no flush needed"},
-        "delta_t": dT("image"), "fill": fill("image"),
+        "delta_t": dT("image"),
+        "delta_t_def": "pipeline makespan growth: per-stage mean FP/BP op durations with vs without the side task "
+                       "(every stage replayed) through build_schedule (pipeline_dt.critical_path_dt)",
+        "delta_t_stage_max": dT_stages("image"), "delta_t_stages": results[0]["image"]["stage_dT"],
+        "dT_budget_met": dT("image") <= 0.01, "fill": fill("image"),
         "overrun_frac": sum(r["image"]["overrun"] for r in results) / max(1e-12, sum(r["image"]["used"] for r in results)),
         "bubble_s_per_step": max(r["image"]["bubble_s"] for r in results) / K,
         "px_per_step": sum(r["image"]["units"] for r in results) / K,
@@ -494,8 +578,9 @@ def emit(args, results, ws, names, csr):
     if results[0].get("c5"):
         workloads["c5_stage_replay"] = dict(
             results[0]["c5"], unit=UNIT,
-            config="configs[4] at one GPU: stage 3 of an 8-stage m=8 1F1B pipeline of nanoGPT-6B-shaped "
-                   f"stages (4 layers x h 4096 each) replayed, image side task, {IMAGES_PER_STEP} frames/step")
+            config="configs[4] at one GPU: every stage of an 8-stage m=8 1F1B pipeline of nanoGPT-6B-shaped "
+                   f"stages (4 layers x h 4096 each) replayed in turn, image side task, {IMAGES_PER_STEP} "
+                   "frames/step; dT_pipeline through build_schedule over the 8 stages' op durations")
     if results[0].get("mixed"):
         workloads["mixed"] = dict(results[0]["mixed"],
                                   config="configs[3]: PageRank + SGD + Image + PageRank on a "
@@ -520,7 +605,7 @@ def reference(args):
             "impl": "reference",
             "config": {"workload": WORKLOAD, "frames": BATCH, "images_per_step": IMAGES_PER_STEP},
             "cpu_baseline": {"value": v, "unit": "px/s", "cores": vals[0]["cores"], "kind": "port",
-                             "sample": vals[0]["sample"]},
+                             "sample": vals[0]["sample"], **cpu_info()},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "note": "the reference ships no side-task code (task.hpp:36-38); this is the CPU restatement "
                     "(oracle/sidetasks.c) -- every CPU second of work counted as a bubble-second"}

@@ -369,7 +369,13 @@ typedef struct fr_harness_config {
                                    task's pool pages go back to the device this long after
                                    the kill (<= 0: at once) */
   int32_t side_sms;           /* SM budget of the side tasks' kernels (set_sm_budget;
-                                 0 = all SMs) */
+                                 0 = all SMs); the starting point when dt_budget > 0 */
+  int32_t min_side_sms;       /* floor of the ΔT controller (<= 0: 8) */
+  double dt_budget;           /* > 0: ΔT-budgeted harvesting.  The worker times every op
+                                 of the stage as it completes, compares it with the same
+                                 op in the last run without side tasks, and sizes the side
+                                 tasks' SM budget so the stage's ops run at most this
+                                 fraction slower (e.g. 0.007); <= 0: fixed side_sms */
 } fr_harness_config;
 
 /* All durations in ns ticks (tick_seconds = 1e-9). */
@@ -406,6 +412,11 @@ typedef struct fr_run_report {
   int64_t kills_pause_timeout;  /* framework_enforce Kill (limits.hpp:34) */
   int64_t kills_init_timeout;   /* ArmInitGuard fired with InitSideTask still running
                                    (manager.hpp:58, KillReason::InitTimeout) */
+  double op_growth;             /* mean (op duration / same op in the last run without
+                                   side tasks) - 1 over this run's ops (0 if no reference) */
+  double side_sms_mean;         /* side-task SM budget averaged over the run's ops */
+  int32_t side_sms_final;       /* the budget at the run's end (ΔT controller state) */
+  int32_t reserved2;
 } fr_run_report;
 
 int fr_harness_create(const fr_harness_config* cfg, fr_harness** out);

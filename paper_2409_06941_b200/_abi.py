@@ -547,6 +547,7 @@ class HarnessConfigC(Struct):
         ("profile_epochs", i32), ("transport", i32),
         ("memory_headroom_gib", dbl), ("grace_ns", i64), ("step_group", i32),
         ("harvest_fraction", dbl), ("reclamation_delay_ns", i64), ("side_sms", i32),
+        ("min_side_sms", i32), ("dt_budget", dbl),
     ]
 
 
@@ -577,6 +578,7 @@ class RunReportC(Struct):
         ("dispatch_host_us", dbl), ("max_step_overrun_s", dbl),
         ("breakdown", StageBreakdownC), ("pauses", i64), ("kills", i64),
         ("kills_oom", i64), ("kills_pause_timeout", i64), ("kills_init_timeout", i64),
+        ("op_growth", dbl), ("side_sms_mean", dbl), ("side_sms_final", i32), ("reserved2", i32),
     ]
 
 

@@ -537,7 +537,7 @@ class Harness:
                  gpu_memory_total=178.0, weight_mem=-1.0, activation_mem=-1.0,
                  fp_ticks=0, bp_ticks=0, profile_epochs=3, transport="replica",
                  memory_headroom_gib=0.0, grace_ns=0, step_group=1, harvest_fraction=1.0,
-                 reclamation_delay_ns=0, side_sms=0):
+                 reclamation_delay_ns=0, side_sms=0, dt_budget=0.0, min_side_sms=0):
         """transport="replica": this GPU replays stage `stage` against the
         device clock (one GPU); "linked": a real pipeline stage whose
         neighbours are linked through mailboxes (see link())."""
@@ -551,7 +551,7 @@ class Harness:
             profile_epochs=profile_epochs if tp == 0 else 0, transport=tp,
             memory_headroom_gib=memory_headroom_gib, grace_ns=grace_ns, step_group=step_group,
             harvest_fraction=harvest_fraction, reclamation_delay_ns=reclamation_delay_ns,
-            side_sms=side_sms)
+            side_sms=side_sms, dt_budget=dt_budget, min_side_sms=min_side_sms)
         h = C.c_void_p()
         check(glib().fr_harness_create(C.byref(self.cfg), C.byref(h)))
         self._h = h
