@@ -63,11 +63,14 @@ LAYERS_6B, HIDDEN_6B = 32, 4096                                       # nanoGPT-
 FRAMES = dict(sw=3840, sh=2160, dw=1920, dh=1080)
 BATCH = 64
 IMAGES_PER_STEP = int(os.environ.get("FR_IMAGES_PER_STEP", "16"))   # ~95 us steps (step size vs fill vs ΔT)
-# side-task SM budgets that keep the pipeline ΔT <= 1 % (DESIGN.md §5c,
-# scripts/harvest_sweep.py); 0 = all SMs.  PageRank is L2-resident and cheap
-# in power: it keeps every SM.
-IMG_SMS = int(os.environ.get("FR_IMG_SMS", "37"))
-SGD_SMS = int(os.environ.get("FR_SGD_SMS", "48"))
+# ΔT-budgeted harvesting: every stage's worker holds its ops'
+# slowdown under DT_BUDGET by sizing the side tasks' SM budget, starting from
+# IMG_SMS / SGD_SMS (scripts/harvest_sweep.py measured 16-24 SMs for the
+# image task at <= 1 %); PageRank is L2-resident and cheap in power and
+# starts from every SM.
+DT_BUDGET = float(os.environ.get("FR_DT_BUDGET", "0.007"))
+IMG_SMS = int(os.environ.get("FR_IMG_SMS", "24"))
+SGD_SMS = int(os.environ.get("FR_SGD_SMS", "32"))
 STEP_GROUP = int(os.environ.get("FR_STEP_GROUP", "3"))   # steps between one pair of timing events
 E2E_IMAGES_PER_STEP = 1
 E2E_RING = int(os.environ.get("FR_E2E_RING", "128"))   # device staging slots: the copy engines run ahead of the steps
@@ -209,11 +212,13 @@ def cpu_info():
 
 
 # ---------------------------------------------------------------- harvest
-def harvest(h, name, task, K, W, sms=0, kinds=None):
+def harvest(h, name, task, K, W, sms=0, kinds=None, budget=0.0):
     """submit + warm-up + ΔT baseline + timed harvest on one stage replica;
-    `sms`: the side task's SM budget; `kinds`: the stage's issue-order op
-    kinds, for the per-stage mean FP / BP op durations of both runs"""
+    `sms`: the side task's SM budget (the ΔT controller's start when
+    budget > 0); `kinds`: the stage's issue-order op kinds, for the per-stage
+    mean FP / BP op durations of both runs"""
     from paper_2409_06941_b200 import pipeline_dt as PD
+    h.set_dt_budget(budget)
     h.set_side_sms(sms)
     ok, tprof = h.submit(name, task, profile_steps=32)
     if not ok:
@@ -237,7 +242,7 @@ def harvest(h, name, task, K, W, sms=0, kinds=None):
     side, train = h.launches()
     h.stop_task(name)
     return {"base": base, "with": r, "durs": durs, "side": side, "train_ops": train,
-            "ops_base": ops_base, "ops_with": ops_with, "sms": sms,
+            "ops_base": ops_base, "ops_with": ops_with, "sms": r["side_sms_mean"], "budget": budget,
             "units_per_step": task.units_per_step, "bytes_per_step": task.bytes_per_step,
             "h2d": task.h2d_per_step, "d2h": task.d2h_per_step, "est_step_s": tprof["est_per_step_duration"]}
 
@@ -288,7 +293,8 @@ def ours(args):
                     task = gpu.PageRankTask(**PR)
                 else:
                     task = gpu.SgdTask(**SGD)
-                runs[n].append(harvest(h, n, task, K, W, sms=sms_of.get(n, 0), kinds=kinds))
+                runs[n].append(harvest(h, n, task, K, W, sms=sms_of.get(n, 0), kinds=kinds,
+                                       budget=0.0 if n == "image_full_gpu" else DT_BUDGET))
             h.close()
     torch.cuda.synchronize()
     if dist:
@@ -308,7 +314,7 @@ def ours(args):
                     pauses=sum(r["with"]["pauses"] for r in rs),
                     steps=sum(r["with"]["steps_completed"] for r in rs),
                     launches=sum(r["side"] for r in rs),
-                    sms=rs[0]["sms"],
+                    sms=statistics.fmean(r["sms"] for r in rs), budget=rs[0]["budget"],
                     mean_step_s=statistics.fmean(d for r in rs for d in r["durs"]) if any(r["durs"] for r in rs) else None,
                     bytes_per_step=rs[0]["bytes_per_step"], units_per_step=rs[0]["units_per_step"],
                     h2d=sum(r["h2d"] * r["with"]["steps_completed"] for r in rs),
@@ -360,11 +366,12 @@ def ours(args):
                 continue
             h = gpu.Harness(num_stages=STAGES, num_micro_batches=MICRO_BATCHES, stage=s, step_group=STEP_GROUP,
                             **SHAPE_36B)
-            r = harvest(h, name, make(), K, W, sms=sms, kinds=PD.issue_kinds(A, s, STAGES, MICRO_BATCHES))
+            r = harvest(h, name, make(), K, W, sms=sms, kinds=PD.issue_kinds(A, s, STAGES, MICRO_BATCHES),
+                        budget=DT_BUDGET)
             h.close()
             mruns.append(dict(r, stage=s))
             mixed["stages"].append({"stage": s, "task": name, "units_per_bubble_s": r["with"]["work_units"] / r["base"]["bubble_s"],
-                                    "unit": "px" if name == "image" else "edges", "side_sms": sms,
+                                    "unit": "px" if name == "image" else "edges", "side_sms_mean": r["sms"],
                                     "dT": (r["with"]["makespan_s"] - r["base"]["makespan_s"]) / r["base"]["makespan_s"],
                                     "fill": r["with"]["used_s"] / r["with"]["bubble_s"]})
         mixed["dT_stage_max"] = max(x["dT"] for x in mixed["stages"])
@@ -383,12 +390,12 @@ def ours(args):
                             tokens=8192, ffn_mult=4, step_group=STEP_GROUP, profile_epochs=2)
             prof = prof or h.profile()
             r = harvest(h, "image", gpu.ImageTask(batch=BATCH, images_per_step=IMAGES_PER_STEP, **FRAMES), K5, W,
-                        sms=IMG_SMS, kinds=PD.issue_kinds(A, s, 8, 8))
+                        sms=IMG_SMS, kinds=PD.issue_kinds(A, s, 8, 8), budget=DT_BUDGET)
             h.close()
             c5runs.append(dict(r, stage=s))
         pipe = pipe_dt(c5runs, 8, 8, K5)
         c5 = {"bubble_rate": prof["bubble_rate"], "fp_ms": prof["fp_ticks"] / 1e6, "bp_ms": prof["bp_ticks"] / 1e6,
-              "epochs": K5, "side_sms": IMG_SMS,
+              "epochs": K5, "side_sms_mean": statistics.fmean(r_["sms"] for r_ in c5runs),
               "units_per_bubble_s": sum(r_["with"]["work_units"] for r_ in c5runs) / sum(r_["base"]["bubble_s"] for r_ in c5runs),
               "dT_pipeline": pipe["dT"],
               "dT_stage_max": max((r_["with"]["makespan_s"] - r_["base"]["makespan_s"]) / r_["base"]["makespan_s"] for r_ in c5runs),
@@ -406,7 +413,7 @@ def ours(args):
             linked = D.linked_harvest(
                 lambda: gpu.ImageTask(batch=BATCH, images_per_step=IMAGES_PER_STEP, **FRAMES),
                 shape, num_micro_batches=max(MICRO_BATCHES, ws), epochs=K, warmup=W, task_name="image",
-                step_group=STEP_GROUP, side_sms=IMG_SMS)
+                step_group=STEP_GROUP, side_sms=IMG_SMS, dt_budget=DT_BUDGET)
             linked["shape"] = shape
         except Exception as e:  # noqa: BLE001 -- reported in the JSON line
             print(f"[bench] rank {rank}: linked pipeline failed: {e!r}", file=sys.stderr, flush=True)
@@ -450,7 +457,8 @@ def emit(args, results, ws, names, csr):
 
     def dT_fields(n):
         return {"dT": dT(n), "dT_stage_max": dT_stages(n),
-                "dT_stages": results[0][n]["stage_dT"], "side_sms": results[0][n]["sms"] or 148,
+                "dT_stages": results[0][n]["stage_dT"], "side_sms_mean": results[0][n]["sms"],
+                "dt_budget": results[0][n]["budget"],
                 "dT_budget_met": dT(n) <= 0.01}
 
     def fill(n):
@@ -524,7 +532,8 @@ def emit(args, results, ws, names, csr):
         "config": {"workload": WORKLOAD, "stages": STAGES, "micro_batches": MICRO_BATCHES, "stage_shape": SHAPE,
                    "frames": BATCH, "images_per_step": IMAGES_PER_STEP,
                    "step": "one 1F1B epoch of all 4 stages (replayed) with the side task",
-                   "parallelism": f"replicas x{ws}", "step_group": STEP_GROUP, "side_sms": IMG_SMS or 148,
+                   "parallelism": f"replicas x{ws}", "step_group": STEP_GROUP, "dt_budget": DT_BUDGET,
+                   "side_sms_start": IMG_SMS, "side_sms_mean": results[0]["image"]["sms"],
                    "l2": "image inputs 1.6 GB per batch > 126 MB L2; no flush needed"},
         "delta_t": dT("image"),
         "delta_t_def": "pipeline makespan growth: per-stage mean FP/BP op durations with vs without the side task "
@@ -551,6 +560,10 @@ def emit(args, results, ws, names, csr):
             "unit": UNIT, "dT": (max(x["with"]["makespan_s"] for x in ls) - t_no) / t_no,
             "fill": sum(x["with"]["used_s"] for x in ls) / sum(x["with"]["bubble_s"] for x in ls),
             "bubble_rate": ls[0]["profile"]["bubble_rate"],
+            "exchange": {"messages": sum(x["with"]["exchange_messages"] for x in ls),
+                         "us_per_message": statistics.fmean(x["with"]["exchange_us"] for x in ls if x["with"]["exchange_messages"]),
+                         "GBps": statistics.fmean(x["with"]["exchange_gbps"] for x in ls if x["with"]["exchange_messages"]),
+                         "how": "copy engine, mailbox slot on the neighbour GPU (NVLink peer memory)"},
             "stages": [{"stage": x["stage"], "dT": (x["with"]["makespan_s"] - x["base"]["makespan_s"])
                         / x["base"]["makespan_s"], "fill": x["with"]["used_s"] / max(1e-12, x["with"]["bubble_s"])}
                        for x in ls]}

@@ -417,6 +417,11 @@ typedef struct fr_run_report {
   double side_sms_mean;         /* side-task SM budget averaged over the run's ops */
   int32_t side_sms_final;       /* the budget at the run's end (ΔT controller state) */
   int32_t reserved2;
+  /* transport 1: the stage-to-stage exchange (activation / gradient messages
+   * this stage sent, copy engine into the neighbour's mailbox) */
+  int64_t exchange_messages;
+  double exchange_us;           /* mean device time per message copy */
+  double exchange_gbps;         /* message bytes / copy time */
 } fr_run_report;
 
 int fr_harness_create(const fr_harness_config* cfg, fr_harness** out);
@@ -445,6 +450,9 @@ int fr_harness_set_harvest_fraction(fr_harness* h, double fraction);
  * tasks' step estimates change with it: re-profile (fr_harness_reprofile)
  * after a run at the new budget */
 int fr_harness_set_side_sms(fr_harness* h, int32_t sms);
+/* ΔT budget of the next runs (fr_harness_config::dt_budget; 0 = off); the
+ * controller restarts from side_sms */
+int fr_harness_set_dt_budget(fr_harness* h, double budget);
 /* Runs `epochs` epochs; with_tasks=0 is the ΔT baseline. Blocks. */
 int fr_harness_run(fr_harness* h, int32_t epochs, int32_t with_tasks, fr_run_report* out);
 /* a submitted task's state (enum fr_task_state), disposition (enum

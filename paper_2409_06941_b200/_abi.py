@@ -579,6 +579,7 @@ class RunReportC(Struct):
         ("breakdown", StageBreakdownC), ("pauses", i64), ("kills", i64),
         ("kills_oom", i64), ("kills_pause_timeout", i64), ("kills_init_timeout", i64),
         ("op_growth", dbl), ("side_sms_mean", dbl), ("side_sms_final", i32), ("reserved2", i32),
+        ("exchange_messages", i64), ("exchange_us", dbl), ("exchange_gbps", dbl),
     ]
 
 
@@ -593,6 +594,7 @@ GPU_PROTOTYPES.update({
     "fr_harness_destroy": (C.c_int, [vp]),
     "fr_harness_set_harvest_fraction": (C.c_int, [vp, dbl]),
     "fr_harness_set_side_sms": (C.c_int, [vp, i32]),
+    "fr_harness_set_dt_budget": (C.c_int, [vp, dbl]),
     "fr_harness_task_memory": (C.c_int, [vp, cp, P(dbl), P(dbl)]),
     "fr_harness_run_trace": (C.c_int, [vp, P(vp)]),
     "fr_harness_gate_log": (C.c_int, [vp, P(GateRecordC), i64, P(i64)]),

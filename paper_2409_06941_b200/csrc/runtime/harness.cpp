@@ -528,6 +528,7 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
   //      as a training framework would, so the worker never blocks on it)
   struct EpochEvents {
     std::vector<cudaEvent_t> op_start, op_end;
+    std::vector<cudaEvent_t> send_a, send_b;  // transport 1: the op's message copy to its neighbour
     cudaEvent_t end;
   };
   std::vector<EpochEvents> eev(static_cast<std::size_t>(epochs));
@@ -537,6 +538,14 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
     for (int i = 0; i < nops; ++i) {
       e.op_start[i] = ev();
       e.op_end[i] = ev();
+    }
+    if (cfg.transport == 1) {
+      e.send_a.resize(static_cast<std::size_t>(nops));
+      e.send_b.resize(static_cast<std::size_t>(nops));
+      for (int i = 0; i < nops; ++i) {
+        e.send_a[i] = ev();
+        e.send_b[i] = ev();
+      }
     }
     e.end = ev();
   }
@@ -598,8 +607,10 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
               if (op.kind == OpKind::FP && st < p - 1) to = &next_mbox, dir = 0;
               if (op.kind == OpKind::BP && st > 0) to = &prev_mbox, dir = 1;
               if (to) {
+                ck(cudaEventRecord(eev[e].send_a[g], train), "record");
                 ck(cudaMemcpyAsync(to->slot(dir, mb0), standin->output(), msg_bytes,
                                    cudaMemcpyDefault, train), "send");
+                ck(cudaEventRecord(eev[e].send_b[g], train), "record");
                 launch_link_signal(to->flag(dir, mb0), seq, train);
               }
             } else {
@@ -1214,6 +1225,22 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
   rep->kills_oom = kills_oom;
   rep->kills_pause_timeout = kills_timeout;
   rep->kills_init_timeout = kills_init;
+  if (cfg.transport == 1) {  // stage-to-stage exchange: each message's copy-engine transfer
+    double t = 0;
+    std::int64_t n = 0;
+    for (int e = 0; e < epochs; ++e)
+      for (int g = 0; g < nops; ++g) {
+        const OpEvent& op = ops[static_cast<std::size_t>(g)];
+        const bool sends = (op.kind == OpKind::FP && cfg.stage < cfg.num_stages - 1) ||
+                           (op.kind == OpKind::BP && cfg.stage > 0);
+        if (!sends) continue;
+        t += elapsed_s(eev[e].send_a[g], eev[e].send_b[g]);
+        ++n;
+      }
+    rep->exchange_messages = n;
+    rep->exchange_us = n ? t / static_cast<double>(n) * 1e6 : 0.0;
+    rep->exchange_gbps = t > 0 ? static_cast<double>(msg_bytes) * static_cast<double>(n) / t * 1e-9 : 0.0;
+  }
   rep->op_growth = growth_n ? growth_sum / static_cast<double>(growth_n) : 0.0;
   rep->side_sms_mean = controlled && meas_idx ? sms_sum / static_cast<double>(meas_idx)
                                               : (cfg.side_sms > 0 ? cfg.side_sms : sm_count);
@@ -1306,6 +1333,24 @@ int fr_harness_link(fr_harness* h, void* prev_mailbox, void* next_mailbox) {
   const int s = h->cfg.stage, p = h->cfg.num_stages;
   if ((s > 0) != (prev_mailbox != nullptr) || (s < p - 1) != (next_mailbox != nullptr))
     return frcapi::fail(FR_ERR_VALIDATION, "a stage links exactly its existing neighbours", "mailbox");
+  // a neighbour on another GPU of this process: its mailbox is written by
+  // this GPU's copy engine and read by our flag waits -> peer access both
+  // ways over NVLink (IPC-opened mailboxes already have it:
+  // cudaIpcMemLazyEnablePeerAccess)
+  for (void* q : {prev_mailbox, next_mailbox}) {
+    if (!q) continue;
+    cudaPointerAttributes at{};
+    FR_CUDA_TRY_H(cudaPointerGetAttributes(&at, q));
+    if (at.type != cudaMemoryTypeDevice || at.device == h->device) continue;
+    int can = 0;
+    FR_CUDA_TRY_H(cudaDeviceCanAccessPeer(&can, h->device, at.device));
+    if (!can)
+      return frcapi::fail(FR_ERR_UNSUPPORTED, "no peer access from GPU " + std::to_string(h->device) + " to GPU " +
+                                                  std::to_string(at.device) + " (NVLink / P2P required)");
+    const cudaError_t e = cudaDeviceEnablePeerAccess(at.device, 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) FR_CUDA_TRY_H(e);
+    cudaGetLastError();  // clear the sticky "already enabled"
+  }
   h->prev_mbox.base = static_cast<char*>(prev_mailbox);
   h->next_mbox.base = static_cast<char*>(next_mailbox);
   h->linked = true;
@@ -1503,6 +1548,14 @@ int fr_harness_set_side_sms(fr_harness* h, int32_t sms) {
       const int rc = kv.second->vt.set_sm_budget(kv.second->user, sms);
       if (rc != FR_OK) return rc;
     }
+  return FR_OK;
+}
+
+int fr_harness_set_dt_budget(fr_harness* h, double budget) {
+  if (!h) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  if (!(budget >= 0.0 && budget < 1.0)) return frcapi::fail(FR_ERR_VALIDATION, "dt_budget in [0, 1)", "dt_budget");
+  h->cfg.dt_budget = budget;
+  h->ctrl_sms = 0;
   return FR_OK;
 }
 

@@ -98,7 +98,7 @@ def link_pipeline(h, group=None) -> List[int]:
 
 def linked_harvest(make_task, stage_shape: dict, num_micro_batches: int, epochs: int,
                    warmup: int, group=None, task_name: str = "side", step_group: int = 1,
-                   side_sms: int = 0) -> dict:
+                   side_sms: int = 0, dt_budget: float = 0.0) -> dict:
     """One stage of a real p-stage pipeline (p = world size) with a side task
     harvesting its bubbles: link, dry-run + bubble profiler, submit (Alg. 1
     on this stage's worker), warm-up, ΔT baseline, harvest.  Every rank must
@@ -106,7 +106,8 @@ def linked_harvest(make_task, stage_shape: dict, num_micro_batches: int, epochs:
     from . import gpu
     rank, p = dist.get_rank(group), dist.get_world_size(group)
     h = gpu.Harness(num_stages=p, num_micro_batches=num_micro_batches, stage=rank,
-                    transport="linked", step_group=step_group, side_sms=side_sms, **stage_shape)
+                    transport="linked", step_group=step_group, side_sms=side_sms,
+                    dt_budget=dt_budget, **stage_shape)
     opened = link_pipeline(h, group)
     dist.barrier(group)
     h.run(2, False)

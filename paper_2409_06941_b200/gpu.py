@@ -628,6 +628,11 @@ class Harness:
         """SM budget of the side tasks' kernels (0 = all); re-profile after a run"""
         check(glib().fr_harness_set_side_sms(self._h, int(sms)))
 
+    def set_dt_budget(self, budget: float):
+        """ΔT-budgeted harvesting for the next runs (0 = off): the worker sizes
+        the side tasks' SM budget so the stage's ops run <= budget slower"""
+        check(glib().fr_harness_set_dt_budget(self._h, float(budget)))
+
     def task_memory(self, task_id: str) -> dict:
         used, reserved = C.c_double(), C.c_double()
         check(glib().fr_harness_task_memory(self._h, task_id.encode(), C.byref(used), C.byref(reserved)))
