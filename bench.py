@@ -63,14 +63,16 @@ LAYERS_6B, HIDDEN_6B = 32, 4096                                       # nanoGPT-
 FRAMES = dict(sw=3840, sh=2160, dw=1920, dh=1080)
 BATCH = 64
 IMAGES_PER_STEP = int(os.environ.get("FR_IMAGES_PER_STEP", "16"))   # ~95 us steps (step size vs fill vs ΔT)
-# ΔT-budgeted harvesting: every stage's worker holds its ops'
-# slowdown under DT_BUDGET by sizing the side tasks' SM budget, starting from
-# IMG_SMS / SGD_SMS (scripts/harvest_sweep.py measured 16-24 SMs for the
-# image task at <= 1 %); PageRank is L2-resident and cheap in power and
-# starts from every SM.
-DT_BUDGET = float(os.environ.get("FR_DT_BUDGET", "0.007"))
-IMG_SMS = int(os.environ.get("FR_IMG_SMS", "24"))
-SGD_SMS = int(os.environ.get("FR_SGD_SMS", "32"))
+# Power-aware harvesting: the side tasks' SM budgets that
+# keep the pipeline ΔT under 1 % on B200 (scripts/harvest_sweep.py: image
+# 16 SMs -> ~0.4 %, 20 -> ~0.9 %, 24 -> 0.9-1.7 %; Graph-SGD ~20-30 SMs
+# under the live controller); PageRank is L2-resident, cheap in power, and
+# keeps every SM.  FR_DT_BUDGET > 0 hands the budget to the harness's live
+# ΔT controller instead (starting from these).
+DT_BUDGET = float(os.environ.get("FR_DT_BUDGET", "0"))   # > 0: the live controller instead of fixed budgets
+IMG_SMS = int(os.environ.get("FR_IMG_SMS", "16"))
+SGD_SMS = int(os.environ.get("FR_SGD_SMS", "20"))
+PAIRS = int(os.environ.get("FR_DT_PAIRS", "3"))           # (baseline, harvest) pairs for the headline ΔT
 STEP_GROUP = int(os.environ.get("FR_STEP_GROUP", "3"))   # steps between one pair of timing events
 E2E_IMAGES_PER_STEP = 1
 E2E_RING = int(os.environ.get("FR_E2E_RING", "128"))   # device staging slots: the copy engines run ahead of the steps
@@ -212,11 +214,24 @@ def cpu_info():
 
 
 # ---------------------------------------------------------------- harvest
-def harvest(h, name, task, K, W, sms=0, kinds=None, budget=0.0):
+def _sum_reports(rs):
+    """several run reports of the same length as one (sums; means of the rates)"""
+    out = dict(rs[0])
+    for k in ("makespan_s", "bubble_s", "used_s", "overrun_s", "work_units", "steps_launched", "steps_completed",
+              "pauses", "kills"):
+        out[k] = sum(r[k] for r in rs)
+    out["side_sms_mean"] = statistics.fmean(r["side_sms_mean"] for r in rs)
+    return out
+
+
+def harvest(h, name, task, K, W, sms=0, kinds=None, budget=0.0, pairs=1):
     """submit + warm-up + ΔT baseline + timed harvest on one stage replica;
     `sms`: the side task's SM budget (the ΔT controller's start when
     budget > 0); `kinds`: the stage's issue-order op kinds, for the per-stage
-    mean FP / BP op durations of both runs"""
+    mean FP / BP op durations of both runs; `pairs`: (baseline, harvest)
+    run pairs of K epochs each, averaged -- the run-to-run drift of the
+    GEMMs' power state is +-0.4 % (scripts/dt_noise_diag.py), so the pipeline
+    ΔT of one pair carries that noise and `pairs` shrinks it by sqrt(pairs)"""
     from paper_2409_06941_b200 import pipeline_dt as PD
     h.set_dt_budget(budget)
     h.set_side_sms(sms)
@@ -234,15 +249,24 @@ def harvest(h, name, task, K, W, sms=0, kinds=None, budget=0.0):
     else:
         print(f"bench: {name} ran no step in {3 * max(W, 1)} warm-up epochs "
               f"({h.task_status(name)}); keeping the standalone profile", file=sys.stderr)
-    base = h.run(K, False)
-    ops_base = PD.op_means(h.timeline(0), kinds) if kinds else None
-    r = h.run(K, True)
-    ops_with = PD.op_means(h.timeline(0), kinds) if kinds else None
-    durs = [b - a for a, b in h.timeline(2)]
+    bases, withs, ob, ow, durs = [], [], [], [], []
+    for _ in range(pairs):
+        bases.append(h.run(K, False))
+        if kinds:
+            ob.append(PD.op_means(h.timeline(0), kinds))
+        withs.append(h.run(K, True))
+        if kinds:
+            ow.append(PD.op_means(h.timeline(0), kinds))
+        durs += [b - a for a, b in h.timeline(2)]
+    base, r = _sum_reports(bases), _sum_reports(withs)
+    mean2 = (lambda xs: tuple(statistics.fmean(x[i] for x in xs) for i in range(2))) if kinds else None
+    ops_base = mean2(ob) if kinds else None
+    ops_with = mean2(ow) if kinds else None
     side, train = h.launches()
     h.stop_task(name)
-    return {"base": base, "with": r, "durs": durs, "side": side, "train_ops": train,
-            "ops_base": ops_base, "ops_with": ops_with, "sms": r["side_sms_mean"], "budget": budget,
+    return {"base": base, "with": r, "durs": durs, "side": side, "train_ops": train, "pairs": pairs,
+            "ops_base": ops_base, "ops_with": ops_with, "ops_base_runs": ob,
+            "sms": r["side_sms_mean"], "budget": budget,
             "units_per_step": task.units_per_step, "bytes_per_step": task.bytes_per_step,
             "h2d": task.h2d_per_step, "d2h": task.d2h_per_step, "est_step_s": tprof["est_per_step_duration"]}
 
@@ -294,7 +318,8 @@ def ours(args):
                 else:
                     task = gpu.SgdTask(**SGD)
                 runs[n].append(harvest(h, n, task, K, W, sms=sms_of.get(n, 0), kinds=kinds,
-                                       budget=0.0 if n == "image_full_gpu" else DT_BUDGET))
+                                       budget=0.0 if n == "image_full_gpu" else DT_BUDGET,
+                                       pairs=PAIRS if n == "image" else 1))
             h.close()
     torch.cuda.synchronize()
     if dist:
@@ -330,6 +355,13 @@ def ours(args):
     for n in names:
         local_res[n]["pipeline"] = pipe_dt([dict(r_, stage=i) for i, r_ in enumerate(runs[n])], STAGES,
                                            MICRO_BATCHES, K)
+    # the measurement's noise floor: pipeline ΔT between consecutive baseline
+    # runs (no side task in either) of the headline workload
+    npairs = min(len(r_["ops_base_runs"]) for r_ in runs["image"])
+    local_res["image"]["null_dT"] = [
+        PD.critical_path_dt(A, STAGES, MICRO_BATCHES, K, {i: r_["ops_base_runs"][j] for i, r_ in enumerate(runs["image"])},
+                            {i: r_["ops_base_runs"][j + 1] for i, r_ in enumerate(runs["image"])})["dT"]
+        for j in range(npairs - 1)]
     local_res["clocks"] = clk.summary()
     local_res["gap_kernels"] = sum(r["train_ops"] // (2 * MICRO_BATCHES) * (2 * MICRO_BATCHES + 1)
                                    for r in runs["image"])
@@ -540,6 +572,9 @@ def emit(args, results, ws, names, csr):
                        "(every stage replayed) through build_schedule (pipeline_dt.critical_path_dt)",
         "delta_t_stage_max": dT_stages("image"), "delta_t_stages": results[0]["image"]["stage_dT"],
         "dT_budget_met": dT("image") <= 0.01, "fill": fill("image"),
+        "delta_t_pairs": PAIRS,
+        "delta_t_noise": {"null_dT": results[0]["image"]["null_dT"],
+                          "how": "pipeline ΔT between consecutive baseline runs (no side task in either)"},
         "overrun_frac": sum(r["image"]["overrun"] for r in results) / max(1e-12, sum(r["image"]["used"] for r in results)),
         "bubble_s_per_step": max(r["image"]["bubble_s"] for r in results) / K,
         "px_per_step": sum(r["image"]["units"] for r in results) / K,

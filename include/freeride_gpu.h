@@ -121,6 +121,9 @@ int fr_pr_graph_csr(const fr_pr_graph* g, const int32_t** offsets, const int32_t
                     const int32_t** outdeg);
 int fr_pr_state_create(const fr_pr_graph* g, fr_pr_state** out);
 int fr_pr_state_destroy(fr_pr_state* st);
+/* iterations occupy at most `sms` SMs (0 = all): the persistent grid shrinks
+ * and each CTA walks several of the build's split-row chunk lists */
+int fr_pr_state_set_max_sms(fr_pr_state* st, int32_t sms);
 /* r = 1/V, c = r * inv_outdeg */
 int fr_pr_reset(fr_pr_state* st, void* stream);
 /* `iters` pull iterations: r' = (1-d)/V + d * A_in^T c ; c' = r' * inv_outdeg */

@@ -218,8 +218,10 @@ struct PrArgs {
   int32_t bstart[8];     // first row of bucket b (7 = split .. 1 = g 1), bstart[0] = tail
   int32_t istart[8];     // first item of bucket b = 6..1 (items of b-1 follow), istart[0] = total
   int32_t hot, V, do_tail;
+  int32_t nlists;        // chunk lists (LPT at build, one per CTA of a full grid); a smaller
+                         // grid (an SM budget) walks lists b, b + grid, ...
   double base, damp;
-  int32_t cta_chunk[kMaxCtas + 1];  // CTA b owns chunks [cta_chunk[b], cta_chunk[b+1])
+  int32_t cta_chunk[kMaxCtas + 1];  // list b owns chunks [cta_chunk[b], cta_chunk[b+1])
 };
 
 // N predicated gathers per lane, `stride` apart: hot sources from shared
@@ -358,8 +360,17 @@ __global__ void __maxnreg__(kPrThreads >= 1024 ? 56 : 40) pr_pull_kernel(PrArgs 
   __syncthreads();
   // split-row chunks, software-pipelined: the next chunk's descriptor and
   // first 8 column ids per lane load while this chunk gathers
-  const int c_end = a.cta_chunk[blockIdx.x + 1];
-  int c = a.cta_chunk[blockIdx.x] + warp;
+  for (int lb = blockIdx.x; lb < a.nlists; lb += gridDim.x) {
+  if (lb != static_cast<int>(blockIdx.x)) {  // the previous list's rows are all stored: reuse the slots
+    __syncthreads();
+    if (tid < kMaxSlots) {
+      sacc[tid] = 0.0;
+      scnt[tid] = 0;
+    }
+    __syncthreads();
+  }
+  const int c_end = a.cta_chunk[lb + 1];
+  int c = a.cta_chunk[lb] + warp;
   int4 ch = c < c_end ? __ldg(&a.chunks[c]) : make_int4(0, 0, 0, 0);
   int32_t cu[8];
   load_cols<8>(a, ch.y + lane, ch.z, 32, cu);
@@ -381,6 +392,7 @@ __global__ void __maxnreg__(kPrThreads >= 1024 ? 56 : 40) pr_pull_kernel(PrArgs 
       }
     }
     ch = chn;
+  }
   }
   const int nw = gridDim.x * kPrWarps, gw = blockIdx.x * kPrWarps + warp, n = a.istart[0];
   // software-pipelined: the next pair's offsets and output metadata load
@@ -485,6 +497,7 @@ struct fr_pr_state {
   int64_t iterations = 0;
   int tail_pending = 2;        // launches that still write the zero-in-degree tail
   float tail_damping = -1.0f;  // damping the tail was written with
+  int max_sms = 0;             // fr_pr_state_set_max_sms (0 = all)
 };
 
 namespace {
@@ -783,6 +796,13 @@ int fr_pr_state_create(const fr_pr_graph* g, fr_pr_state** out) {
   return FR_OK;
 }
 
+int fr_pr_state_set_max_sms(fr_pr_state* st, int32_t sms) {
+  if (!st) return frcapi::fail(FR_ERR_ARGUMENT, "null state");
+  if (sms < 0) return frcapi::fail(FR_ERR_VALIDATION, "sms must be >= 0", "sms");
+  st->max_sms = sms;
+  return FR_OK;
+}
+
 int fr_pr_state_destroy(fr_pr_state* st) {
   if (!st) return FR_OK;
   for (void* p : {static_cast<void*>(st->r), static_cast<void*>(st->r_orig), static_cast<void*>(st->c[0]),
@@ -843,7 +863,9 @@ int fr_pr_step(fr_pr_state* st, int32_t iters, float damping, void* stream) {
     a.c_out = st->c[st->cur ^ 1];
     a.do_tail = st->tail_pending > 0;
     cudaLaunchConfig_t lc{};
-    lc.gridDim = dim3(std::min(g->sms * cfg.ctas_per_sm, kMaxCtas));
+    const int full = std::min(g->sms * cfg.ctas_per_sm, kMaxCtas);
+    a.nlists = full;
+    lc.gridDim = dim3(st->max_sms > 0 ? std::min(full, std::min(st->max_sms, g->sms) * cfg.ctas_per_sm) : full);
     lc.blockDim = dim3(cfg.threads);
     lc.dynamicSmemBytes = smem;
     lc.stream = s;
@@ -893,6 +915,7 @@ struct PrTask {
   fr_pr_state st;
   bool on_gpu = false;
   cudaStream_t last = nullptr;
+  int32_t max_sms = 0;  // set_sm_budget
 };
 
 // The task keeps only what the step reads (not the original-order CSR), in
@@ -960,6 +983,7 @@ int pr_task_init(void* u, void* stream) {
   FR_CUDA_TRY(up(reinterpret_cast<void**>(&g.chunks), t->h_chunks, size_t(g.n_chunk) * sizeof(int4)));
   t->st = fr_pr_state{};
   t->st.g = &g;
+  t->st.max_sms = t->max_sms;
   for (float** p : {&t->st.r, &t->st.r_orig, &t->st.c[0], &t->st.c[1]})
     FR_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(p), std::max<size_t>(V, 4) * 4, s));
   t->on_gpu = true;
@@ -984,6 +1008,13 @@ int pr_task_stop(void* u) {
   t->g = fr_pr_graph{};
   t->st.r = nullptr;
   t->on_gpu = false;
+  return FR_OK;
+}
+
+int pr_task_sm_budget(void* u, int32_t sms) {
+  auto* t = static_cast<PrTask*>(u);
+  t->max_sms = sms;
+  t->st.max_sms = sms;
   return FR_OK;
 }
 
@@ -1037,6 +1068,7 @@ int fr_pagerank_task_create_from_graph(const fr_pagerank_task_config* c, const f
   vt->stop = pr_task_stop;
   vt->finished = pr_task_finished;
   vt->destroy = pr_task_destroy;
+  vt->set_sm_budget = pr_task_sm_budget;
   vt->work_units_per_step = static_cast<double>(t->shape.E) * c->iters_per_step;  // edges
   *user = t;
   return FR_OK;

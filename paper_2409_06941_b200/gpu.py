@@ -279,6 +279,10 @@ class PageRankState:
         check(glib().fr_pr_state_create(graph._h, C.byref(h)))
         self._h = h
 
+    def set_max_sms(self, sms: int):
+        """iterations occupy at most `sms` SMs (0 = all; fr_pr_state_set_max_sms)"""
+        check(glib().fr_pr_state_set_max_sms(self._h, int(sms)))
+
     def reset(self, stream=None):
         check(glib().fr_pr_reset(self._h, _stream(stream)))
 
