@@ -77,6 +77,7 @@ STEP_GROUP = int(os.environ.get("FR_STEP_GROUP", "3"))   # steps between one pai
 E2E_IMAGES_PER_STEP = 1
 E2E_RING = int(os.environ.get("FR_E2E_RING", "128"))   # device staging slots: the copy engines run ahead of the steps
 OUT_PX = FRAMES["dw"] * FRAMES["dh"]
+K5_WARP_INSTR_PER_PX = 1.434   # img_resize2x_wm_tma<2,0,3>, ncu instruction count (profiles/r2_k5_harvest_20sm_ncu.txt)
 PR = dict(scale=20, edge_factor=16, seed=1, iters_per_step=2)
 SGD = dict(V=3072441, E=117185083, k=16, edge_seed=2, init_seed=3,
            edges_per_step=int(os.environ.get("FR_SGD_EDGES_PER_STEP", str(1 << 22))))
@@ -508,8 +509,24 @@ def emit(args, results, ws, names, csr):
     traffic, timgs = load_ncu_traffic()
     if traffic and timgs and timgs != IMAGES_PER_STEP:
         traffic = traffic / timgs * IMAGES_PER_STEP
-    image_roof = roof("image", f"img_resize2x_wm_tma ({IMAGES_PER_STEP} frames/launch, in-pipeline)")
+    image_roof = roof("image", f"img_resize2x_wm_tma ({IMAGES_PER_STEP} frames/launch, in-pipeline, "
+                               f"{IMG_SMS}-SM budget)")
     image_roof["traffic"] = traffic
+    # At the power budget the kernel runs on IMG_SMS SMs and is issue-bound
+    # there (profiles/r2_k5_harvest_20sm_ncu.txt: 3.5 of 4 warp-instructions
+    # per cycle per active SM, 1.434 warp-instructions per output pixel):
+    # its roofline is those SMs' issue rate, not HBM.
+    sms = results[0]["image"]["sms"] or 148
+    px_per_byte = OUT_PX * IMAGES_PER_STEP / results[0]["image"]["bytes_per_step"]
+    clk = (results[0]["clocks"].get("sm_mhz") or 1800) * 1e6
+    issue_peak = sms * 4 * clk / K5_WARP_INSTR_PER_PX / px_per_byte / 1e9
+    image_roof["sm_issue_roofline"] = {
+        "sms": sms, "peak_GBps": issue_peak, "frac": image_roof["achieved"] / issue_peak,
+        "how": f"{sms} SMs x 4 warp-instr/cycle x {clk / 1e6:.0f} MHz (median SM clock of the run) / "
+               f"{K5_WARP_INSTR_PER_PX} warp-instr per px (ncu) / {px_per_byte:.4f} px per algorithmic byte"}
+    full = roof("image_full_gpu", f"img_resize2x_wm_tma ({IMAGES_PER_STEP} frames/launch, all SMs, in-pipeline)")
+    if full:
+        image_roof["full_gpu"] = {k: full[k] for k in ("achieved", "peak", "frac", "mean_launch_us", "unit")}
     cpu = cpu_image(args.cpu_seconds) if not args.no_cpu else None
     if cpu:
         cpu.update(cpu_info())
@@ -558,7 +575,7 @@ def emit(args, results, ws, names, csr):
     launches = sum(r[n]["launches"] for r in results for n in names) + sum(r["gap_kernels"] for r in results)
     line = {
         "metric": METRIC, "value": rate("image"), "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": W,
-        "ms_per_step": max(r["image"]["t_with"] for r in results) / K * 1e3, "higher_is_better": True,
+        "ms_per_step": max(r["image"]["t_with"] for r in results) / (K * PAIRS) * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic (seeded counter-based frames/watermark, RMAT graph, Orkut-shaped ratings)",
         "config": {"workload": WORKLOAD, "stages": STAGES, "micro_batches": MICRO_BATCHES, "stage_shape": SHAPE,
@@ -576,8 +593,8 @@ def emit(args, results, ws, names, csr):
         "delta_t_noise": {"null_dT": results[0]["image"]["null_dT"],
                           "how": "pipeline ΔT between consecutive baseline runs (no side task in either)"},
         "overrun_frac": sum(r["image"]["overrun"] for r in results) / max(1e-12, sum(r["image"]["used"] for r in results)),
-        "bubble_s_per_step": max(r["image"]["bubble_s"] for r in results) / K,
-        "px_per_step": sum(r["image"]["units"] for r in results) / K,
+        "bubble_s_per_step": max(r["image"]["bubble_s"] for r in results) / (K * PAIRS),
+        "px_per_step": sum(r["image"]["units"] for r in results) / (K * PAIRS),
         "roofline": image_roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": results[0]["clocks"],
         "gpu_launches": launches, "workloads": workloads, "stages": results[0]["stages"],
     }
