@@ -1,5 +1,6 @@
 """Device-timed microbenchmark of the K5 image step (CUDA events on the
-launching stream).  Usage: python scripts/img_microbench.py [n_per_step] [reps]"""
+launching stream).  Usage: python scripts/img_microbench.py [n_per_step] [reps]
+env FR_IMG_MAX_SMS: the plan's SM budget (fr_img_plan_set_max_sms)"""
 import json
 import os
 import sys
@@ -15,6 +16,7 @@ def main():
     reps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
     batch = 64
     plan = gpu.ImagePlan(3840, 2160, 1920, 1080)
+    plan.set_max_sms(int(os.environ.get("FR_IMG_MAX_SMS", "0")))
     src = gpu.img_generate(batch, 3840, 2160, seed=1)
     wm = gpu.img_generate_watermark(1920, 1080, seed=7)
     dst = torch.empty((batch, 1080, 1920, 3), dtype=torch.uint8, device="cuda")
