@@ -364,6 +364,7 @@ def ours(args):
                             {i: r_["ops_base_runs"][j + 1] for i, r_ in enumerate(runs["image"])})["dT"]
         for j in range(npairs - 1)]
     local_res["clocks"] = clk.summary()
+    local_res["l2_gbps"] = gpu.l2_read_gbps()   # PageRank's working set is L2-resident: its roofline
     local_res["gap_kernels"] = sum(r["train_ops"] // (2 * MICRO_BATCHES) * (2 * MICRO_BATCHES + 1)
                                    for r in runs["image"])
     local_res["stages"] = [{"stage": s, "fp_ms": p["fp_ticks"] / 1e6, "bp_ms": p["bp_ticks"] / 1e6,
@@ -538,12 +539,18 @@ def emit(args, results, ws, names, csr):
                **dT_fields("image_e2e"), "fill": fill("image_e2e"),
                "path": f"fr_image_task host_io=1: pinned host frames -> {E2E_RING}-slot device ring filled by the "
                        "copy engines ahead of the steps (also while the pipeline computes) -> K5 -> D2H per frame"}
+    pr_roof = roof("pagerank", "pr_pull_kernel (2 launches of 1 iteration per step, in-pipeline); "
+                               "working set L2-resident: latency-bound gathers, not HBM")
+    if pr_roof:
+        l2 = results[0]["l2_gbps"]
+        pr_roof["l2"] = {"achieved": pr_roof["achieved"], "peak": l2, "unit": "GB/s", "frac": pr_roof["achieved"] / l2,
+                         "peak_source": "measured in this run: coalesced 16 B ld.global.cg sweeps of a 48 MB "
+                                        "L2-resident buffer (fr_l2_read_probe)"}
     workloads = {
         "pagerank": {"config": "configs[0]: RMAT scale 20 (edge factor 16, seed 1), pull, d=0.85, 2 iterations/step",
                      "value": rate("pagerank"), "unit": "edges/bubble-s", **dT_fields("pagerank"),
                      "fill": fill("pagerank"),
-                     "roofline": roof("pagerank", "pr_pull_kernel (2 launches of 1 iteration per step, in-pipeline); "
-                                      "working set L2-resident: latency-bound gathers, not HBM"),
+                     "roofline": pr_roof,
                      "cpu_baseline": cpu_pagerank(args.cpu_seconds / 2, csr) if csr is not None else None},
         "sgd": {"config": f"configs[2]: Orkut shape V=3,072,441 E=117,185,083 k=16, {SGD['edges_per_step']} edges/step, "
                           "by-user layout (fr_sgd_group_by_user)",

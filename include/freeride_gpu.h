@@ -35,6 +35,10 @@ int fr_get_device(int32_t* device);
 int fr_memcpy(void* dst, const void* src, int64_t bytes);
 /* diagnostics: spin `cycles` SM clocks on one warp, write {cycles, ns} */
 int fr_clock_probe(uint64_t* out_cycles_ns, int64_t cycles, void* stream);
+/* L2 read bandwidth probe: `passes` coalesced 16 B ld.global.cg sweeps of
+ * `buf` (size it to fit in L2); time it with events on `stream`.  sink16:
+ * 16 device bytes the kernel may write (keeps the loads alive). */
+int fr_l2_read_probe(const void* buf, int64_t bytes, int32_t passes, void* sink16, void* stream);
 
 /* Device-side preemption for the imperative interface: the workload stops
  * taking new work items once *stop_word >= token.  The harness's gap kernel

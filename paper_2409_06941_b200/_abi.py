@@ -602,6 +602,7 @@ GPU_PROTOTYPES.update({
     "fr_img_plan_set_max_sms": (C.c_int, [vp, i32]),
     "fr_sgd_problem_set_max_sms": (C.c_int, [vp, i32]),
     "fr_pr_state_set_max_sms": (C.c_int, [vp, i32]),
+    "fr_l2_read_probe": (C.c_int, [vp, i64, i32, vp, vp]),
     "fr_harness_get_profile": (C.c_int, [vp, P(HarnessProfileC)]),
     "fr_harness_stage_bubbles": (C.c_int, [vp, P(BubbleC), i32, P(i32)]),
     "fr_harness_submit": (C.c_int, [vp, cp, P(SideTaskVTableC), vp, dbl, i32, P(TaskProfileC), P(i32)]),

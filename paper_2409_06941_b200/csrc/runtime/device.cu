@@ -17,9 +17,38 @@ __global__ void clock_probe_kernel(unsigned long long* out, long long cycles) {
   out[1] = t1 - t0;
 }
 
+// L2 bandwidth probe: every CTA streams its slice of an L2-resident buffer
+// `passes` times with 16 B ld.global.cg (L2, not L1), so after the first pass
+// the bytes come from L2 -- the bound of a kernel whose working set stays in
+// L2 (PageRank at RMAT-20).  The xor into `sink` keeps the loads alive.
+__global__ void l2_read_kernel(const int4* __restrict__ p, int64_t n, int passes, int4* sink) {
+  int4 acc = make_int4(0, 0, 0, 0);
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int q = 0; q < passes; ++q)
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
+      const int4 v = __ldcg(p + i);
+      acc.x ^= v.x;
+      acc.y ^= v.y;
+      acc.z ^= v.z;
+      acc.w ^= v.w;
+    }
+  if ((acc.x & acc.y & acc.z & acc.w) == 0x7fffffff) sink[0] = acc;  // practically never
+}
+
 }  // namespace
 
 extern "C" {
+
+int fr_l2_read_probe(const void* buf, int64_t bytes, int32_t passes, void* sink16, void* stream) {
+  if (!buf || !sink16 || bytes < 16 || passes < 1) return frcapi::fail(FR_ERR_ARGUMENT, "bad probe args");
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  l2_read_kernel<<<sms * 4, 512, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const int4*>(buf), bytes / 16, passes, static_cast<int4*>(sink16));
+  FR_CUDA_LAUNCHED("l2_read_probe");
+  return FR_OK;
+}
 
 int fr_clock_probe(uint64_t* out_cycles_ns, int64_t cycles, void* stream) {
   if (!out_cycles_ns || cycles < 1) return frcapi::fail(FR_ERR_ARGUMENT, "bad probe args");

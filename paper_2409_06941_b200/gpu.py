@@ -54,6 +54,25 @@ def _stream(stream) -> int:
     return int(stream)
 
 
+def l2_read_gbps(mbytes: int = 48, passes: int = 20) -> float:
+    """Measured L2 read bandwidth (GB/s): an L2-resident buffer swept
+    `passes` times (fr_l2_read_probe), CUDA events around the sweeps after a
+    warm-up pass that brings the buffer into L2."""
+    buf = torch.ones(mbytes << 18, dtype=torch.int32, device="cuda")
+    sink = torch.zeros(4, dtype=torch.int32, device="cuda")
+    s = torch.cuda.current_stream()
+    check(glib().fr_l2_read_probe(_ptr(buf), buf.numel() * 4, 1, _ptr(sink), s.cuda_stream))
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    best = 0.0
+    for _ in range(3):
+        a.record(s)
+        check(glib().fr_l2_read_probe(_ptr(buf), buf.numel() * 4, passes, _ptr(sink), s.cuda_stream))
+        b.record(s)
+        b.synchronize()
+        best = max(best, buf.numel() * 4 * passes / (a.elapsed_time(b) * 1e-3) / 1e9)
+    return best
+
+
 def low_priority_stream(device=None) -> torch.cuda.Stream:
     """The stream class side-task steps run in (lowest CUDA priority)."""
     lo, _hi = torch.cuda.Stream.priority_range()
