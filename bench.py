@@ -204,6 +204,16 @@ def cpu_sgd(seconds, edges=1 << 24):
                                      f"by-user layout), Hogwild OpenMP on {os.cpu_count()} host threads"}
 
 
+def bench_config(ws):
+    """the workload both arms report (the reference arm runs the same op on
+    the same frames and step size on the host cores)"""
+    return {"workload": WORKLOAD, "stages": STAGES, "micro_batches": MICRO_BATCHES, "stage_shape": SHAPE,
+            "frames": BATCH, "images_per_step": IMAGES_PER_STEP,
+            "step": "one 1F1B epoch of all 4 stages (replayed) with the side task",
+            "parallelism": f"replicas x{ws}", "step_group": STEP_GROUP, "dt_budget": DT_BUDGET,
+            "side_sms_start": IMG_SMS, "l2": "image inputs 1.6 GB per batch > 126 MB L2; no flush needed"}
+
+
 def cpu_info():
     model = None
     try:
@@ -591,12 +601,8 @@ def emit(args, results, ws, names, csr):
         "ms_per_step": max(r["image"]["t_with"] for r in results) / (K * PAIRS) * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic (seeded counter-based frames/watermark, RMAT graph, Orkut-shaped ratings)",
-        "config": {"workload": WORKLOAD, "stages": STAGES, "micro_batches": MICRO_BATCHES, "stage_shape": SHAPE,
-                   "frames": BATCH, "images_per_step": IMAGES_PER_STEP,
-                   "step": "one 1F1B epoch of all 4 stages (replayed) with the side task",
-                   "parallelism": f"replicas x{ws}", "step_group": STEP_GROUP, "dt_budget": DT_BUDGET,
-                   "side_sms_start": IMG_SMS, "side_sms_mean": results[0]["image"]["sms"],
-                   "l2": "image inputs 1.6 GB per batch > 126 MB L2; no flush needed"},
+        "config": bench_config(ws),
+        "side_sms_mean": results[0]["image"]["sms"],
         "delta_t": dT("image"),
         "delta_t_def": "pipeline makespan growth: per-stage mean FP/BP op durations with vs without the side task "
                        "(every stage replayed) through build_schedule (pipeline_dt.critical_path_dt)",
@@ -681,7 +687,7 @@ def reference(args):
             "ms_per_step": secs / K * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u8", "data": "synthetic (seeded counter-based frames/watermark)",
             "impl": "reference",
-            "config": {"workload": WORKLOAD, "frames": BATCH, "images_per_step": IMAGES_PER_STEP},
+            "config": bench_config(ws),
             "cpu_baseline": {"value": v, "unit": "px/s", "cores": vals[0]["cores"], "kind": "port",
                              "sample": vals[0]["sample"], **cpu_info()},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
