@@ -25,6 +25,7 @@ MIRRORS = {
     "ImageTaskConfigC": "fr_image_task_config", "PageRankTaskConfigC": "fr_pagerank_task_config",
     "SgdTaskConfigC": "fr_sgd_task_config", "HarnessConfigC": "fr_harness_config",
     "HarnessProfileC": "fr_harness_profile", "RunReportC": "fr_run_report",
+    "GateRecordC": "fr_gate_record", "SignalRecordC": "fr_signal_record",
 }
 
 
