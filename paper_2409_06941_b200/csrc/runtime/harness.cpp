@@ -226,6 +226,11 @@ struct fr_harness {
   std::vector<SignalRec> sig_log;
   std::vector<GateRec> gate_log;
   std::vector<TransitionRecord> tr_log;
+  // per tr_log entry: step records completed when it was applied (a pause or
+  // stop lands only after them; the export lifts its host-clock stamp to
+  // their device end, see fr_harness_run_trace)
+  std::vector<std::size_t> tr_recs_done;
+  std::vector<std::size_t> rec_slices;  // per step record of the last run: first slice in step_se
   std::vector<KillRecord> kill_log;
   std::map<std::string, SideTaskState> run_start_state;
   std::vector<std::pair<std::string, std::pair<double, double>>> init_log;  // event seconds
@@ -496,6 +501,7 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
   sig_log.clear();
   gate_log.clear();
   tr_log.clear();
+  tr_recs_done.clear();
   kill_log.clear();
   init_log.clear();
   run_start_state.clear();
@@ -686,12 +692,14 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
   // task, so the trace's time order is the order they were applied in (a
   // BubbleStarted held while a pause drained is applied after that pause).
   std::map<std::string, std::int64_t> last_stamp;
+  std::size_t recs_done = 0;  // step records [0, recs_done) have completed
   const auto trans = [&](Task& t, TransitionKind k, std::int64_t now) {
     auto it = last_stamp.find(t.id);
     if (it != last_stamp.end()) now = std::max(now, it->second);
     last_stamp[t.id] = now;
     apply_transition(t.rt, k, now);
     tr_log.push_back(TransitionRecord{now, t.id, k, cfg.stage});
+    tr_recs_done.push_back(recs_done);
   };
   const auto log_signal = [&](std::int64_t t, int kind, std::uint32_t id, std::int64_t dur, bool deferred,
                               const std::vector<ManagerAction>& acts) {
@@ -798,6 +806,7 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
         const double per = elapsed_s(steps[inflight.front()].a, steps[inflight.front()].b) / n;
         if (prof_est > 0 && per > 0) st->est_scale = 0.7 * st->est_scale + 0.3 * (per / prof_est);
       }
+      recs_done = std::max(recs_done, inflight.front() + 1);
       inflight.pop_front();
       inflight_steps -= n;
       completed += n;
@@ -1141,7 +1150,9 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
     prev_end = eev[e].end;
   }
   step_task.clear();
+  rec_slices.clear();
   for (const StepRec& r : steps) {  // a group of n back-to-back steps: n equal slices
+    rec_slices.push_back(step_se.size() / 2);
     const double a = elapsed_s(run_start, r.a), b = elapsed_s(run_start, r.b);
     const int n = std::max(1, r.n);
     for (int i = 0; i < n; ++i) {
@@ -1674,8 +1685,26 @@ int fr_harness_run_trace(const fr_harness* h, fr_run_trace** out) {
       if (st0 == SideTaskState::Stopped) pre.push_back(TransitionKind::StopSideTask);
       for (TransitionKind k : pre) r.transitions.push_back(TransitionRecord{0, t.id, k, s});
     }
-    for (const TransitionRecord& x : h->tr_log)
-      r.transitions.push_back(TransitionRecord{rel(x.t), x.task, x.kind, x.worker});
+    // A pause (or stop) is applied once the task's in-flight steps have
+    // drained; its stamp is the host clock mapped to the device's, which
+    // trails the device by the polling latency (~10 us).  It cannot have
+    // landed before those steps ended, so it is lifted to their device end,
+    // and the task's later stamps keep their order.
+    std::map<std::string, Tick> floor_of;
+    for (std::size_t i = 0; i < h->tr_log.size(); ++i) {
+      const TransitionRecord& x = h->tr_log[i];
+      Tick t = rel(x.t);
+      const std::size_t done = i < h->tr_recs_done.size() ? h->tr_recs_done[i] : 0;
+      if ((x.kind == TransitionKind::PauseSideTask || x.kind == TransitionKind::StopSideTask) && done > 0 &&
+          done <= h->rec_slices.size()) {
+        const std::size_t end_slice = done < h->rec_slices.size() ? h->rec_slices[done] : h->step_se.size() / 2;
+        if (end_slice > 0) t = std::max(t, tick_of(h->step_se[2 * end_slice - 1]));
+      }
+      Tick& fl = floor_of[x.task];
+      t = std::max(t, fl);
+      fl = t;
+      r.transitions.push_back(TransitionRecord{t, x.task, x.kind, x.worker});
+    }
     std::stable_sort(r.transitions.begin(), r.transitions.end(),
                      [](const TransitionRecord& a, const TransitionRecord& b) { return a.t < b.t; });
     const std::size_t nops = h->ops.size();
