@@ -27,6 +27,8 @@
 #include <string>
 #include <vector>
 
+#include <cuda/atomic>
+
 #include "freeride_gpu.h"
 #include "kernels/common.cuh"
 
@@ -121,6 +123,116 @@ __device__ __forceinline__ void img_group8(const uint8_t* __restrict__ ra, const
   po[2] = make_uint2(__byte_perm(rgb[5], rgb[6], 0x5421), __byte_perm(rgb[6], rgb[7], 0x6542));
     }
 
+// ---- Math variant 1 (dot-product form; the default)
+// The 2x2 sums come straight out of IDP.4A (dp4a): one dp4a sums the two
+// bytes of a channel that lie in one source word, with weight 64, so
+// 64 * (a + b + c + d + 2) < 2^16 carries floor((sum + 2) / 4) in its byte 1
+// and zeros in bytes 2-3 -- the shift and the lane packing become one PRMT.
+// A pixel pair (12 source bytes per row, words w0 w1 w2) gives channels
+//   p0: R = w0.b0 + w0.b3, G = w0.b1 + w1.b0, B = w0.b2 + w1.b1
+//   p1: R = w1.b2 + w2.b1, G = w1.b3 + w2.b2, B = w2.b0 + w2.b3
+// (the cross-word pairs gathered into one word by a PRMT per row first),
+// blended in three 16-bit-lane words X = [R0, B0] (alpha of p0),
+// Z = [B1, G1] (p1) and Y = [G0, R1] (one IMAD per lane).  Prepared
+// watermark: 5 words per pair {wX, wY, wZ, 255 - a0, 255 - a1}, wc = w*a + 127
+// in the matching lane, group-transposed [y][5][groups] (uint4) like variant 0.
+constexpr int kWmVecs1 = 5;  // uint4 per 8-pixel group
+
+__global__ void img_prepare_wm1_kernel(const uint8_t* __restrict__ wm, uint4* __restrict__ out,
+                                       int dw, int dh) {
+  const int groups = dw >> 3;
+  const int64_t total = static_cast<int64_t>(dh) * groups;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int g = static_cast<int>(i % groups);
+    const int64_t y = i / groups;
+    uint32_t v[4 * kWmVecs1];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint8_t* p0 = wm + (y * dw + 8 * g + 2 * q) * 4;
+      const uint8_t* p1 = p0 + 4;
+      const uint32_t a0 = p0[3], a1 = p1[3];
+      const auto wc = [](uint32_t w, uint32_t a) { return w * a + 127u; };
+      v[5 * q + 0] = wc(p0[0], a0) | (wc(p0[2], a0) << 16);  // R0 | B0
+      v[5 * q + 1] = wc(p0[1], a0) | (wc(p1[0], a1) << 16);  // G0 | R1
+      v[5 * q + 2] = wc(p1[2], a1) | (wc(p1[1], a1) << 16);  // B1 | G1
+      v[5 * q + 3] = 255u - a0;
+      v[5 * q + 4] = 255u - a1;
+    }
+#pragma unroll
+    for (int k = 0; k < kWmVecs1; ++k)
+      out[(y * kWmVecs1 + k) * groups + g] = make_uint4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+  }
+}
+
+__device__ __forceinline__ uint32_t dp4(uint32_t a, uint32_t w, uint32_t c) {
+  return static_cast<uint32_t>(__dp4a(a, w, c));
+}
+
+// floor(t / 255) per 16-bit lane, t < 65408: (t + 1 + (t >> 8)) >> 8, the
+// quotient left in bytes 1 and 3
+__device__ __forceinline__ uint32_t div255_lanes(uint32_t t) {
+  return t + __byte_perm(t, 0u, 0x4341) + 0x00010001u;
+}
+
+template <bool GLOBAL_OUT = false>
+__device__ __forceinline__ void img_group8_dp(const uint8_t* __restrict__ ra, const uint8_t* __restrict__ rb,
+                                          const uint32_t (&wv)[4 * kWmVecs1], uint8_t* po8, int g) {
+  uint32_t va[12], vb[12];
+  const uint4* pa = reinterpret_cast<const uint4*>(ra + 48 * g);
+  const uint4* pb = reinterpret_cast<const uint4*>(rb + 48 * g);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const uint4 x = pa[i], z = pb[i];
+    va[4 * i + 0] = x.x; va[4 * i + 1] = x.y; va[4 * i + 2] = x.z; va[4 * i + 3] = x.w;
+    vb[4 * i + 0] = z.x; vb[4 * i + 1] = z.y; vb[4 * i + 2] = z.z; vb[4 * i + 3] = z.w;
+  }
+  constexpr uint32_t kW03 = 0x40000040u, kW02 = 0x00400040u, kW13 = 0x40004000u, kBias = 128u;
+  uint32_t uX[4], uY[4], uZ[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t a0 = va[3 * q], a1 = va[3 * q + 1], a2 = va[3 * q + 2];
+    const uint32_t b0 = vb[3 * q], b1 = vb[3 * q + 1], b2 = vb[3 * q + 2];
+    const uint32_t ga = __byte_perm(a0, a1, 0x5421), gb = __byte_perm(b0, b1, 0x5421);  // G0 B0 G1 B1
+    const uint32_t ha = __byte_perm(a1, a2, 0x6532), hb = __byte_perm(b1, b2, 0x6532);  // R2 G2 R3 G3
+    const uint32_t sR0 = dp4(a0, kW03, dp4(b0, kW03, kBias));
+    const uint32_t sG0 = dp4(ga, kW02, dp4(gb, kW02, kBias));
+    const uint32_t sB0 = dp4(ga, kW13, dp4(gb, kW13, kBias));
+    const uint32_t sR1 = dp4(ha, kW02, dp4(hb, kW02, kBias));
+    const uint32_t sG1 = dp4(ha, kW13, dp4(hb, kW13, kBias));
+    const uint32_t sB1 = dp4(a2, kW03, dp4(b2, kW03, kBias));
+    const uint32_t wX = wv[5 * q], wY = wv[5 * q + 1], wZ = wv[5 * q + 2];
+    const uint32_t na0 = wv[5 * q + 3], na1 = wv[5 * q + 4];
+    const uint32_t X = __byte_perm(sR0, sB0, 0x6521);      // [R0, B0] lanes
+    const uint32_t Z = __byte_perm(sB1, sG1, 0x6521);      // [B1, G1]
+    const uint32_t Ylo = __byte_perm(sG0, 0u, 0x4441);     // [G0, 0]
+    const uint32_t Yhi = __byte_perm(sR1, 0u, 0x4144);     // [0, R1]
+    uX[q] = div255_lanes(X * na0 + wX);
+    uZ[q] = div255_lanes(Z * na1 + wZ);
+    uY[q] = div255_lanes(Yhi * na1 + (Ylo * na0 + wY));
+  }
+  uint32_t o[6];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int q = 2 * h;
+    const uint32_t A0 = __byte_perm(uX[q], uY[q], 0x7351);          // R0 G0 B0 R1
+    const uint32_t A1 = __byte_perm(uX[q + 1], uY[q + 1], 0x7351);  // R2 G2 B2 R3
+    o[3 * h + 0] = A0;
+    o[3 * h + 1] = __byte_perm(uZ[q], A1, 0x5413);      // G1 B1 R2 G2
+    o[3 * h + 2] = __byte_perm(A1, uZ[q + 1], 0x5732);  // B2 R3 G3 B3
+  }
+  uint2* po = reinterpret_cast<uint2*>(po8);
+  if constexpr (GLOBAL_OUT) {  // straight to HBM, evict-first (st.global.cs)
+    __stcs(po + 0, make_uint2(o[0], o[1]));
+    __stcs(po + 1, make_uint2(o[2], o[3]));
+    __stcs(po + 2, make_uint2(o[4], o[5]));
+  } else {
+    po[0] = make_uint2(o[0], o[1]);
+    po[1] = make_uint2(o[2], o[3]);
+    po[2] = make_uint2(o[4], o[5]);
+  }
+}
+
 // Rows are handed out dynamically (one atomicAdd per row by the elected
 // thread) rather than statically strided: in a pipeline bubble some SMs may
 // be unavailable (the stage's dependency-wait kernel, an NCCL receive, the
@@ -136,7 +248,7 @@ __device__ __forceinline__ void img_group8(const uint8_t* __restrict__ ra, const
 // loop over the batch several times; the last CTA out advances base by the
 // rows taken, so the next launch resumes at the first untaken row, and adds
 // them to counters[2..3] (every taken row is completed before exit).
-template <int S, bool PREEMPT, int CPS>
+template <int S, bool PREEMPT, int CPS, int MATH>
 __global__ void __launch_bounds__(kImgThreads, CPS)
     img_resize2x_wm_tma(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
                         const uint4* __restrict__ wmp, int dw, int dh, uint32_t rows,
@@ -204,15 +316,19 @@ __global__ void __launch_bounds__(kImgThreads, CPS)
     uint8_t* orow = st + a_src;
     for (int g = tid; g < groups; g += kImgThreads) {
       // watermark first (L2): its latency overlaps the wait for the rows
-      uint32_t wv[16];
-      const uint4* pw = wmp + static_cast<size_t>(y) * 4 * groups + g;
+      constexpr int kVecs = MATH == 1 ? kWmVecs1 : 4;
+      uint32_t wv[4 * kVecs];
+      const uint4* pw = wmp + (y * static_cast<uint32_t>(kVecs * groups) + static_cast<uint32_t>(g));
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < kVecs; ++j) {
         const uint4 x = __ldg(pw + j * groups);
         wv[4 * j + 0] = x.x; wv[4 * j + 1] = x.y; wv[4 * j + 2] = x.z; wv[4 * j + 3] = x.w;
       }
       frk::mbar_wait(&full[s], (k / S) & 1u);
-      img_group8(ra, rb, wv, orow + 24 * g, g);
+      if constexpr (MATH == 1)
+        img_group8_dp(ra, rb, wv, orow + 24 * g, g);
+      else
+        img_group8(ra, rb, wv, orow + 24 * g, g);
     }
     frk::fence_proxy_async_smem();
     // Before anyone writes the next stage's output buffer, the bulk store
@@ -237,6 +353,134 @@ __global__ void __launch_bounds__(kImgThreads, CPS)
     __threadfence();
     if (atomicAdd(&counters[1], 1u) == gridDim.x - 1) {  // last CTA out re-arms
       if (PREEMPT) {
+        const uint32_t taken = min(atomicAdd(&counters[4], 0u), budget);
+        counters[0] = static_cast<uint32_t>((static_cast<uint64_t>(base) + taken) % rows);
+        counters[4] = 0;
+      } else {
+        counters[0] = 0;
+      }
+      counters[1] = 0;
+    }
+  }
+}
+
+// Warp-specialised variant (the default exact-2x kernel).  The per-row CTA
+// barrier of img_resize2x_wm_tma held every warp to the slowest one each row
+// (36 % of the stall samples at a 16-SM budget once the dp4a math had cut
+// the issue count).  Here no consumer warp waits for another:
+//  * one producer warp (one lane) claims rows, one ahead (the claim's
+//    global-atomic round trip overlaps the previous copy), and streams each
+//    row's two source rows into one of S stages with a TMA bulk copy;
+//  * it publishes the row id on meta[s] before the copy lands, so consumers
+//    issue their watermark loads (L2) while the copy is in flight, then wait
+//    on full[s] for the data;
+//  * 8 consumer warps compute and store straight from registers to HBM
+//    (st.global.cs, 24 B per thread, 768 B per warp), so the whole smem
+//    budget is input (3 CTAs x 3 stages x 23 KB per SM); each warp releases
+//    the stage on empty[s] (one arrival per warp) and moves on.
+template <int S, bool PREEMPT, int CPS>
+__global__ void __launch_bounds__(kImgThreads + 32, CPS)
+    img_resize2x_wm_ws(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
+                       const uint4* __restrict__ wmp, int dw, int dh, uint32_t rows,
+                       uint32_t* __restrict__ counters, const uint32_t* __restrict__ stop_word,
+                       uint32_t token, uint32_t budget) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint32_t row_of[S];
+  constexpr int kWarps = kImgThreads / 32;  // consumer warps; warp kWarps is the producer
+  const uint32_t src_row = 6u * static_cast<uint32_t>(dw);  // one source row, RGB
+  const uint32_t out_row = 3u * static_cast<uint32_t>(dw);
+  const uint32_t stage_bytes = (2u * src_row + 127u) & ~127u;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
+  uint64_t* meta = full + S;
+  uint64_t* empty = meta + S;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int groups = dw >> 3;
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      frk::mbar_init(&full[s], 1);
+      frk::mbar_init(&meta[s], 1);
+      frk::mbar_init(&empty[s], kWarps);
+    }
+    frk::fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == kWarps) {  // ---- producer
+    if (lane == 0) {
+      const uint64_t pol_stream = frk::policy_evict_first();
+      const uint32_t base = PREEMPT ? counters[0] : 0u;  // advanced only after this launch
+      auto take = [&]() -> uint32_t {
+        if (!PREEMPT) return atomicAdd(&counters[0], 1u);
+        if (frk::ld_relaxed_gpu(stop_word) >= token) return rows;  // paused: no new row
+        const uint32_t t = atomicAdd(&counters[4], 1u);
+        if (t >= budget) return rows;
+        return (base + t) % rows;  // base < rows, t < budget < 2^31
+      };
+      uint32_t next = take(), done = 0;
+      for (uint32_t k = 0;; ++k) {
+        const int s = static_cast<int>(k % S);
+        if (k >= S) frk::mbar_wait(&empty[s], ((k / S) - 1) & 1u);
+        const uint32_t r = next;
+        row_of[s] = r;
+        frk::mbar_arrive(&meta[s]);
+        if (r >= rows) {  // no more rows: consumers leave at this stage
+          if (!PREEMPT) asm volatile("griddepcontrol.launch_dependents;");
+          break;
+        }
+        next = take();  // consumed next iteration: the round trip overlaps this copy
+        ++done;
+        const uint32_t img = r / static_cast<uint32_t>(dh);
+        const uint32_t y = r - img * static_cast<uint32_t>(dh);
+        frk::mbar_arrive_expect_tx(&full[s], 2u * src_row);
+        frk::bulk_g2s(smem + s * stage_bytes,
+                      src + (static_cast<uint64_t>(img) * 2 * dh + 2 * y) * src_row, 2u * src_row,
+                      &full[s], pol_stream);
+      }
+      if (PREEMPT) {
+        // every claimed row was loaded (a claim after the stop returns no row)
+        atomicAdd(reinterpret_cast<unsigned long long*>(counters + 2), done);
+      }
+    }
+  } else {  // ---- consumers
+    for (uint32_t k = 0;; ++k) {
+      const int s = static_cast<int>(k % S);
+      const uint32_t ph = (k / S) & 1u;
+      frk::mbar_wait(&meta[s], ph);
+      const uint32_t row = row_of[s];
+      if (row >= rows) break;
+      const uint32_t img = row / static_cast<uint32_t>(dh);
+      const uint32_t y = row - img * static_cast<uint32_t>(dh);
+      const uint8_t* ra = smem + s * stage_bytes;
+      const uint8_t* rb = ra + src_row;
+      uint8_t* orow = dst + static_cast<uint64_t>(row) * out_row;
+      bool waited = false;
+      for (int g = tid; g < groups; g += kImgThreads) {
+        // watermark first (L2): its latency overlaps the copy still in flight
+        uint32_t wv[4 * kWmVecs1];
+        const uint4* pw = wmp + (y * static_cast<uint32_t>(kWmVecs1 * groups) + static_cast<uint32_t>(g));
+#pragma unroll
+        for (int j = 0; j < kWmVecs1; ++j) {
+          const uint4 x = __ldg(pw + j * groups);
+          wv[4 * j + 0] = x.x; wv[4 * j + 1] = x.y; wv[4 * j + 2] = x.z; wv[4 * j + 3] = x.w;
+        }
+        if (!waited) {
+          frk::mbar_wait(&full[s], ph);
+          waited = true;
+        }
+        img_group8_dp<true>(ra, rb, wv, orow + 24 * g, g);
+      }
+      if (!waited) frk::mbar_wait(&full[s], ph);  // lanes with no group still release in order
+      __syncwarp();
+      if (lane == 0) frk::mbar_arrive(&empty[s]);
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(&counters[1], 1u) == gridDim.x - 1) {  // last CTA out re-arms
+      if (PREEMPT) {
+        const uint32_t base = counters[0];
         const uint32_t taken = min(atomicAdd(&counters[4], 0u), budget);
         counters[0] = static_cast<uint32_t>((static_cast<uint64_t>(base) + taken) % rows);
         counters[4] = 0;
@@ -342,10 +586,24 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 
 constexpr uint32_t kImgCtrSlots = 64;
 
+namespace {
+using ImgKernel = void (*)(const uint8_t*, uint8_t*, const uint4*, int, int, uint32_t, uint32_t*,
+                           const uint32_t*, uint32_t, uint32_t);
+template <bool PREEMPT>
+ImgKernel img_kernel(int stages, int math, bool ws) {
+  if (ws) return img_resize2x_wm_ws<3, PREEMPT, 3>;
+  if (math == 1)
+    return stages == 2 ? img_resize2x_wm_tma<2, PREEMPT, 3, 1> : img_resize2x_wm_tma<3, PREEMPT, 2, 1>;
+  return stages == 2 ? img_resize2x_wm_tma<2, PREEMPT, 3, 0> : img_resize2x_wm_tma<3, PREEMPT, 2, 0>;
+}
+}  // namespace
+
 struct fr_img_plan {
   int sw = 0, sh = 0, dw = 0, dh = 0;
   int stages = kImgStages, ctas_per_sm = kImgCtasPerSm;  // TMA path pipeline shape
   int path = FR_IMG_PATH_GENERAL;
+  int math = 1;  // exact-2x math variant: 1 = dp4a sums (default), 0 = 16-bit lane sums (FR_IMG_MATH=0)
+  bool ws = true;  // warp-decoupled kernel (default); FR_IMG_CFG=bar|3x2: the per-row-barrier kernel
   int32_t* d_tab = nullptr;
   void* d_wm = nullptr;  // plan-owned prepared watermark for fr_img_resize_watermark
   uint32_t* d_ctr = nullptr;  // dynamic row scheduler {next row, CTAs done} x kImgCtrSlots; one stream at a time
@@ -363,7 +621,8 @@ struct fr_img_plan {
   int max_sms = 0;  // fr_img_plan_set_max_sms: grid sized for this many SMs (0 = all)
   int64_t grid_sms() const { return max_sms > 0 ? std::min(max_sms, sms) : sms; }
   size_t prepared_bytes() const {
-    return path == FR_IMG_PATH_TMA_2X ? static_cast<size_t>(dw) * dh * 8 : static_cast<size_t>(dw) * dh * 4;
+    if (path != FR_IMG_PATH_TMA_2X) return static_cast<size_t>(dw) * dh * 4;
+    return static_cast<size_t>(dw) * dh * (math == 1 ? 2 * kWmVecs1 : 8);
   }
 };
 
@@ -388,17 +647,20 @@ int fr_img_plan_create(int32_t sw, int32_t sh, int32_t dw, int32_t dh, fr_img_pl
   const bool two_x = sw == 2 * dw && sh == 2 * dh && dw % 16 == 0;
   if (two_x) {
     auto al = [](int x) { return (x + 127) & ~127; };
-    if (const char* e = std::getenv("FR_IMG_CFG")) {  // tuning hook: "<stages>x<ctas per SM>"
+    if (const char* e = std::getenv("FR_IMG_CFG")) {  // tuning hook: "bar" | "3x2" (barrier kernel)
       if (std::string(e) == "3x2") plan->stages = 3, plan->ctas_per_sm = 2;
+      if (std::string(e) == "bar" || std::string(e) == "3x2") plan->ws = false;
     }
-    plan->smem = plan->stages * (al(12 * dw) + al(3 * dw)) + plan->stages * 8;
+    if (const char* m = std::getenv("FR_IMG_MATH")) plan->math = std::atoi(m) == 0 ? 0 : 1;
+    if (plan->math == 0) plan->ws = false;  // the warp-decoupled kernel has the dp4a math only
+    if (plan->ws) plan->stages = 3, plan->ctas_per_sm = 3;
+    plan->smem = plan->ws ? plan->stages * al(12 * dw) + plan->stages * 24
+                          : plan->stages * (al(12 * dw) + al(3 * dw)) + plan->stages * 8;
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     if (plan->smem <= optin) {
-      for (const void* fn : {reinterpret_cast<const void*>(img_resize2x_wm_tma<3, false, 2>),
-                             reinterpret_cast<const void*>(img_resize2x_wm_tma<3, true, 2>),
-                             reinterpret_cast<const void*>(img_resize2x_wm_tma<2, false, 3>),
-                             reinterpret_cast<const void*>(img_resize2x_wm_tma<2, true, 3>)}) {
+      for (const void* fn : {reinterpret_cast<const void*>(img_kernel<false>(plan->stages, plan->math, plan->ws)),
+                             reinterpret_cast<const void*>(img_kernel<true>(plan->stages, plan->math, plan->ws))}) {
         if (e == cudaSuccess)
           e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, plan->smem);
         if (e == cudaSuccess)
@@ -476,9 +738,13 @@ int fr_img_prepare_watermark(const fr_img_plan* plan, const uint8_t* wm_rgba, vo
   plan->chained = false;
   if (plan->path == FR_IMG_PATH_TMA_2X) {
     if (!aligned16(prepared)) return frcapi::fail(FR_ERR_UNSUPPORTED, "prepared watermark must be 16-byte aligned");
-    const int64_t total = static_cast<int64_t>(plan->dh) * (plan->dw >> 3) * 4;
-    img_prepare_wm_kernel<<<grid_for(total, 256, 8), 256, 0, s>>>(
-        wm_rgba, static_cast<uint4*>(prepared), plan->dw, plan->dh);
+    const int64_t groups = static_cast<int64_t>(plan->dh) * (plan->dw >> 3);
+    if (plan->math == 1)
+      img_prepare_wm1_kernel<<<grid_for(groups, 256, 8), 256, 0, s>>>(
+          wm_rgba, static_cast<uint4*>(prepared), plan->dw, plan->dh);
+    else
+      img_prepare_wm_kernel<<<grid_for(groups * 4, 256, 8), 256, 0, s>>>(
+          wm_rgba, static_cast<uint4*>(prepared), plan->dw, plan->dh);
   } else {
     FR_CUDA_TRY(cudaMemcpyAsync(prepared, wm_rgba, plan->prepared_bytes(), cudaMemcpyDeviceToDevice, s));
   }
@@ -498,7 +764,7 @@ int fr_img_resize_watermark_prepared(const fr_img_plan* plan, const uint8_t* src
     const int64_t rows = static_cast<int64_t>(n) * plan->dh;
     if (rows >= (int64_t{1} << 31)) return frcapi::fail(FR_ERR_UNSUPPORTED, "too many rows in one step");
     const int grid = static_cast<int>(std::min<int64_t>(rows, plan->grid_sms() * plan->ctas_per_sm));
-    auto k = plan->stages == 2 ? img_resize2x_wm_tma<2, false, 3> : img_resize2x_wm_tma<3, false, 2>;
+    const ImgKernel k = img_kernel<false>(plan->stages, plan->math, plan->ws);
     // Consecutive steps overlap their tail and head (programmatic dependent
     // launch: a launch's CTAs start once every CTA of the previous one took
     // its last row).  Steps touch different frames; the row counters rotate
@@ -513,7 +779,7 @@ int fr_img_resize_watermark_prepared(const fr_img_plan* plan, const uint8_t* src
     plan->chain_stream = s;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kImgThreads);
+    cfg.blockDim = dim3(plan->ws ? kImgThreads + 32 : kImgThreads);
     cfg.dynamicSmemBytes = plan->smem;
     cfg.stream = s;
     cudaLaunchAttribute at[1];
@@ -554,9 +820,9 @@ int fr_img_resize_watermark_preemptible(const fr_img_plan* plan, const uint8_t* 
   // no preempt: a stop word that never fires (counters[5] stays 0 < token)
   const uint32_t* word = preempt && preempt->stop_word ? preempt->stop_word : counters + 5;
   const uint32_t token = preempt && preempt->stop_word ? preempt->token : 0xFFFFFFFFu;
-  auto k = plan->stages == 2 ? img_resize2x_wm_tma<2, true, 3> : img_resize2x_wm_tma<3, true, 2>;
+  const ImgKernel k = img_kernel<true>(plan->stages, plan->math, plan->ws);
   plan->chained = false;
-  k<<<grid, kImgThreads, plan->smem, static_cast<cudaStream_t>(stream)>>>(
+  k<<<grid, plan->ws ? kImgThreads + 32 : kImgThreads, plan->smem, static_cast<cudaStream_t>(stream)>>>(
       src, dst, static_cast<const uint4*>(prepared), plan->dw, plan->dh, static_cast<uint32_t>(rows),
       counters, word, token, static_cast<uint32_t>(max_rows));
   FR_CUDA_LAUNCHED("img_resize_watermark_preemptible");

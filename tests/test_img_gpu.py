@@ -36,13 +36,17 @@ def test_tma_2x_4k_bit_exact(g, sidetask_oracle, n):
     assert np.array_equal(dst.cpu().numpy(), want)
 
 
-def test_prepared_watermark_path_bit_exact(g, sidetask_oracle):
-    """The task's path: watermark prepared once, per-step kernel on the prepared form."""
+@pytest.mark.parametrize("math", ["1", "0"])
+def test_prepared_watermark_path_bit_exact(g, sidetask_oracle, monkeypatch, math):
+    """The task's path: watermark prepared once, per-step kernel on the prepared form.
+    Both exact-2x math variants (FR_IMG_MATH: 1 = dp4a sums, the default; 0 =
+    16-bit lane sums), each with its own prepared layout (10 / 8 B per pixel)."""
+    monkeypatch.setenv("FR_IMG_MATH", math)
     plan = g.ImagePlan(3840, 2160, 1920, 1080)
     src = g.img_generate(3, 3840, 2160, seed=21)
     wm = g.img_generate_watermark(1920, 1080, seed=22)
     prepared = plan.prepare(wm)
-    assert prepared.numel() == 1920 * 1080 * 8
+    assert prepared.numel() == 1920 * 1080 * (10 if math == "1" else 8)
     dst = torch.empty((3, 1080, 1920, 3), dtype=torch.uint8, device="cuda")
     plan.run_prepared(src, dst, prepared)
     want = sidetask_oracle.img_resize_watermark(src.cpu().numpy(), wm.cpu().numpy(), 1920, 1080)
