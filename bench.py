@@ -80,7 +80,7 @@ STEP_GROUP = int(os.environ.get("FR_STEP_GROUP", "3"))   # steps between one pai
 E2E_IMAGES_PER_STEP = 1
 E2E_RING = int(os.environ.get("FR_E2E_RING", "128"))   # device staging slots: the copy engines run ahead of the steps
 OUT_PX = FRAMES["dw"] * FRAMES["dh"]
-K5_WARP_INSTR_PER_PX = 1.434   # img_resize2x_wm_tma<2,0,3>, ncu instruction count (profiles/r2_k5_harvest_20sm_ncu.txt)
+K5_WARP_INSTR_PER_PX = 0.982   # img_resize2x_wm_ws, ncu instruction count (profiles/r2s_k5ws_ncu.txt; round 1: 1.434)
 PR = dict(scale=20, edge_factor=16, seed=1, iters_per_step=2)
 SGD = dict(V=3072441, E=117185083, k=16, edge_seed=2, init_seed=3,
            edges_per_step=int(os.environ.get("FR_SGD_EDGES_PER_STEP", str(1 << 22))))
@@ -525,25 +525,22 @@ def emit(args, results, ws, names, csr):
         traffic = traffic / timgs * IMAGES_PER_STEP
     # The dominant kernel's HBM roofline: K5 on every SM, launched by the
     # runtime in the bubbles of this run (workload image_full_gpu).  The
-    # headline runs the same kernel on an IMG_SMS budget, where it is bound by
-    # those SMs' issue rate (profiles/r2_k5_harvest_20sm_ncu.txt: 3.5 of 4
-    # warp-instructions per cycle per active SM, 1.434 per output pixel), not
-    # by HBM: that operating point and its SM-issue roofline sit beside it.
-    image_roof = roof("image_full_gpu", f"img_resize2x_wm_tma ({IMAGES_PER_STEP} frames/launch, all 148 SMs, "
+    # headline runs the same kernel on the ΔT controller's budget (DESIGN.md
+    # §5c): there the bound is the GPU's power budget, not HBM or issue --
+    # that operating point (SM-equivalents, GB/s, fraction of HBM) sits beside it.
+    image_roof = roof("image_full_gpu", f"img_resize2x_wm_ws ({IMAGES_PER_STEP} frames/launch, all 148 SMs, "
                                         "in-pipeline)") or {}
     image_roof["traffic"] = traffic
-    op = roof("image", f"img_resize2x_wm_tma ({IMAGES_PER_STEP} frames/launch, in-pipeline, {IMG_SMS}-SM budget)")
+    op = roof("image", f"img_resize2x_wm_ws ({IMAGES_PER_STEP} frames/launch, in-pipeline, ΔT-controlled budget)")
     if op:
         sms = results[0]["image"]["sms"] or 148
-        px_per_byte = OUT_PX * IMAGES_PER_STEP / results[0]["image"]["bytes_per_step"]
-        clk = (results[0]["clocks"].get("sm_mhz") or 1800) * 1e6
-        issue_peak = sms * 4 * clk / K5_WARP_INSTR_PER_PX / px_per_byte / 1e9
         image_roof["operating_point"] = {
-            "sms": sms, "achieved": op["achieved"], "unit": "GB/s", "mean_launch_us": op["mean_launch_us"],
-            "hbm_frac": op["frac"], "bound": "SM issue (the power budget's SMs)",
-            "sm_issue_peak": issue_peak, "frac": op["achieved"] / issue_peak,
-            "how": f"{sms} SMs x 4 warp-instr/cycle x {clk / 1e6:.0f} MHz (median SM clock of the run) / "
-                   f"{K5_WARP_INSTR_PER_PX} warp-instr per px (ncu) / {px_per_byte:.4f} px per algorithmic byte"}
+            "sm_equivalents": sms, "ctas": 3 * sms, "achieved": op["achieved"], "unit": "GB/s",
+            "mean_launch_us": op["mean_launch_us"], "hbm_frac": op["frac"],
+            "bound": "the GPU power budget (ΔT controller): every joule the side task spends in a bubble "
+                     "comes out of the GEMMs' boost clock",
+            "how": f"{sms:.1f} SM-equivalents = {3 * sms:.0f} one-pipeline CTAs spread one per SM; "
+                   f"{K5_WARP_INSTR_PER_PX} warp-instructions per output pixel (ncu)"}
     cpu = cpu_image(args.cpu_seconds) if not args.no_cpu else None
     if cpu:
         cpu.update(cpu_info())
@@ -593,7 +590,7 @@ def emit(args, results, ws, names, csr):
         "config": "configs[1] with the side task on all 148 SMs: the most px per bubble-second, but the "
                   "power its HBM streaming draws slows every GEMM of the pipeline (DESIGN.md §5c)",
         "value": rate("image_full_gpu"), "unit": UNIT, **dT_fields("image_full_gpu"), "fill": fill("image_full_gpu"),
-        "roofline": roof("image_full_gpu", f"img_resize2x_wm_tma ({IMAGES_PER_STEP} frames/launch, 148 SMs, "
+        "roofline": roof("image_full_gpu", f"img_resize2x_wm_ws ({IMAGES_PER_STEP} frames/launch, 148 SMs, "
                                            "in-pipeline)")}
     launches = sum(r[n]["launches"] for r in results for n in names) + sum(r["gap_kernels"] for r in results)
     line = {

@@ -137,6 +137,7 @@ __device__ __forceinline__ void img_group8(const uint8_t* __restrict__ ra, const
 // watermark: 5 words per pair {wX, wY, wZ, 255 - a0, 255 - a1}, wc = w*a + 127
 // in the matching lane, group-transposed [y][5][groups] (uint4) like variant 0.
 constexpr int kWmVecs1 = 5;  // uint4 per 8-pixel group
+constexpr int kWsPipes = 3;  // producer/consumer pipelines per CTA of the warp-specialised kernel
 
 __global__ void img_prepare_wm1_kernel(const uint8_t* __restrict__ wm, uint4* __restrict__ out,
                                        int dw, int dh) {
@@ -376,27 +377,36 @@ __global__ void __launch_bounds__(kImgThreads, CPS)
 //    on full[s] for the data;
 //  * 8 consumer warps compute and store straight from registers to HBM
 //    (st.global.cs, 24 B per thread, 768 B per warp), so the whole smem
-//    budget is input (3 CTAs x 3 stages x 23 KB per SM); each warp releases
-//    the stage on empty[s] (one arrival per warp) and moves on.
-template <int S, bool PREEMPT, int CPS>
-__global__ void __launch_bounds__(kImgThreads + 32, CPS)
+//    budget is input (3 pipelines x 3 stages x 23 KB per SM); each warp
+//    releases the stage on empty[s] (one arrival per warp) and moves on;
+//  * a CTA holds G such pipelines (G x 9 warps, G x S stages) and the grid
+//    is one CTA per SM, so an SM budget of n launches n CTAs on n SMs (with
+//    3 small CTAs per SM the block scheduler spreads 3n CTAs over 3n SMs).
+constexpr int kWsWarps = kImgThreads / 32 + 1;  // per pipeline: 8 consumers + the producer
+
+template <int S, bool PREEMPT, int G>
+__global__ void __launch_bounds__(G * kWsWarps * 32, kWsPipes / G)
     img_resize2x_wm_ws(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
                        const uint4* __restrict__ wmp, int dw, int dh, uint32_t rows,
                        uint32_t* __restrict__ counters, const uint32_t* __restrict__ stop_word,
                        uint32_t token, uint32_t budget) {
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ uint32_t row_of[S];
-  constexpr int kWarps = kImgThreads / 32;  // consumer warps; warp kWarps is the producer
+  __shared__ uint32_t row_of_all[G][S];
+  constexpr int kWarps = kWsWarps - 1;  // consumer warps; warp kWarps of a pipeline is its producer
   const uint32_t src_row = 6u * static_cast<uint32_t>(dw);  // one source row, RGB
   const uint32_t out_row = 3u * static_cast<uint32_t>(dw);
   const uint32_t stage_bytes = (2u * src_row + 127u) & ~127u;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int pipe = tid / (kWsWarps * 32), warp = (tid >> 5) - pipe * kWsWarps;
+  const int ctid = tid - pipe * kWsWarps * 32;  // thread index within the pipeline
+  uint8_t* stages = smem + static_cast<uint32_t>(pipe) * S * stage_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + G * S * stage_bytes) + pipe * 3 * S;
   uint64_t* meta = full + S;
   uint64_t* empty = meta + S;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint32_t* row_of = row_of_all[pipe];
   const int groups = dw >> 3;
 
-  if (tid == 0) {
+  if (ctid == 0) {
     for (int s = 0; s < S; ++s) {
       frk::mbar_init(&full[s], 1);
       frk::mbar_init(&meta[s], 1);
@@ -424,7 +434,7 @@ __global__ void __launch_bounds__(kImgThreads + 32, CPS)
         const uint32_t r = next;
         row_of[s] = r;
         frk::mbar_arrive(&meta[s]);
-        if (r >= rows) {  // no more rows: consumers leave at this stage
+        if (r >= rows) {  // no more rows: this pipeline's consumers leave at this stage
           if (!PREEMPT) asm volatile("griddepcontrol.launch_dependents;");
           break;
         }
@@ -433,7 +443,7 @@ __global__ void __launch_bounds__(kImgThreads + 32, CPS)
         const uint32_t img = r / static_cast<uint32_t>(dh);
         const uint32_t y = r - img * static_cast<uint32_t>(dh);
         frk::mbar_arrive_expect_tx(&full[s], 2u * src_row);
-        frk::bulk_g2s(smem + s * stage_bytes,
+        frk::bulk_g2s(stages + s * stage_bytes,
                       src + (static_cast<uint64_t>(img) * 2 * dh + 2 * y) * src_row, 2u * src_row,
                       &full[s], pol_stream);
       }
@@ -451,11 +461,11 @@ __global__ void __launch_bounds__(kImgThreads + 32, CPS)
       if (row >= rows) break;
       const uint32_t img = row / static_cast<uint32_t>(dh);
       const uint32_t y = row - img * static_cast<uint32_t>(dh);
-      const uint8_t* ra = smem + s * stage_bytes;
+      const uint8_t* ra = stages + s * stage_bytes;
       const uint8_t* rb = ra + src_row;
       uint8_t* orow = dst + static_cast<uint64_t>(row) * out_row;
       bool waited = false;
-      for (int g = tid; g < groups; g += kImgThreads) {
+      for (int g = ctid; g < groups; g += kImgThreads) {
         // watermark first (L2): its latency overlaps the copy still in flight
         uint32_t wv[4 * kWmVecs1];
         const uint4* pw = wmp + (y * static_cast<uint32_t>(kWmVecs1 * groups) + static_cast<uint32_t>(g));
@@ -590,8 +600,8 @@ namespace {
 using ImgKernel = void (*)(const uint8_t*, uint8_t*, const uint4*, int, int, uint32_t, uint32_t*,
                            const uint32_t*, uint32_t, uint32_t);
 template <bool PREEMPT>
-ImgKernel img_kernel(int stages, int math, bool ws) {
-  if (ws) return img_resize2x_wm_ws<3, PREEMPT, 3>;
+ImgKernel img_kernel(int stages, int math, bool ws, int pipes) {
+  if (ws) return pipes == 1 ? img_resize2x_wm_ws<3, PREEMPT, 1> : img_resize2x_wm_ws<3, PREEMPT, kWsPipes>;
   if (math == 1)
     return stages == 2 ? img_resize2x_wm_tma<2, PREEMPT, 3, 1> : img_resize2x_wm_tma<3, PREEMPT, 2, 1>;
   return stages == 2 ? img_resize2x_wm_tma<2, PREEMPT, 3, 0> : img_resize2x_wm_tma<3, PREEMPT, 2, 0>;
@@ -603,7 +613,13 @@ struct fr_img_plan {
   int stages = kImgStages, ctas_per_sm = kImgCtasPerSm;  // TMA path pipeline shape
   int path = FR_IMG_PATH_GENERAL;
   int math = 1;  // exact-2x math variant: 1 = dp4a sums (default), 0 = 16-bit lane sums (FR_IMG_MATH=0)
-  bool ws = true;  // warp-decoupled kernel (default); FR_IMG_CFG=bar|3x2: the per-row-barrier kernel
+  bool ws = true;  // warp-specialised kernel (default); FR_IMG_CFG=bar|3x2: the per-row-barrier kernel
+  // pipelines per CTA: 1 (default) = one-pipeline CTAs, up to 3 per SM, an SM
+  // budget of n launching 3n of them (spread one per SM over 3n SMs while
+  // 3n <= 148); FR_IMG_PIPES=3: one 3-pipeline CTA per SM, n CTAs on n SMs.
+  // Spread CTAs harvest ~40 % more pixels at the same pipeline ΔT
+  // (gpurun_out/r2s_ctrl_pipes.log).
+  int pipes = 1;
   int32_t* d_tab = nullptr;
   void* d_wm = nullptr;  // plan-owned prepared watermark for fr_img_resize_watermark
   uint32_t* d_ctr = nullptr;  // dynamic row scheduler {next row, CTAs done} x kImgCtrSlots; one stream at a time
@@ -620,6 +636,7 @@ struct fr_img_plan {
   int sms = 0;
   int max_sms = 0;  // fr_img_plan_set_max_sms: grid sized for this many SMs (0 = all)
   int64_t grid_sms() const { return max_sms > 0 ? std::min(max_sms, sms) : sms; }
+  int block() const { return ws ? pipes * kWsWarps * 32 : kImgThreads; }
   size_t prepared_bytes() const {
     if (path != FR_IMG_PATH_TMA_2X) return static_cast<size_t>(dw) * dh * 4;
     return static_cast<size_t>(dw) * dh * (math == 1 ? 2 * kWmVecs1 : 8);
@@ -653,14 +670,15 @@ int fr_img_plan_create(int32_t sw, int32_t sh, int32_t dw, int32_t dh, fr_img_pl
     }
     if (const char* m = std::getenv("FR_IMG_MATH")) plan->math = std::atoi(m) == 0 ? 0 : 1;
     if (plan->math == 0) plan->ws = false;  // the warp-decoupled kernel has the dp4a math only
-    if (plan->ws) plan->stages = 3, plan->ctas_per_sm = 3;
-    plan->smem = plan->ws ? plan->stages * al(12 * dw) + plan->stages * 24
+    if (const char* e = std::getenv("FR_IMG_PIPES")) plan->pipes = std::atoi(e) == kWsPipes ? kWsPipes : 1;
+    if (plan->ws) plan->stages = 3, plan->ctas_per_sm = kWsPipes / plan->pipes;
+    plan->smem = plan->ws ? plan->pipes * plan->stages * (al(12 * dw) + 24)
                           : plan->stages * (al(12 * dw) + al(3 * dw)) + plan->stages * 8;
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     if (plan->smem <= optin) {
-      for (const void* fn : {reinterpret_cast<const void*>(img_kernel<false>(plan->stages, plan->math, plan->ws)),
-                             reinterpret_cast<const void*>(img_kernel<true>(plan->stages, plan->math, plan->ws))}) {
+      for (const void* fn : {reinterpret_cast<const void*>(img_kernel<false>(plan->stages, plan->math, plan->ws, plan->pipes)),
+                             reinterpret_cast<const void*>(img_kernel<true>(plan->stages, plan->math, plan->ws, plan->pipes))}) {
         if (e == cudaSuccess)
           e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, plan->smem);
         if (e == cudaSuccess)
@@ -764,7 +782,7 @@ int fr_img_resize_watermark_prepared(const fr_img_plan* plan, const uint8_t* src
     const int64_t rows = static_cast<int64_t>(n) * plan->dh;
     if (rows >= (int64_t{1} << 31)) return frcapi::fail(FR_ERR_UNSUPPORTED, "too many rows in one step");
     const int grid = static_cast<int>(std::min<int64_t>(rows, plan->grid_sms() * plan->ctas_per_sm));
-    const ImgKernel k = img_kernel<false>(plan->stages, plan->math, plan->ws);
+    const ImgKernel k = img_kernel<false>(plan->stages, plan->math, plan->ws, plan->pipes);
     // Consecutive steps overlap their tail and head (programmatic dependent
     // launch: a launch's CTAs start once every CTA of the previous one took
     // its last row).  Steps touch different frames; the row counters rotate
@@ -779,7 +797,7 @@ int fr_img_resize_watermark_prepared(const fr_img_plan* plan, const uint8_t* src
     plan->chain_stream = s;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(plan->ws ? kImgThreads + 32 : kImgThreads);
+    cfg.blockDim = dim3(plan->block());
     cfg.dynamicSmemBytes = plan->smem;
     cfg.stream = s;
     cudaLaunchAttribute at[1];
@@ -820,9 +838,9 @@ int fr_img_resize_watermark_preemptible(const fr_img_plan* plan, const uint8_t* 
   // no preempt: a stop word that never fires (counters[5] stays 0 < token)
   const uint32_t* word = preempt && preempt->stop_word ? preempt->stop_word : counters + 5;
   const uint32_t token = preempt && preempt->stop_word ? preempt->token : 0xFFFFFFFFu;
-  const ImgKernel k = img_kernel<true>(plan->stages, plan->math, plan->ws);
+  const ImgKernel k = img_kernel<true>(plan->stages, plan->math, plan->ws, plan->pipes);
   plan->chained = false;
-  k<<<grid, plan->ws ? kImgThreads + 32 : kImgThreads, plan->smem, static_cast<cudaStream_t>(stream)>>>(
+  k<<<grid, plan->block(), plan->smem, static_cast<cudaStream_t>(stream)>>>(
       src, dst, static_cast<const uint4*>(prepared), plan->dw, plan->dh, static_cast<uint32_t>(rows),
       counters, word, token, static_cast<uint32_t>(max_rows));
   FR_CUDA_LAUNCHED("img_resize_watermark_preemptible");

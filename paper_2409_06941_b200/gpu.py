@@ -190,7 +190,10 @@ class ImageTask:
         self.units_per_step = self.vt.work_units_per_step
         # per-step algorithmic HBM bytes (src + dst per image; the watermark
         # is read once per step and stays L2-resident across its images)
-        self.bytes_per_step = images_per_step * (sw * sh * 3 + dw * dh * 3) + dw * dh * 8
+        # frames in + frames out + the prepared watermark once (L2-resident: 10 B/px
+        # on the exact-2x path, read by every launch; the raw RGBA 4 B/px otherwise)
+        exact2x = sw == 2 * dw and sh == 2 * dh and dw % 16 == 0
+        self.bytes_per_step = images_per_step * (sw * sh * 3 + dw * dh * 3) + dw * dh * (10 if exact2x else 4)
         self.h2d_per_step = images_per_step * sw * sh * 3 if host_io else 0
         self.d2h_per_step = images_per_step * dw * dh * 3 if host_io else 0
 

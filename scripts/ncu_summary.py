@@ -1,41 +1,39 @@
-"""Print the headline sections of an ncu report (details page) and the top
-warp-stall reasons (raw page) -- used to write the profiles/ summaries."""
+"""Summarise ncu reports (raw page) into the numbers DESIGN.md / bench.py cite.
+Usage: python scripts/ncu_summary.py REPORT.ncu-rep [...]  (run where ncu is installed)"""
 import csv
 import subprocess
 import sys
 
-KEYS = ['Throughput', 'Hit', 'Duration', 'Occupancy', 'Warp Cycles', 'Issue', 'Registers',
-        'Shared Memory', 'Elapsed Cycles', 'SM Frequency']
+UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3}
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "dram__bytes.sum.per_second",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "smsp__inst_executed.sum",
+        "sm__cycles_elapsed.avg.per_second", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "sm__warps_active.avg.pct_of_peak_sustained_active", "lts__t_sector_hit_rate.pct",
+        "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
+        "launch__occupancy_limit_shared_mem", "sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_active"]
 
 
-def main(rep, kernel_filter=""):
-    det = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
-    for r in csv.reader(det.splitlines()):
-        if len(r) > 14 and kernel_filter in r[4] and any(k in r[12] for k in KEYS):
-            print(f"{r[11][:28]:28s} | {r[12]} [{r[13]}] {r[14]}")
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-    rows = list(csv.reader(raw.splitlines()))
-    h = rows[0]
+def summarise(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    head, units = rows[0], rows[1]
     for v in rows[2:]:
-        if kernel_filter not in v[4]:
-            continue
+        d = {k: (u, x) for k, u, x in zip(head, units, v)}
+        print(f"== {path}: {d.get('Kernel Name', ('', '?'))[1][:100]}")
+        for k in KEYS:
+            if k in d:
+                print(f"  {k:70s} {d[k][1]:>16s} {d[k][0]}")
         st = []
-        for k, x in zip(h, v):
-            if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued"):
+        for k, (u, x) in d.items():
+            if k.startswith("smsp__pcsamp_warps_issue_stalled") and not k.endswith("not_issued"):
                 try:
-                    st.append((float(x.replace(",", "")), k[len("smsp__pcsamp_warps_issue_stalled_"):]))
+                    st.append((float(x.replace(",", "")), k.replace("smsp__pcsamp_warps_issue_stalled_", "")))
                 except ValueError:
                     pass
         tot = sum(x for x, _ in st) or 1
-        print("stalls:", ", ".join(f"{n} {100 * x / tot:.0f}%" for x, n in sorted(st, reverse=True)[:6]))
-        for k, x in zip(h, v):
-            if k in ("dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum",
-                     "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum",
-                     "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum",
-                     "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
-                     "smsp__inst_executed.sum"):
-                print(f"{k} = {x}")
+        print("  stall samples: " + ", ".join(f"{k} {x / tot * 100:.0f}%" for x, k in sorted(st, reverse=True)[:7]))
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else "")
+    for p in sys.argv[1:]:
+        summarise(p)
