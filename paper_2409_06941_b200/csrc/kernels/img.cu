@@ -391,7 +391,7 @@ __global__ void __launch_bounds__(G * kWsWarps * 32, kWsPipes / G)
                        uint32_t* __restrict__ counters, const uint32_t* __restrict__ stop_word,
                        uint32_t token, uint32_t budget) {
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ uint32_t row_of_all[G][S];
+  __shared__ uint32_t row_of_all[G][S], y_of_all[G][S];
   constexpr int kWarps = kWsWarps - 1;  // consumer warps; warp kWarps of a pipeline is its producer
   const uint32_t src_row = 6u * static_cast<uint32_t>(dw);  // one source row, RGB
   const uint32_t out_row = 3u * static_cast<uint32_t>(dw);
@@ -404,6 +404,7 @@ __global__ void __launch_bounds__(G * kWsWarps * 32, kWsPipes / G)
   uint64_t* meta = full + S;
   uint64_t* empty = meta + S;
   uint32_t* row_of = row_of_all[pipe];
+  uint32_t* y_of = y_of_all[pipe];  // the row's output y: consumers skip the division
   const int groups = dw >> 3;
 
   if (ctid == 0) {
@@ -433,15 +434,17 @@ __global__ void __launch_bounds__(G * kWsWarps * 32, kWsPipes / G)
         if (k >= S) frk::mbar_wait(&empty[s], ((k / S) - 1) & 1u);
         const uint32_t r = next;
         row_of[s] = r;
-        frk::mbar_arrive(&meta[s]);
         if (r >= rows) {  // no more rows: this pipeline's consumers leave at this stage
+          frk::mbar_arrive(&meta[s]);
           if (!PREEMPT) asm volatile("griddepcontrol.launch_dependents;");
           break;
         }
-        next = take();  // consumed next iteration: the round trip overlaps this copy
-        ++done;
         const uint32_t img = r / static_cast<uint32_t>(dh);
         const uint32_t y = r - img * static_cast<uint32_t>(dh);
+        y_of[s] = y;
+        frk::mbar_arrive(&meta[s]);
+        next = take();  // consumed next iteration: the round trip overlaps this copy
+        ++done;
         frk::mbar_arrive_expect_tx(&full[s], 2u * src_row);
         frk::bulk_g2s(stages + s * stage_bytes,
                       src + (static_cast<uint64_t>(img) * 2 * dh + 2 * y) * src_row, 2u * src_row,
@@ -459,8 +462,7 @@ __global__ void __launch_bounds__(G * kWsWarps * 32, kWsPipes / G)
       frk::mbar_wait(&meta[s], ph);
       const uint32_t row = row_of[s];
       if (row >= rows) break;
-      const uint32_t img = row / static_cast<uint32_t>(dh);
-      const uint32_t y = row - img * static_cast<uint32_t>(dh);
+      const uint32_t y = y_of[s];
       const uint8_t* ra = stages + s * stage_bytes;
       const uint8_t* rb = ra + src_row;
       uint8_t* orow = dst + static_cast<uint64_t>(row) * out_row;
