@@ -75,7 +75,8 @@ DT_BUDGET = float(os.environ.get("FR_DT_BUDGET", "0.006"))
 IMG_SMS = int(os.environ.get("FR_IMG_SMS", "16"))
 SGD_SMS = int(os.environ.get("FR_SGD_SMS", "20"))
 E2E_SMS = int(os.environ.get("FR_E2E_SMS", "8"))     # PCIe-bound (4.5e9 px/s): 8 SMs of K5 keep up with the link
-PAIRS = int(os.environ.get("FR_DT_PAIRS", "3"))           # (baseline, harvest) pairs for the headline ΔT
+PAIRS = int(os.environ.get("FR_DT_PAIRS", "4"))           # (baseline, harvest) pairs for the headline ΔT (ABBA order)
+PAIRS_OTHER = int(os.environ.get("FR_DT_PAIRS_OTHER", "2"))   # ... for every other workload
 STEP_GROUP = int(os.environ.get("FR_STEP_GROUP", "3"))   # steps between one pair of timing events
 E2E_IMAGES_PER_STEP = 1
 E2E_RING = int(os.environ.get("FR_E2E_RING", "128"))   # device staging slots: the copy engines run ahead of the steps
@@ -264,14 +265,20 @@ def harvest(h, name, task, K, W, sms=0, kinds=None, budget=0.0, pairs=1):
         print(f"bench: {name} ran no step in {3 * max(W, 1)} warm-up epochs "
               f"({h.task_status(name)}); keeping the standalone profile", file=sys.stderr)
     bases, withs, ob, ow, durs = [], [], [], [], []
-    for _ in range(pairs):
-        bases.append(h.run(K, False))
-        if kinds:
-            ob.append(PD.op_means(h.timeline(0), kinds))
-        withs.append(h.run(K, True))
-        if kinds:
-            ow.append(PD.op_means(h.timeline(0), kinds))
-        durs += [b - a for a, b in h.timeline(2)]
+    for i in range(pairs):
+        # ABBA order (baseline first in even pairs, harvest first in odd ones):
+        # a drift of the power / thermal state over the run (the GPU warming
+        # up) then cancels from the averaged ΔT instead of biasing it
+        for with_tasks in ((False, True) if i % 2 == 0 else (True, False)):
+            if with_tasks:
+                withs.append(h.run(K, True))
+                if kinds:
+                    ow.append(PD.op_means(h.timeline(0), kinds))
+                durs += [b - a for a, b in h.timeline(2)]
+            else:
+                bases.append(h.run(K, False))
+                if kinds:
+                    ob.append(PD.op_means(h.timeline(0), kinds))
     base, r = _sum_reports(bases), _sum_reports(withs)
     mean2 = (lambda xs: tuple(statistics.fmean(x[i] for x in xs) for i in range(2))) if kinds else None
     ops_base = mean2(ob) if kinds else None
@@ -306,7 +313,8 @@ def ours(args):
     from paper_2409_06941_b200 import api as host_api
     from paper_2409_06941_b200 import pipeline_dt as PD
     A = host_api()
-    names = ["image", "image_full_gpu", "image_imperative", "pagerank", "sgd"] + ([] if args.no_e2e else ["image_e2e"])
+    names = (["image", "image_full_gpu", "image_imperative", "pagerank", "pagerank_full_gpu", "sgd", "sgd_full_gpu"]
+             + ([] if args.no_e2e else ["image_e2e"]))
     sms_of = {"image": IMG_SMS, "image_imperative": IMG_SMS, "image_e2e": E2E_SMS, "sgd": SGD_SMS}
     runs = {n: [] for n in names}
     stage_prof = []
@@ -327,13 +335,13 @@ def ours(args):
                 elif n == "image_e2e":
                     task = gpu.ImageTask(batch=BATCH, images_per_step=E2E_IMAGES_PER_STEP, host_io=True,
                                          host_ring=E2E_RING, **FRAMES)
-                elif n == "pagerank":
+                elif n in ("pagerank", "pagerank_full_gpu"):
                     task = gpu.PageRankTask(**PR)
                 else:
                     task = gpu.SgdTask(**SGD)
                 runs[n].append(harvest(h, n, task, K, W, sms=sms_of.get(n, 0), kinds=kinds,
-                                       budget=0.0 if n == "image_full_gpu" else DT_BUDGET,
-                                       pairs=PAIRS if n == "image" else 1))
+                                       budget=0.0 if n.endswith("_full_gpu") else DT_BUDGET,
+                                       pairs=PAIRS if n == "image" else PAIRS_OTHER))
             h.close()
     torch.cuda.synchronize()
     if dist:
@@ -414,7 +422,7 @@ def ours(args):
             h = gpu.Harness(num_stages=STAGES, num_micro_batches=MICRO_BATCHES, stage=s, step_group=STEP_GROUP,
                             **SHAPE_36B)
             r = harvest(h, name, make(), K, W, sms=sms, kinds=PD.issue_kinds(A, s, STAGES, MICRO_BATCHES),
-                        budget=DT_BUDGET)
+                        budget=DT_BUDGET, pairs=PAIRS_OTHER)
             h.close()
             mruns.append(dict(r, stage=s))
             mixed["stages"].append({"stage": s, "task": name, "units_per_bubble_s": r["with"]["work_units"] / r["base"]["bubble_s"],
@@ -437,7 +445,7 @@ def ours(args):
                             tokens=8192, ffn_mult=4, step_group=STEP_GROUP, profile_epochs=2)
             prof = prof or h.profile()
             r = harvest(h, "image", gpu.ImageTask(batch=BATCH, images_per_step=IMAGES_PER_STEP, **FRAMES), K5, W,
-                        sms=IMG_SMS, kinds=PD.issue_kinds(A, s, 8, 8), budget=DT_BUDGET)
+                        sms=IMG_SMS, kinds=PD.issue_kinds(A, s, 8, 8), budget=DT_BUDGET, pairs=PAIRS_OTHER)
             h.close()
             c5runs.append(dict(r, stage=s))
         pipe = pipe_dt(c5runs, 8, 8, K5)
@@ -552,8 +560,11 @@ def emit(args, results, ws, names, csr):
                **dT_fields("image_e2e"), "fill": fill("image_e2e"),
                "path": f"fr_image_task host_io=1: pinned host frames -> {E2E_RING}-slot device ring filled by the "
                        "copy engines ahead of the steps (also while the pipeline computes) -> K5 -> D2H per frame"}
-    pr_roof = roof("pagerank", "pr_pull_kernel (2 launches of 1 iteration per step, in-pipeline); "
-                               "working set L2-resident: latency-bound gathers, not HBM")
+    # PageRank and Graph-SGD kernel rooflines: on all SMs, launched by the
+    # runtime in this run's bubbles (workloads *_full_gpu), like K5's; their
+    # ΔT-controlled operating points are the workloads' values
+    pr_roof = roof("pagerank_full_gpu", "pr_pull_kernel (2 launches of 1 iteration per step, all 148 SMs, "
+                                        "in-pipeline); working set L2-resident: latency-bound gathers, not HBM")
     if pr_roof:
         l2 = results[0]["l2_gbps"]
         pr_roof["l2"] = {"achieved": pr_roof["achieved"], "peak": l2, "unit": "GB/s", "frac": pr_roof["achieved"] / l2,
@@ -568,13 +579,19 @@ def emit(args, results, ws, names, csr):
         "sgd": {"config": f"configs[2]: Orkut shape V=3,072,441 E=117,185,083 k=16, {SGD['edges_per_step']} edges/step, "
                           "by-user layout (fr_sgd_group_by_user)",
                 "value": rate("sgd"), "unit": "edges/bubble-s", **dT_fields("sgd"), "fill": fill("sgd"),
-                "roofline": dict(roof("sgd", f"sgd_user_kernel<16> ({SGD['edges_per_step']} edges/launch, in-pipeline; "
+                "roofline": dict(roof("sgd_full_gpu", f"sgd_user_kernel<16> ({SGD['edges_per_step']} edges/launch, "
+                                                      "all 148 SMs, in-pipeline; "
                                              "alg bytes 12 + 128 per edge + 128 per L_u load; item blocks keep "
                                              "L_v in L2, so part of them never reaches DRAM)") or {},
-                                 traffic=70.7 * SGD["edges_per_step"],
-                                 traffic_source="profiles/r1_sgd_user_blk_ncu.txt (cold, standalone)"),
+                                 traffic=63.6 * SGD["edges_per_step"],
+                                 traffic_source="profiles/r2_sgd_harvest_ncu.txt (inside a harvest, all SMs: "
+                                                "266.7 MB DRAM per 2^22-edge step)"),
                 "cpu_baseline": cpu_sgd(args.cpu_seconds / 2) if not args.no_cpu else None},
     }
+    for n, unit in (("pagerank_full_gpu", "edges/bubble-s"), ("sgd_full_gpu", "edges/bubble-s")):
+        workloads[n] = {"config": f"{n[:-9]} with the side task on all 148 SMs (no ΔT budget): the kernel's "
+                                  "roofline is measured here", "value": rate(n), "unit": unit, **dT_fields(n),
+                        "fill": fill(n)}
     imp = results[0]["image_imperative"]
     workloads["image_imperative"] = {
         "config": "configs[1] through the imperative interface (RunGpuWorkload): one preemptible K5 "
@@ -607,7 +624,7 @@ def emit(args, results, ws, names, csr):
         "dT_budget_met": dT("image") <= 0.01, "fill": fill("image"),
         "delta_t_pairs": PAIRS,
         "delta_t_noise": {"null_dT": results[0]["image"]["null_dT"],
-                          "how": "pipeline ΔT between consecutive baseline runs (no side task in either)"},
+                          "how": "pipeline ΔT between the baseline runs (no side task in either) of successive ABBA pairs"},
         "overrun_frac": sum(r["image"]["overrun"] for r in results) / max(1e-12, sum(r["image"]["used"] for r in results)),
         "bubble_s_per_step": max(r["image"]["bubble_s"] for r in results) / (K * PAIRS),
         "px_per_step": sum(r["image"]["units"] for r in results) / (K * PAIRS),

@@ -346,7 +346,9 @@ class PageRankTask:
         self.units_per_step = self.vt.work_units_per_step
         # compulsory bytes per pull iteration: offsets + col_idx + c gather
         # source (read once) + inv_outdeg + r' and c' writes
-        self.bytes_per_step = iters_per_step * (4 * (self.V + 1) + 4 * self.E + 16 * self.V)
+        # offsets, a column id and a source value per edge, r/c reads
+        # and writes -- the standard pull-SpMV byte count
+        self.bytes_per_step = iters_per_step * (4 * (self.V + 1) + 8 * self.E + 16 * self.V)
         self.h2d_per_step = self.d2h_per_step = 0
 
     def ranks(self):
