@@ -75,8 +75,8 @@ DT_BUDGET = float(os.environ.get("FR_DT_BUDGET", "0.006"))
 IMG_SMS = int(os.environ.get("FR_IMG_SMS", "16"))
 SGD_SMS = int(os.environ.get("FR_SGD_SMS", "20"))
 E2E_SMS = int(os.environ.get("FR_E2E_SMS", "8"))     # PCIe-bound (4.5e9 px/s): 8 SMs of K5 keep up with the link
-PAIRS = int(os.environ.get("FR_DT_PAIRS", "4"))           # (baseline, harvest) pairs for the headline ΔT (ABBA order)
-PAIRS_OTHER = int(os.environ.get("FR_DT_PAIRS_OTHER", "2"))   # ... for every other workload
+PAIRS = int(os.environ.get("FR_DT_PAIRS", "8"))           # (baseline, harvest) pairs for the headline ΔT (ABBA order)
+PAIRS_OTHER = int(os.environ.get("FR_DT_PAIRS_OTHER", "3"))   # ... for every other workload
 STEP_GROUP = int(os.environ.get("FR_STEP_GROUP", "3"))   # steps between one pair of timing events
 E2E_IMAGES_PER_STEP = 1
 E2E_RING = int(os.environ.get("FR_E2E_RING", "128"))   # device staging slots: the copy engines run ahead of the steps
@@ -286,7 +286,7 @@ def harvest(h, name, task, K, W, sms=0, kinds=None, budget=0.0, pairs=1):
     side, train = h.launches()
     h.stop_task(name)
     return {"base": base, "with": r, "durs": durs, "side": side, "train_ops": train, "pairs": pairs,
-            "ops_base": ops_base, "ops_with": ops_with, "ops_base_runs": ob,
+            "ops_base": ops_base, "ops_with": ops_with, "ops_base_runs": ob, "ops_with_runs": ow,
             "sms": r["side_sms_mean"], "budget": budget,
             "units_per_step": task.units_per_step, "bytes_per_step": task.bytes_per_step,
             "h2d": task.h2d_per_step, "d2h": task.d2h_per_step, "est_step_s": tprof["est_per_step_duration"]}
@@ -384,6 +384,12 @@ def ours(args):
         PD.critical_path_dt(A, STAGES, MICRO_BATCHES, K, {i: r_["ops_base_runs"][j] for i, r_ in enumerate(runs["image"])},
                             {i: r_["ops_base_runs"][j + 1] for i, r_ in enumerate(runs["image"])})["dT"]
         for j in range(npairs - 1)]
+    # per-pair pipeline ΔTs of the headline: their spread is the estimate's
+    # standard error (the GPU's clock transients hit runs at random)
+    local_res["image"]["pair_dT"] = [
+        PD.critical_path_dt(A, STAGES, MICRO_BATCHES, K, {i: r_["ops_base_runs"][j] for i, r_ in enumerate(runs["image"])},
+                            {i: r_["ops_with_runs"][j] for i, r_ in enumerate(runs["image"])})["dT"]
+        for j in range(npairs)]
     local_res["clocks"] = clk.summary()
     local_res["l2_gbps"] = gpu.l2_read_gbps()   # PageRank's working set is L2-resident: its roofline
     local_res["gap_kernels"] = sum(r["train_ops"] // (2 * MICRO_BATCHES) * (2 * MICRO_BATCHES + 1)
@@ -623,6 +629,9 @@ def emit(args, results, ws, names, csr):
         "delta_t_stage_max": dT_stages("image"), "delta_t_stages": results[0]["image"]["stage_dT"],
         "dT_budget_met": dT("image") <= 0.01, "fill": fill("image"),
         "delta_t_pairs": PAIRS,
+        "delta_t_pair_values": results[0]["image"]["pair_dT"],
+        "delta_t_se": (statistics.stdev(results[0]["image"]["pair_dT"]) / len(results[0]["image"]["pair_dT"]) ** 0.5
+                       if len(results[0]["image"]["pair_dT"]) > 1 else None),
         "delta_t_noise": {"null_dT": results[0]["image"]["null_dT"],
                           "how": "pipeline ΔT between the baseline runs (no side task in either) of successive ABBA pairs"},
         "overrun_frac": sum(r["image"]["overrun"] for r in results) / max(1e-12, sum(r["image"]["used"] for r in results)),
