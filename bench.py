@@ -72,7 +72,7 @@ IMAGES_PER_STEP = int(os.environ.get("FR_IMAGES_PER_STEP", "16"))   # ~95 us ste
 # on one, +1.6 % on another), so a fixed budget cannot hold the ΔT
 # everywhere.  FR_DT_BUDGET=0 runs the fixed budgets instead.
 DT_BUDGET = float(os.environ.get("FR_DT_BUDGET", "0.006"))
-IMG_SMS = int(os.environ.get("FR_IMG_SMS", "16"))
+IMG_SMS = int(os.environ.get("FR_IMG_SMS", "8"))
 SGD_SMS = int(os.environ.get("FR_SGD_SMS", "20"))
 E2E_SMS = int(os.environ.get("FR_E2E_SMS", "8"))     # PCIe-bound (4.5e9 px/s): 8 SMs of K5 keep up with the link
 PAIRS = int(os.environ.get("FR_DT_PAIRS", "8"))           # (baseline, harvest) pairs for the headline ΔT (ABBA order)

@@ -377,7 +377,7 @@ typedef struct fr_harness_config {
                                    the kill (<= 0: at once) */
   int32_t side_sms;           /* SM budget of the side tasks' kernels (set_sm_budget;
                                  0 = all SMs); the starting point when dt_budget > 0 */
-  int32_t min_side_sms;       /* floor of the ΔT controller (<= 0: 8) */
+  int32_t min_side_sms;       /* floor of the ΔT controller (<= 0: 2) */
   double dt_budget;           /* > 0: ΔT-budgeted harvesting.  The worker times every op
                                  of the stage as it completes, compares it with the same
                                  op in the last run without side tasks, and sizes the side

@@ -457,19 +457,19 @@ struct fr_harness {
     }
   }
   void control(double growth) {
-    const double a = 1.0 / 8.0;
+    const double a = 1.0 / 16.0;  // ~2 epochs of a 4-stage stage's 8 ops: the per-op clock jitter averages out
     ctrl_ewma = (1 - a) * ctrl_ewma + a * growth;
     if (ctrl_hold > 0) {
       --ctrl_hold;
       return;
     }
-    const int lo = cfg.min_side_sms > 0 ? cfg.min_side_sms : 8;
+    const int lo = cfg.min_side_sms > 0 ? cfg.min_side_sms : 2;
     int next = ctrl_sms;
     if (ctrl_ewma > cfg.dt_budget) next = std::max(lo, static_cast<int>(ctrl_sms * 0.8));
     else if (ctrl_ewma < 0.5 * cfg.dt_budget) next = std::min(sm_count, ctrl_sms + std::max(2, ctrl_sms / 8));
     if (next != ctrl_sms) {
       apply_sms(next);
-      ctrl_hold = 4;
+      ctrl_hold = 8;
     }
   }
 
@@ -748,7 +748,10 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
   };
 
   auto task_of = [&](const std::string& id) -> Task& { return *tasks.at(id); };
-  const bool controlled = with_tasks && cfg.dt_budget > 0 && op_ref.size() == static_cast<std::size_t>(nops);
+  // the op-slowdown sensor runs whenever a no-task reference exists (its mean
+  // is reported as op_growth); the controller acts on it only with a budget
+  const bool sensing = with_tasks && op_ref.size() == static_cast<std::size_t>(nops);
+  const bool controlled = sensing && cfg.dt_budget > 0;
   if (controlled && ctrl_sms == 0) {
     ctrl_sms = cfg.side_sms > 0 ? std::min(cfg.side_sms, sm_count) : sm_count;
     ctrl_ewma = 0.0;
@@ -768,7 +771,7 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
       growth_sum += growth;
       sms_sum += ctrl_sms;
       ++growth_n;
-      control(growth);
+      if (controlled) control(growth);
       ++meas_idx;
     }
   };
@@ -998,7 +1001,7 @@ void fr_harness::run(int epochs, bool with_tasks, fr_run_report* rep) {
       drain_completions();
       finish_init();
       finish_pause();
-      if (controlled) measure_ops();
+      if (sensing) measure_ops();
       // 3a. imperative: one preemptible workload at a time (each loops over
       // its input until the device-side stop; a queued second launch would
       // only run -- and exit -- after the next op has taken the SMs)

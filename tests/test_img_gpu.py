@@ -60,8 +60,18 @@ def test_prepared_watermark_path_bit_exact(g, sidetask_oracle, monkeypatch, math
         assert np.array_equal(dst[:1].cpu().numpy(), want)
 
 
-@pytest.mark.parametrize("sw,sh,dw,dh", [(32, 2, 16, 1), (64, 30, 32, 15), (1024, 6, 512, 3)])
-def test_tma_2x_small_shapes(g, sidetask_oracle, sw, sh, dw, dh):
+# exact-2x kernel variants: the warp-specialised kernel with one-pipeline CTAs
+# (default) or 3-pipeline CTAs, the round-1 per-row-barrier kernel with the
+# dp4a math or the 16-bit lane math
+VARIANTS = {"ws": {}, "ws_pipes3": {"FR_IMG_PIPES": "3"}, "bar_dp4a": {"FR_IMG_CFG": "bar"},
+            "bar_lanes": {"FR_IMG_MATH": "0"}}
+
+
+@pytest.mark.parametrize("variant", sorted(VARIANTS))
+@pytest.mark.parametrize("sw,sh,dw,dh", [(32, 2, 16, 1), (64, 30, 32, 15), (1024, 6, 512, 3), (4128, 10, 2064, 5)])
+def test_tma_2x_small_shapes(g, sidetask_oracle, monkeypatch, variant, sw, sh, dw, dh):
+    for k, v in VARIANTS[variant].items():
+        monkeypatch.setenv(k, v)
     plan = g.ImagePlan(sw, sh, dw, dh)
     assert plan.path == g.ImagePlan.TMA_2X
     src = g.img_generate(3, sw, sh, seed=4)
@@ -117,8 +127,11 @@ def test_edge_cases(g):
         plan.run(src.cpu(), dst, wm)
 
 
-def test_full_batch_64_bit_exact(g, sidetask_oracle):
+@pytest.mark.parametrize("variant", ["ws", "ws_pipes3"])
+def test_full_batch_64_bit_exact(g, sidetask_oracle, monkeypatch, variant):
     """configs[1] at its full size: 64 4K images -> 1080p, every byte checked."""
+    for k, v in VARIANTS[variant].items():
+        monkeypatch.setenv(k, v)
     n = 64
     plan = g.ImagePlan(3840, 2160, 1920, 1080)
     src = g.img_generate(n, 3840, 2160, seed=1)
