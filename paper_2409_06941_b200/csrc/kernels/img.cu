@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(kImgThreads, CPS)
     img_resize2x_wm_tma(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
                         const uint4* __restrict__ wmp, int dw, int dh, uint32_t rows,
                         uint32_t* __restrict__ counters, const uint32_t* __restrict__ stop_word,
-                        uint32_t token, uint32_t budget) {
+                        uint32_t token, uint32_t budget, uint32_t /*fpu: rows are claimed one by one*/) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint32_t row_of[S], y_of[S], next_of[S];
   const uint32_t src_row = 6u * static_cast<uint32_t>(dw);  // one source row, RGB
@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(G * kWsWarps * 32, kWsPipes / G)
     img_resize2x_wm_ws(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
                        const uint4* __restrict__ wmp, int dw, int dh, uint32_t rows,
                        uint32_t* __restrict__ counters, const uint32_t* __restrict__ stop_word,
-                       uint32_t token, uint32_t budget) {
+                       uint32_t token, uint32_t budget, uint32_t fpu) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint32_t row_of_all[G][S], y_of_all[G][S];
   constexpr int kWarps = kWsWarps - 1;  // consumer warps; warp kWarps of a pipeline is its producer
@@ -421,6 +421,10 @@ __global__ void __launch_bounds__(G * kWsWarps * 32, kWsPipes / G)
     if (lane == 0) {
       const uint64_t pol_stream = frk::policy_evict_first();
       const uint32_t base = PREEMPT ? counters[0] : 0u;  // advanced only after this launch
+      // Claims are units of `fpu` rows with the same y in consecutive frames
+      // (frames f0 .. f0+fpu-1), loaded into consecutive stages: consumers
+      // keep that y's watermark in registers across them.  PREEMPT: fpu = 1.
+      const uint32_t units = rows / fpu;
       auto take = [&]() -> uint32_t {
         if (!PREEMPT) return atomicAdd(&counters[0], 1u);
         if (frk::ld_relaxed_gpu(stop_word) >= token) return rows;  // paused: no new row
@@ -428,27 +432,34 @@ __global__ void __launch_bounds__(G * kWsWarps * 32, kWsPipes / G)
         if (t >= budget) return rows;
         return (base + t) % rows;  // base < rows, t < budget < 2^31
       };
-      uint32_t next = take(), done = 0;
+      uint32_t unit = take(), next = take(), j = 0, done = 0;
+      uint32_t fb = unit / static_cast<uint32_t>(dh), y = unit - fb * static_cast<uint32_t>(dh);
       for (uint32_t k = 0;; ++k) {
         const int s = static_cast<int>(k % S);
         if (k >= S) frk::mbar_wait(&empty[s], ((k / S) - 1) & 1u);
-        const uint32_t r = next;
-        row_of[s] = r;
-        if (r >= rows) {  // no more rows: this pipeline's consumers leave at this stage
+        if (unit >= units) {  // no more rows: this pipeline's consumers leave at this stage
+          row_of[s] = rows;
           frk::mbar_arrive(&meta[s]);
           if (!PREEMPT) asm volatile("griddepcontrol.launch_dependents;");
           break;
         }
-        const uint32_t img = r / static_cast<uint32_t>(dh);
-        const uint32_t y = r - img * static_cast<uint32_t>(dh);
+        const uint32_t img = fb * fpu + j;
+        const uint32_t r = img * static_cast<uint32_t>(dh) + y;
+        row_of[s] = r;
         y_of[s] = y;
         frk::mbar_arrive(&meta[s]);
-        next = take();  // consumed next iteration: the round trip overlaps this copy
         ++done;
         frk::mbar_arrive_expect_tx(&full[s], 2u * src_row);
         frk::bulk_g2s(stages + s * stage_bytes,
                       src + (static_cast<uint64_t>(img) * 2 * dh + 2 * y) * src_row, 2u * src_row,
                       &full[s], pol_stream);
+        if (++j == fpu) {  // next unit (claimed one ahead: its round trip overlapped these copies)
+          j = 0;
+          unit = next;
+          fb = unit / static_cast<uint32_t>(dh);
+          y = unit - fb * static_cast<uint32_t>(dh);
+          if (unit < units) next = take();
+        }
       }
       if (PREEMPT) {
         // every claimed row was loaded (a claim after the stop returns no row)
@@ -456,6 +467,8 @@ __global__ void __launch_bounds__(G * kWsWarps * 32, kWsPipes / G)
       }
     }
   } else {  // ---- consumers
+    uint32_t wc[4 * kWmVecs1];  // the cached watermark of y == last_y (one group per thread)
+    uint32_t last_y = 0xFFFFFFFFu;
     for (uint32_t k = 0;; ++k) {
       const int s = static_cast<int>(k % S);
       const uint32_t ph = (k / S) & 1u;
@@ -467,20 +480,37 @@ __global__ void __launch_bounds__(G * kWsWarps * 32, kWsPipes / G)
       const uint8_t* rb = ra + src_row;
       uint8_t* orow = dst + static_cast<uint64_t>(row) * out_row;
       bool waited = false;
-      for (int g = ctid; g < groups; g += kImgThreads) {
-        // watermark first (L2): its latency overlaps the copy still in flight
-        uint32_t wv[4 * kWmVecs1];
-        const uint4* pw = wmp + (y * static_cast<uint32_t>(kWmVecs1 * groups) + static_cast<uint32_t>(g));
+      if (groups <= kImgThreads) {
+        // one group per thread: the watermark stays in registers while the
+        // producer's units keep y (consecutive frames, same output row)
+        if (y != last_y && ctid < groups) {
+          const uint4* pw = wmp + (y * static_cast<uint32_t>(kWmVecs1 * groups) + static_cast<uint32_t>(ctid));
 #pragma unroll
-        for (int j = 0; j < kWmVecs1; ++j) {
-          const uint4 x = __ldg(pw + j * groups);
-          wv[4 * j + 0] = x.x; wv[4 * j + 1] = x.y; wv[4 * j + 2] = x.z; wv[4 * j + 3] = x.w;
+          for (int j = 0; j < kWmVecs1; ++j) {
+            const uint4 x = __ldg(pw + j * groups);
+            wc[4 * j + 0] = x.x; wc[4 * j + 1] = x.y; wc[4 * j + 2] = x.z; wc[4 * j + 3] = x.w;
+          }
         }
-        if (!waited) {
-          frk::mbar_wait(&full[s], ph);
-          waited = true;
+        last_y = y;
+        frk::mbar_wait(&full[s], ph);
+        waited = true;
+        if (ctid < groups) img_group8_dp<true>(ra, rb, wc, orow + 24 * ctid, ctid);
+      } else {
+        for (int g = ctid; g < groups; g += kImgThreads) {  // wide rows: > 1 group per thread
+          // watermark first (L2): its latency overlaps the copy still in flight
+          uint32_t wv[4 * kWmVecs1];
+          const uint4* pw = wmp + (y * static_cast<uint32_t>(kWmVecs1 * groups) + static_cast<uint32_t>(g));
+#pragma unroll
+          for (int j = 0; j < kWmVecs1; ++j) {
+            const uint4 x = __ldg(pw + j * groups);
+            wv[4 * j + 0] = x.x; wv[4 * j + 1] = x.y; wv[4 * j + 2] = x.z; wv[4 * j + 3] = x.w;
+          }
+          if (!waited) {
+            frk::mbar_wait(&full[s], ph);
+            waited = true;
+          }
+          img_group8_dp<true>(ra, rb, wv, orow + 24 * g, g);
         }
-        img_group8_dp<true>(ra, rb, wv, orow + 24 * g, g);
       }
       if (!waited) frk::mbar_wait(&full[s], ph);  // lanes with no group still release in order
       __syncwarp();
@@ -600,7 +630,7 @@ constexpr uint32_t kImgCtrSlots = 64;
 
 namespace {
 using ImgKernel = void (*)(const uint8_t*, uint8_t*, const uint4*, int, int, uint32_t, uint32_t*,
-                           const uint32_t*, uint32_t, uint32_t);
+                           const uint32_t*, uint32_t, uint32_t, uint32_t);
 template <bool PREEMPT>
 ImgKernel img_kernel(int stages, int math, bool ws, int pipes) {
   if (ws) return pipes == 1 ? img_resize2x_wm_ws<3, PREEMPT, 1> : img_resize2x_wm_ws<3, PREEMPT, kWsPipes>;
@@ -807,8 +837,12 @@ int fr_img_resize_watermark_prepared(const fr_img_plan* plan, const uint8_t* src
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = pdl ? 1 : 0;
+    // frames per claimed unit (same output row in consecutive frames: the
+    // watermark is loaded once per unit); must divide the launch's frames
+    const uint32_t fpu = n % 4 == 0 ? 4u : n % 2 == 0 ? 2u : 1u;
     FR_CUDA_TRY(cudaLaunchKernelEx(&cfg, k, src, dst, static_cast<const uint4*>(prepared), plan->dw, plan->dh,
-                                   static_cast<uint32_t>(rows), ctr, static_cast<const uint32_t*>(nullptr), 0u, 0u));
+                                   static_cast<uint32_t>(rows), ctr, static_cast<const uint32_t*>(nullptr), 0u, 0u,
+                                   plan->ws ? fpu : 1u));
   } else {
     const int64_t total = static_cast<int64_t>(n) * plan->dw * plan->dh;
     img_resize_wm_general<<<grid_for(total, 256, 8), 256, 0, s>>>(
@@ -844,7 +878,7 @@ int fr_img_resize_watermark_preemptible(const fr_img_plan* plan, const uint8_t* 
   plan->chained = false;
   k<<<grid, plan->block(), plan->smem, static_cast<cudaStream_t>(stream)>>>(
       src, dst, static_cast<const uint4*>(prepared), plan->dw, plan->dh, static_cast<uint32_t>(rows),
-      counters, word, token, static_cast<uint32_t>(max_rows));
+      counters, word, token, static_cast<uint32_t>(max_rows), 1u);
   FR_CUDA_LAUNCHED("img_resize_watermark_preemptible");
   return FR_OK;
 }

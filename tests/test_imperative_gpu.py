@@ -51,6 +51,10 @@ def test_preempted_then_resumed_is_bit_exact(g, batch):
     src, wm, want = batch
     n = src.shape[0]
     plan = g.ImagePlan(3840, 2160, 1920, 1080)
+    # leave SMs free for the stopper: the fill_ below is a new launch, and the
+    # workload's CTAs fill every register file they sit on (in the runtime the
+    # stop word is raised by the stage's resident gap kernel instead)
+    plan.set_max_sms(100)
     prep = plan.prepare(wm)
     lo = g.low_priority_stream()
     hi = torch.cuda.Stream(priority=torch.cuda.Stream.priority_range()[1])
