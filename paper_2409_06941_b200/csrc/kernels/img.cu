@@ -838,8 +838,14 @@ int fr_img_resize_watermark_prepared(const fr_img_plan* plan, const uint8_t* src
     cfg.attrs = at;
     cfg.numAttrs = pdl ? 1 : 0;
     // frames per claimed unit (same output row in consecutive frames: the
-    // watermark is loaded once per unit); must divide the launch's frames
-    const uint32_t fpu = n % 4 == 0 ? 4u : n % 2 == 0 ? 2u : 1u;
+    // watermark is loaded once per unit): the largest of 16/8/4/2 that divides
+    // the launch's frames and still leaves >= 8 units per CTA (load balance)
+    uint32_t fpu = 1;
+    for (uint32_t f : {16u, 8u, 4u, 2u})
+      if (n % static_cast<int32_t>(f) == 0 && rows / f >= 8 * static_cast<int64_t>(grid)) {
+        fpu = f;
+        break;
+      }
     FR_CUDA_TRY(cudaLaunchKernelEx(&cfg, k, src, dst, static_cast<const uint4*>(prepared), plan->dw, plan->dh,
                                    static_cast<uint32_t>(rows), ctr, static_cast<const uint32_t*>(nullptr), 0u, 0u,
                                    plan->ws ? fpu : 1u));
