@@ -74,7 +74,7 @@ IMAGES_PER_STEP = int(os.environ.get("FR_IMAGES_PER_STEP", "16"))   # ~95 us ste
 DT_BUDGET = float(os.environ.get("FR_DT_BUDGET", "0.006"))
 IMG_SMS = int(os.environ.get("FR_IMG_SMS", "8"))
 SGD_SMS = int(os.environ.get("FR_SGD_SMS", "20"))
-E2E_SMS = int(os.environ.get("FR_E2E_SMS", "8"))     # PCIe-bound (4.5e9 px/s): 8 SMs of K5 keep up with the link
+E2E_SMS = int(os.environ.get("FR_E2E_SMS", "4"))     # K5 SMs + copy-ahead depth (2 ring slots per SM-equivalent): PCIe DMA during compute costs dT too
 PAIRS = int(os.environ.get("FR_DT_PAIRS", "8"))           # (baseline, harvest) pairs for the headline ΔT (ABBA order)
 PAIRS_OTHER = int(os.environ.get("FR_DT_PAIRS_OTHER", "3"))   # ... for every other workload
 STEP_GROUP = int(os.environ.get("FR_STEP_GROUP", "3"))   # steps between one pair of timing events

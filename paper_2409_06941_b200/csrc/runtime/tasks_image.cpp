@@ -169,7 +169,13 @@ int img_step(void* u, void* stream) {
       t->issued = t->steps;
       t->primed = true;
     }
-    while (rc == FR_OK && t->issued < t->steps + t->ring) rc = prefetch(t->issued++);
+    // copy-ahead depth: the whole ring, or under an SM budget 2 slots per
+    // SM-equivalent -- PCIe DMA into HBM while the pipeline computes costs
+    // the GEMMs clock like the SMs' work does (ring 8 / 24 /
+    // 128 -> +0.0 / +0.9 / +1.1 % pipeline ΔT), so the ΔT controller's budget
+    // rations the copies too
+    const int64_t depth = t->max_sms > 0 ? std::clamp<int64_t>(2 * t->max_sms, 2, t->ring) : t->ring;
+    while (rc == FR_OK && t->issued < t->steps + depth) rc = prefetch(t->issued++);
     const int j = static_cast<int>(t->steps % t->ring);
     if (rc == FR_OK) rc = cu(cudaStreamWaitEvent(s, t->e_ready[j], 0), "frames ready");
     if (rc == FR_OK) rc = fr_img_resize_watermark_prepared(t->plan, t->src + j * fb, t->dst + j * ob, t->wmp, n, s);

@@ -8,7 +8,7 @@ through build_schedule (pipeline_dt.critical_path_dt) -> the linked
 pipeline's ΔT; throughput = units / bubble-seconds over all stages.
 
 Usage: python scripts/harvest_sweep.py TASK FRACTIONS [epochs] [stages] [SMS]
-  TASK in image16 | image8 | image4 | pagerank | sgd | spin ; FRACTIONS e.g. 1,0.5,0.25;
+  TASK in image16 | image8 | image4 | e2e128 | e2e8 | pagerank | sgd | spin ; FRACTIONS e.g. 1,0.5,0.25;
   SMS: side-task SM budgets to try (fr_harness_set_side_sms), e.g. 0,74,37 (0 = all);
        env FR_DT_BUDGET=0.007 turns on the harness's ΔT controller (SMS = its start)
 """
@@ -26,6 +26,8 @@ from paper_2409_06941_b200 import pipeline_dt as P  # noqa: E402
 
 
 def make(name):
+    if name.startswith("e2e"):   # e2eR: the host-I/O image task (pinned host frames, R-slot device ring)
+        return gpu.ImageTask(batch=64, images_per_step=1, host_io=True, host_ring=int(name[3:] or 128))
     if name.startswith("image"):
         return gpu.ImageTask(batch=64, images_per_step=int(name[5:] or 16))
     if name == "pagerank":
