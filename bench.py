@@ -81,7 +81,7 @@ STEP_GROUP = int(os.environ.get("FR_STEP_GROUP", "3"))   # steps between one pai
 E2E_IMAGES_PER_STEP = 1
 E2E_RING = int(os.environ.get("FR_E2E_RING", "128"))   # device staging slots: the copy engines run ahead of the steps
 OUT_PX = FRAMES["dw"] * FRAMES["dh"]
-K5_WARP_INSTR_PER_PX = 0.982   # img_resize2x_wm_ws, ncu instruction count (profiles/r2s_k5ws_ncu.txt; round 1: 1.434)
+K5_WARP_INSTR_PER_PX = 0.938   # img_resize2x_wm_ws in a harvest on all SMs, ncu instruction count (profiles/r2s_k5ws_harvest_ncu.txt; round 1: 1.434)
 PR = dict(scale=20, edge_factor=16, seed=1, iters_per_step=2)
 SGD = dict(V=3072441, E=117185083, k=16, edge_seed=2, init_seed=3,
            edges_per_step=int(os.environ.get("FR_SGD_EDGES_PER_STEP", str(1 << 22))))
