@@ -111,21 +111,29 @@ __global__ void col_perm_kernel(const uint64_t* __restrict__ sorted, int32_t V,
 }
 
 // In-degree bucket: 7 = split (> kSplitEdges), 6..1 = g = 32..1 lanes per
-// row (smallest power of two with 4g >= deg), 0 = no in-edges.
-__host__ __device__ __forceinline__ int row_bucket(int32_t d, int32_t split_edges) {
+// row (smallest power of two with E g >= deg, E = lane_edges()), 0 = no in-edges.
+int lane_edges() {
+  static const int v = [] {
+    const char* e = std::getenv("FR_PR_LANE_EDGES");  // tuning hook: 4, 8 (default) or 16
+    const int x = e ? std::atoi(e) : 8;
+    return x == 4 || x == 16 ? x : 8;
+  }();
+  return v;
+}
+__host__ __device__ __forceinline__ int row_bucket(int32_t d, int32_t split_edges, int32_t lane_e) {
   if (d > split_edges) return 7;
   if (d == 0) return 0;
   int k = 0;
-  while (k < 5 && (4 << k) < d) ++k;
+  while (k < 5 && (lane_e << k) < d) ++k;
   return k + 1;
 }
 
 // Row order: bucket descending, then column id (keeps c' stores of a warp close).
 __global__ void row_keys_kernel(const int32_t* __restrict__ indeg,
                                 const int32_t* __restrict__ colid, int32_t V, int32_t split_edges,
-                                uint64_t* __restrict__ keys) {
+                                int32_t lane_e, uint64_t* __restrict__ keys) {
   for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x)
-    keys[v] = (static_cast<uint64_t>(7 - row_bucket(indeg[v], split_edges)) << 40) |
+    keys[v] = (static_cast<uint64_t>(7 - row_bucket(indeg[v], split_edges, lane_e)) << 40) |
               (static_cast<uint64_t>(static_cast<uint32_t>(colid[v])) << 8) |
               0u;  // low byte unused
 }
@@ -531,7 +539,7 @@ int build_work(fr_pr_graph* g, cudaStream_t s) {
   FR_CUDA_TRY(cudaStreamSynchronize(s));
   int32_t count[8] = {};
   const int split = split_edges();
-  for (int32_t r = 0; r < g->V; ++r) ++count[row_bucket(off[r + 1] - off[r], split)];
+  for (int32_t r = 0; r < g->V; ++r) ++count[row_bucket(off[r + 1] - off[r], split, lane_edges())];
   // rows are sorted by bucket descending: bucket 7 first
   int32_t at = 0;
   for (int b = 7; b >= 0; --b) {
@@ -693,7 +701,7 @@ int build_graph(int32_t Vn, int64_t m, const int32_t* user_src, const int32_t* u
     step(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, vkeys, vkeys + V, g->V, 0, 63, s), "column sort");
     col_perm_kernel<<<gv, 256, 0, s>>>(vkeys + V, g->V, colid);
     col_inv_kernel<<<gv, 256, 0, s>>>(vkeys + V, g->V, colinv);
-    row_keys_kernel<<<gv, 256, 0, s>>>(indeg, colid, g->V, split_edges(), vkeys);
+    row_keys_kernel<<<gv, 256, 0, s>>>(indeg, colid, g->V, split_edges(), lane_edges(), vkeys);
     step(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, vkeys, vkeys + V, g->V, 8, 43, s), "row sort");
     row_perm_kernel<<<gv, 256, 0, s>>>(vkeys + V, g->V, colinv, g->outdeg, indeg, rowof, g->rowc,
                                        g->rowr, g->rinv, rindeg);
