@@ -384,7 +384,16 @@ __global__ void __launch_bounds__(kImgThreads, CPS)
 //    3 small CTAs per SM the block scheduler spreads 3n CTAs over 3n SMs).
 constexpr int kWsWarps = kImgThreads / 32 + 1;  // per pipeline: 8 consumers + the producer
 
-template <int S, bool PREEMPT, int G>
+// CHAOS (tests only, FR_IMG_CHAOS=1): pseudo-random nanosleeps at every
+// hand-off (producer before publishing a row, consumers after taking one and
+// before releasing the stage), so any ordering the mbarriers did not enforce
+// would show up as a wrong byte.
+__device__ __forceinline__ void chaos_sleep(uint32_t a, uint32_t b) {
+  const uint32_t h = static_cast<uint32_t>(frk::splitmix64((static_cast<uint64_t>(a) << 32) ^ b ^ clock()));
+  __nanosleep(h & 4095u);
+}
+
+template <int S, bool PREEMPT, int G, bool CHAOS = false>
 __global__ void __launch_bounds__(G * kWsWarps * 32, kWsPipes / G)
     img_resize2x_wm_ws(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
                        const uint4* __restrict__ wmp, int dw, int dh, uint32_t rows,
@@ -437,6 +446,7 @@ __global__ void __launch_bounds__(G * kWsWarps * 32, kWsPipes / G)
       for (uint32_t k = 0;; ++k) {
         const int s = static_cast<int>(k % S);
         if (k >= S) frk::mbar_wait(&empty[s], ((k / S) - 1) & 1u);
+        if (CHAOS) chaos_sleep(blockIdx.x * 64 + pipe, k);
         if (unit >= units) {  // no more rows: this pipeline's consumers leave at this stage
           row_of[s] = rows;
           frk::mbar_arrive(&meta[s]);
@@ -473,6 +483,7 @@ __global__ void __launch_bounds__(G * kWsWarps * 32, kWsPipes / G)
       const int s = static_cast<int>(k % S);
       const uint32_t ph = (k / S) & 1u;
       frk::mbar_wait(&meta[s], ph);
+      if (CHAOS) chaos_sleep(blockIdx.x * 64 + warp + 16 * pipe, k);
       const uint32_t row = row_of[s];
       if (row >= rows) break;
       const uint32_t y = y_of[s];
@@ -513,6 +524,7 @@ __global__ void __launch_bounds__(G * kWsWarps * 32, kWsPipes / G)
         }
       }
       if (!waited) frk::mbar_wait(&full[s], ph);  // lanes with no group still release in order
+      if (CHAOS) chaos_sleep(blockIdx.x * 64 + warp + 16 * pipe, k + 0x10000u);
       __syncwarp();
       if (lane == 0) frk::mbar_arrive(&empty[s]);
     }
@@ -632,7 +644,8 @@ namespace {
 using ImgKernel = void (*)(const uint8_t*, uint8_t*, const uint4*, int, int, uint32_t, uint32_t*,
                            const uint32_t*, uint32_t, uint32_t, uint32_t);
 template <bool PREEMPT>
-ImgKernel img_kernel(int stages, int math, bool ws, int pipes) {
+ImgKernel img_kernel(int stages, int math, bool ws, int pipes, bool chaos = false) {
+  if (ws && chaos) return img_resize2x_wm_ws<3, PREEMPT, 1, true>;
   if (ws) return pipes == 1 ? img_resize2x_wm_ws<3, PREEMPT, 1> : img_resize2x_wm_ws<3, PREEMPT, kWsPipes>;
   if (math == 1)
     return stages == 2 ? img_resize2x_wm_tma<2, PREEMPT, 3, 1> : img_resize2x_wm_tma<3, PREEMPT, 2, 1>;
@@ -652,6 +665,7 @@ struct fr_img_plan {
   // Spread CTAs harvest ~40 % more pixels at the same pipeline ΔT
   // (gpurun_out/r2s_ctrl_pipes.log).
   int pipes = 1;
+  bool chaos = false;  // FR_IMG_CHAOS=1 (tests): the ws kernel with random sleeps at every hand-off
   int32_t* d_tab = nullptr;
   void* d_wm = nullptr;  // plan-owned prepared watermark for fr_img_resize_watermark
   uint32_t* d_ctr = nullptr;  // dynamic row scheduler {next row, CTAs done} x kImgCtrSlots; one stream at a time
@@ -703,14 +717,16 @@ int fr_img_plan_create(int32_t sw, int32_t sh, int32_t dw, int32_t dh, fr_img_pl
     if (const char* m = std::getenv("FR_IMG_MATH")) plan->math = std::atoi(m) == 0 ? 0 : 1;
     if (plan->math == 0) plan->ws = false;  // the warp-decoupled kernel has the dp4a math only
     if (const char* e = std::getenv("FR_IMG_PIPES")) plan->pipes = std::atoi(e) == kWsPipes ? kWsPipes : 1;
+    if (const char* e = std::getenv("FR_IMG_CHAOS")) plan->chaos = std::atoi(e) != 0;
+    if (plan->chaos) plan->pipes = 1;
     if (plan->ws) plan->stages = 3, plan->ctas_per_sm = kWsPipes / plan->pipes;
     plan->smem = plan->ws ? plan->pipes * plan->stages * (al(12 * dw) + 24)
                           : plan->stages * (al(12 * dw) + al(3 * dw)) + plan->stages * 8;
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     if (plan->smem <= optin) {
-      for (const void* fn : {reinterpret_cast<const void*>(img_kernel<false>(plan->stages, plan->math, plan->ws, plan->pipes)),
-                             reinterpret_cast<const void*>(img_kernel<true>(plan->stages, plan->math, plan->ws, plan->pipes))}) {
+      for (const void* fn : {reinterpret_cast<const void*>(img_kernel<false>(plan->stages, plan->math, plan->ws, plan->pipes, plan->chaos)),
+                             reinterpret_cast<const void*>(img_kernel<true>(plan->stages, plan->math, plan->ws, plan->pipes, plan->chaos))}) {
         if (e == cudaSuccess)
           e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, plan->smem);
         if (e == cudaSuccess)
@@ -814,7 +830,7 @@ int fr_img_resize_watermark_prepared(const fr_img_plan* plan, const uint8_t* src
     const int64_t rows = static_cast<int64_t>(n) * plan->dh;
     if (rows >= (int64_t{1} << 31)) return frcapi::fail(FR_ERR_UNSUPPORTED, "too many rows in one step");
     const int grid = static_cast<int>(std::min<int64_t>(rows, plan->grid_sms() * plan->ctas_per_sm));
-    const ImgKernel k = img_kernel<false>(plan->stages, plan->math, plan->ws, plan->pipes);
+    const ImgKernel k = img_kernel<false>(plan->stages, plan->math, plan->ws, plan->pipes, plan->chaos);
     // Consecutive steps overlap their tail and head (programmatic dependent
     // launch: a launch's CTAs start once every CTA of the previous one took
     // its last row).  Steps touch different frames; the row counters rotate
@@ -880,7 +896,7 @@ int fr_img_resize_watermark_preemptible(const fr_img_plan* plan, const uint8_t* 
   // no preempt: a stop word that never fires (counters[5] stays 0 < token)
   const uint32_t* word = preempt && preempt->stop_word ? preempt->stop_word : counters + 5;
   const uint32_t token = preempt && preempt->stop_word ? preempt->token : 0xFFFFFFFFu;
-  const ImgKernel k = img_kernel<true>(plan->stages, plan->math, plan->ws, plan->pipes);
+  const ImgKernel k = img_kernel<true>(plan->stages, plan->math, plan->ws, plan->pipes, plan->chaos);
   plan->chained = false;
   k<<<grid, plan->block(), plan->smem, static_cast<cudaStream_t>(stream)>>>(
       src, dst, static_cast<const uint4*>(prepared), plan->dw, plan->dh, static_cast<uint32_t>(rows),

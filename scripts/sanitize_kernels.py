@@ -26,6 +26,26 @@ for i in range(3):
 plan.set_overlap(False)
 ctr = torch.zeros(8, dtype=torch.int32, device="cuda")
 plan.run_preemptible(src, dst, prep, ctr, max_rows=700, stream=s)
+# round 2: every exact-2x variant (plan-creation knobs), frame units (a small
+# SM budget so a 4-frame launch claims 4-frame units), the preemptible path
+for env in ({}, {"FR_IMG_PIPES": "3"}, {"FR_IMG_CFG": "bar"}, {"FR_IMG_MATH": "0"}):
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    pv = gpu.ImagePlan(640, 360, 320, 180)
+    for k, v in old.items():
+        if v is None:
+            os.environ.pop(k)
+        else:
+            os.environ[k] = v
+    pp = pv.prepare(wm, stream=s)
+    src4 = gpu.img_generate(4, 640, 360, seed=9)
+    dst4 = torch.empty((4, 180, 320, 3), dtype=torch.uint8, device="cuda")
+    pv.run_prepared(src4, dst4, pp, stream=s)
+    pv.set_max_sms(2)
+    pv.run_prepared(src4, dst4, pp, stream=s)
+    c4 = torch.zeros(8, dtype=torch.int32, device="cuda")
+    pv.run_preemptible(src4, dst4, pp, c4, max_rows=500, stream=s)
+    s.synchronize()
 gen = gpu.ImagePlan(300, 200, 170, 90)
 src2 = gpu.img_generate(2, 300, 200, seed=3)
 wm2 = gpu.img_generate_watermark(170, 90, seed=4)

@@ -144,3 +144,32 @@ def test_full_batch_64_bit_exact(g, sidetask_oracle, monkeypatch, variant):
     got = dst.cpu().numpy()
     want = sidetask_oracle.img_resize_watermark(src.cpu().numpy(), wm.cpu().numpy(), 1920, 1080)
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("budget", [0, 3])
+def test_ws_kernel_under_chaos_is_bit_exact(g, sidetask_oracle, monkeypatch, budget):
+    """The warp-specialised K5 hands rows and stages between its producer and
+    consumer warps on mbarriers only (no CTA barrier; compute-sanitizer's
+    racecheck does not model mbarrier ordering and reports those hand-offs).
+    With FR_IMG_CHAOS=1 every hand-off sleeps a pseudo-random 0-4 us first, so
+    an ordering the mbarriers did not enforce would corrupt output bytes.
+    budget 3: 9 CTAs, so a 16-frame launch claims 16-frame units."""
+    monkeypatch.setenv("FR_IMG_CHAOS", "1")
+    plan = g.ImagePlan(3840, 2160, 1920, 1080)
+    plan.set_max_sms(budget)
+    src = g.img_generate(16, 3840, 2160, seed=31)
+    wm = g.img_generate_watermark(1920, 1080, seed=32)
+    prep = plan.prepare(wm)
+    dst = torch.empty((16, 1080, 1920, 3), dtype=torch.uint8, device="cuda")
+    want = sidetask_oracle.img_resize_watermark(src.cpu().numpy(), wm.cpu().numpy(), 1920, 1080)
+    for _ in range(2):
+        dst.zero_()
+        plan.run_prepared(src, dst, prep)
+        torch.cuda.synchronize()
+        assert np.array_equal(dst.cpu().numpy(), want)
+    # the preemptible path (one-row claims) under the same chaos
+    ctr = torch.zeros(8, dtype=torch.int32, device="cuda")
+    dst.zero_()
+    plan.run_preemptible(src, dst, prep, ctr)
+    torch.cuda.synchronize()
+    assert np.array_equal(dst.cpu().numpy(), want)
