@@ -561,11 +561,14 @@ def emit(args, results, ws, names, csr):
     e2e = None
     if "image_e2e" in names:
         e2e = {"value": rate("image_e2e"), "unit": UNIT,
-               "h2d_bytes_per_step": sum(r["image_e2e"]["h2d"] for r in results) / (K * STAGES),
-               "d2h_bytes_per_step": sum(r["image_e2e"]["d2h"] for r in results) / (K * STAGES),
+               # a step = one 1F1B epoch of all 4 stages (replayed), as for the headline; the e2e leg runs
+               # K epochs in each of its PAIRS harvest runs
+               "h2d_bytes_per_step": sum(r["image_e2e"]["h2d"] for r in results) / (K * PAIRS),
+               "d2h_bytes_per_step": sum(r["image_e2e"]["d2h"] for r in results) / (K * PAIRS),
                **dT_fields("image_e2e"), "fill": fill("image_e2e"),
                "path": f"fr_image_task host_io=1: pinned host frames -> {E2E_RING}-slot device ring filled by the "
-                       "copy engines ahead of the steps (also while the pipeline computes) -> K5 -> D2H per frame"}
+                       "copy engines ahead of the steps (also while the pipeline computes; copy-ahead depth 2 slots "
+                       "per SM-equivalent of the ΔT controller's budget) -> K5 -> D2H per frame"}
     # PageRank and Graph-SGD kernel rooflines: on all SMs, launched by the
     # runtime in this run's bubbles (workloads *_full_gpu), like K5's; their
     # ΔT-controlled operating points are the workloads' values
