@@ -38,8 +38,10 @@ def main():
         kinds = P.issue_kinds(a, s, p, m)
         ok, _ = h.submit(name, make(name), profile_steps=16)
         assert ok
+        frac = float(os.environ.get("FR_HARVEST_FRACTION", "1"))   # the gate sees the first f of each bubble
         for n in smss:
             h.set_side_sms(n)
+            h.set_harvest_fraction(frac)
             h.run(2, False)
             h.run(2, True)
             try:
@@ -63,7 +65,8 @@ def main():
     for n in smss:
         R = res[n]
         d = [P.critical_path_dt(a, p, m, K, R["b"][i], R["w"][i])["dT"] for i in range(pairs)]
-        print(json.dumps({"task": name, "side_sms": n, "budget": budget, "units_per_bubble_s": R["units"] / R["bubble_s"],
+        print(json.dumps({"task": name, "side_sms": n, "budget": budget,
+                          "harvest_fraction": float(os.environ.get("FR_HARVEST_FRACTION", "1")), "units_per_bubble_s": R["units"] / R["bubble_s"],
                           "dT_mean": statistics.fmean(d), "dT_se": statistics.stdev(d) / len(d) ** 0.5,
                           "dT_pairs": d, "sensor_growth_mean": statistics.fmean(R["sensor"]),
                           "sms_mean": statistics.fmean(R["sms"])}), flush=True)
