@@ -30,8 +30,8 @@ def make(name):
         return gpu.ImageTask(batch=64, images_per_step=1, host_io=True, host_ring=int(name[3:] or 128))
     if name.startswith("image"):
         return gpu.ImageTask(batch=64, images_per_step=int(name[5:] or 16))
-    if name == "pagerank":
-        return gpu.PageRankTask(scale=20, edge_factor=16, seed=1, iters_per_step=2)
+    if name.startswith("pagerank"):   # pagerankN: N iterations per step (default 2)
+        return gpu.PageRankTask(scale=20, edge_factor=16, seed=1, iters_per_step=int(name[8:] or 2))
     if name == "sgd":
         return gpu.SgdTask(edges_per_step=1 << 22)
     if name == "spin":
