@@ -379,9 +379,12 @@ __global__ void __launch_bounds__(kImgThreads, CPS)
 //    (st.global.cs, 24 B per thread, 768 B per warp), so the whole smem
 //    budget is input (3 pipelines x 3 stages x 23 KB per SM); each warp
 //    releases the stage on empty[s] (one arrival per warp) and moves on;
-//  * a CTA holds G such pipelines (G x 9 warps, G x S stages) and the grid
-//    is one CTA per SM, so an SM budget of n launches n CTAs on n SMs (with
-//    3 small CTAs per SM the block scheduler spreads 3n CTAs over 3n SMs).
+//  * a CTA holds G such pipelines (G x 9 warps, G x S stages).  Default G = 1:
+//    up to 3 CTAs per SM, and an SM budget of n launches 3n CTAs, which the
+//    block scheduler spreads one per SM (measured the better use of a ΔT
+//    budget); G = 3 (FR_IMG_PIPES=3) packs one CTA per SM;
+//  * claims are units of up to 16 frames' row y (fpu), so the consumers'
+//    watermark stays in registers across a unit.
 constexpr int kWsWarps = kImgThreads / 32 + 1;  // per pipeline: 8 consumers + the producer
 
 // CHAOS (tests only, FR_IMG_CHAOS=1): pseudo-random nanosleeps at every
