@@ -1,3 +1,7 @@
+"""The GPU RunTrace of a short harvest (stage 2, image task, step groups 1 and
+3) with its gate / signal logs written to gpurun_out/, for checking
+replay_check verdicts by hand (the pause-stamp flake of round 2).
+Usage: python scripts/diag_trace.py"""
 import json, sys
 sys.path.insert(0, '.')
 from paper_2409_06941_b200 import gpu
