@@ -79,10 +79,15 @@ int fr_img_plan_path(const fr_img_plan* plan, int32_t* path);
 int fr_img_resize_watermark(const fr_img_plan* plan, const uint8_t* src, uint8_t* dst,
                             const uint8_t* wm_rgba, int32_t n, void* stream);
 /* The watermark is a task constant: prepare it once (InitSideTask) into the
- * plan's layout (TMA path: per pixel w*a+127 and 255-a in 16-bit lanes,
- * group-transposed, 8 B/px; general path: RGBA copy, 4 B/px) and run the
- * prepared variant per step.  fr_img_resize_watermark prepares into a
- * plan-owned buffer on every call. */
+ * plan's layout and run the prepared variant per step (exact-2x path: per
+ * pixel pair the premultiplied w*a+127 of the blend lanes [R0,B0] [G0,R1]
+ * [B1,G1] and the two 255-a, group-transposed, 10 B/px; 8 B/px with the
+ * round-1 math FR_IMG_MATH=0; general path: RGBA copy, 4 B/px -- always size
+ * the buffer with fr_img_prepared_bytes of the plan that runs it).
+ * fr_img_resize_watermark prepares into a plan-owned buffer on every call.
+ * Exact-2x launches claim rows in units of the same output row in up to 16
+ * consecutive frames (the consumers keep that row's watermark in registers);
+ * the output is byte-identical for any unit size, grid or SM budget. */
 int fr_img_prepared_bytes(const fr_img_plan* plan, int64_t* bytes);
 int fr_img_prepare_watermark(const fr_img_plan* plan, const uint8_t* wm_rgba, void* prepared,
                              void* stream);
