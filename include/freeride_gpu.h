@@ -93,17 +93,21 @@ int fr_img_prepare_watermark(const fr_img_plan* plan, const uint8_t* wm_rgba, vo
                              void* stream);
 int fr_img_resize_watermark_prepared(const fr_img_plan* plan, const uint8_t* src, uint8_t* dst,
                                      const void* prepared, int32_t n, void* stream);
-/* Preemptible K5 over a resident batch of n frames (fast 2x path only):
- * takes up to max_rows output rows, row (base + t) mod (n * dh) for the
- * t-th row taken, base = counters[0] -- so a launch may loop over the batch
- * and the next launch resumes at the first row this one did not take.
- * counters: 8 x uint32 of zeroed device memory owned by the caller (the
- * cursor, scheduler state, and counters[2..3] = rows completed, uint64).
- * Stops taking rows once *preempt->stop_word >= preempt->token (preempt may
- * be null); every row taken is completed before the launch ends. */
+/* Preemptible K5 over a resident batch of n frames (fast 2x path only).
+ * Work is claimed in units of U = fr_img_preemptible_unit_rows(plan, n) rows
+ * (the same output row of U consecutive frames; U depends on n only): a
+ * launch takes up to floor(max_rows / U) units, unit (base + t) mod
+ * (n * dh / U) for the t-th unit taken, base = counters[0] -- so a launch may
+ * loop over the batch and the next launch resumes at the first unit this one
+ * did not take.  counters: 8 x uint32 of zeroed device memory owned by the
+ * caller (the unit cursor, scheduler state, and counters[2..3] = rows
+ * completed, uint64).  Stops taking units once *preempt->stop_word >=
+ * preempt->token (preempt may be null); every unit taken is completed
+ * before the launch ends. */
 int fr_img_resize_watermark_preemptible(const fr_img_plan* plan, const uint8_t* src, uint8_t* dst,
                                         const void* prepared, int32_t n, uint32_t* counters,
                                         int64_t max_rows, const fr_preempt* preempt, void* stream);
+int fr_img_preemptible_unit_rows(const fr_img_plan* plan, int32_t n, int32_t* rows);
 /* synthetic inputs (same counter-based arithmetic as oracle/sidetasks.c) */
 int fr_img_generate(uint8_t* dst, int32_t n, int32_t w, int32_t h, int32_t channels,
                     uint64_t seed, int32_t first_index, void* stream);

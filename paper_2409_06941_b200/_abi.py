@@ -446,6 +446,7 @@ GPU_PROTOTYPES = {
     "fr_img_prepare_watermark": (C.c_int, [vp, vp, vp, vp]),
     "fr_img_resize_watermark_prepared": (C.c_int, [vp, vp, vp, vp, i32, vp]),
     "fr_img_resize_watermark_preemptible": (C.c_int, [vp, vp, vp, vp, i32, vp, i64, vp, vp]),
+    "fr_img_preemptible_unit_rows": (C.c_int, [vp, i32, P(i32)]),
     "fr_img_generate": (C.c_int, [vp, i32, i32, i32, i32, u64, i32, vp]),
     "fr_img_generate_watermark": (C.c_int, [vp, i32, i32, u64, vp]),
 }

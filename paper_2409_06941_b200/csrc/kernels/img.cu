@@ -435,14 +435,16 @@ __global__ void __launch_bounds__(G * kWsWarps * 32, kWsPipes / G)
       const uint32_t base = PREEMPT ? counters[0] : 0u;  // advanced only after this launch
       // Claims are units of `fpu` rows with the same y in consecutive frames
       // (frames f0 .. f0+fpu-1), loaded into consecutive stages: consumers
-      // keep that y's watermark in registers across them.  PREEMPT: fpu = 1.
+      // keep that y's watermark in registers across them.  PREEMPT counts in
+      // units too: base = counters[0] and the budget are units, unit
+      // (base + t) mod units is the t-th taken.
       const uint32_t units = rows / fpu;
       auto take = [&]() -> uint32_t {
         if (!PREEMPT) return atomicAdd(&counters[0], 1u);
-        if (frk::ld_relaxed_gpu(stop_word) >= token) return rows;  // paused: no new row
+        if (frk::ld_relaxed_gpu(stop_word) >= token) return units;  // paused: no new unit
         const uint32_t t = atomicAdd(&counters[4], 1u);
-        if (t >= budget) return rows;
-        return (base + t) % rows;  // base < rows, t < budget < 2^31
+        if (t >= budget) return units;
+        return (base + t) % units;  // base < units, t < budget < 2^31
       };
       uint32_t unit = take(), next = take(), j = 0, done = 0;
       uint32_t fb = unit / static_cast<uint32_t>(dh), y = unit - fb * static_cast<uint32_t>(dh);
@@ -539,7 +541,7 @@ __global__ void __launch_bounds__(G * kWsWarps * 32, kWsPipes / G)
       if (PREEMPT) {
         const uint32_t base = counters[0];
         const uint32_t taken = min(atomicAdd(&counters[4], 0u), budget);
-        counters[0] = static_cast<uint32_t>((static_cast<uint64_t>(base) + taken) % rows);
+        counters[0] = static_cast<uint32_t>((static_cast<uint64_t>(base) + taken) % (rows / fpu));
         counters[4] = 0;
       } else {
         counters[0] = 0;
@@ -691,6 +693,15 @@ struct fr_img_plan {
     return static_cast<size_t>(dw) * dh * (math == 1 ? 2 * kWmVecs1 : 8);
   }
 };
+
+namespace {
+// rows per claimed unit of a preemptible launch over n frames (fixed by n,
+// so every launch of one workload counts its cursor in the same unit)
+uint32_t preemptible_fpu(const fr_img_plan* plan, int32_t n) {
+  if (!plan->ws) return 1;  // the round-1 kernel claims single rows
+  return n % 4 == 0 ? 4u : n % 2 == 0 ? 2u : 1u;
+}
+}  // namespace
 
 extern "C" {
 
@@ -878,6 +889,12 @@ int fr_img_resize_watermark_prepared(const fr_img_plan* plan, const uint8_t* src
   return FR_OK;
 }
 
+int fr_img_preemptible_unit_rows(const fr_img_plan* plan, int32_t n, int32_t* rows) {
+  if (!plan || !rows) return frcapi::fail(FR_ERR_ARGUMENT, "null argument");
+  *rows = static_cast<int32_t>(preemptible_fpu(plan, n));
+  return FR_OK;
+}
+
 int fr_img_resize_watermark_preemptible(const fr_img_plan* plan, const uint8_t* src, uint8_t* dst,
                                         const void* prepared, int32_t n, uint32_t* counters,
                                         int64_t max_rows, const fr_preempt* preempt, void* stream) {
@@ -901,9 +918,14 @@ int fr_img_resize_watermark_preemptible(const fr_img_plan* plan, const uint8_t* 
   const uint32_t token = preempt && preempt->stop_word ? preempt->token : 0xFFFFFFFFu;
   const ImgKernel k = img_kernel<true>(plan->stages, plan->math, plan->ws, plan->pipes, plan->chaos);
   plan->chained = false;
+  // units of fpu frames (the ws kernel; fixed by n alone, so every launch of
+  // a workload counts its cursor in the same unit): max_rows is taken in
+  // whole units
+  const uint32_t fpu = preemptible_fpu(plan, n);
+  if (max_rows < fpu) return FR_OK;
   k<<<grid, plan->block(), plan->smem, static_cast<cudaStream_t>(stream)>>>(
       src, dst, static_cast<const uint4*>(prepared), plan->dw, plan->dh, static_cast<uint32_t>(rows),
-      counters, word, token, static_cast<uint32_t>(max_rows), 1u);
+      counters, word, token, static_cast<uint32_t>(max_rows / fpu), fpu);
   FR_CUDA_LAUNCHED("img_resize_watermark_preemptible");
   return FR_OK;
 }

@@ -138,9 +138,10 @@ class ImagePlan:
     def run_preemptible(self, src, dst, prepared, counters, stop_word=None, token=0, max_rows=None,
                         stream=None):
         """Preemptible K5 (imperative interface): takes up to max_rows rows
-        (default: one pass) starting at row counters[0] (mod n*dh), stops
-        taking rows once stop_word[0] >= token; counters is a zeroed int32
-        tensor of 8 (counters[2:4] = rows completed, uint64)."""
+        (default: one pass) in units of preemptible_unit_rows(n) rows,
+        starting at unit counters[0] (mod n*dh / unit), stops taking units
+        once stop_word[0] >= token; counters is a zeroed int32 tensor of 8
+        (counters[2:4] = rows completed, uint64)."""
         n = src.shape[0]
         if tuple(src.shape[1:]) != (self.sh, self.sw, 3) or tuple(dst.shape) != (n, self.dh, self.dw, 3):
             raise ValueError("image shapes do not match the plan")
@@ -153,6 +154,12 @@ class ImagePlan:
             self._h, _ptr(src), _ptr(dst), _ptr(prepared), n, _ptr(counters), max_rows,
             C.byref(pre) if pre is not None else None, _stream(stream)))
         return dst
+
+    def preemptible_unit_rows(self, n: int) -> int:
+        """rows per claimed unit of a preemptible launch over n frames"""
+        out = C.c_int32()
+        check(glib().fr_img_preemptible_unit_rows(self._h, n, C.byref(out)))
+        return out.value
 
     def __del__(self):
         h = getattr(self, "_h", None)

@@ -28,6 +28,8 @@ from paper_2409_06941_b200 import pipeline_dt as P  # noqa: E402
 def make(name):
     if name.startswith("e2e"):   # e2eR: the host-I/O image task (pinned host frames, R-slot device ring)
         return gpu.ImageTask(batch=64, images_per_step=1, host_io=True, host_ring=int(name[3:] or 128))
+    if name.startswith("imp"):   # impN: the imperative (device-preempted) image task over a 64-frame batch
+        return gpu.ImageTask(batch=64, images_per_step=int(name[3:] or 16), imperative=True)
     if name.startswith("image"):
         return gpu.ImageTask(batch=64, images_per_step=int(name[5:] or 16))
     if name.startswith("pagerank"):   # pagerankN: N iterations per step (default 2)

@@ -75,7 +75,9 @@ def test_preempted_then_resumed_is_bit_exact(g, batch):
             t2.record(hi)
         torch.cuda.synchronize()
         first = rows_done(ctr)
-        assert int(ctr[0]) == first % (n * 1080)   # base advanced by the rows taken = completed
+        unit = plan.preemptible_unit_rows(n)
+        assert first % unit == 0                    # whole units only
+        assert int(ctr[0]) == (first // unit) % (n * 1080 // unit)   # base advanced by the units taken = completed
         end_us, stop_us = t0.elapsed_time(t1) * 1e3, t0.elapsed_time(t2) * 1e3
         if stop_us < end_us - 1.0:
             assert end_us - stop_us < 50.0          # exits within a few rows of the stop
@@ -96,9 +98,11 @@ def test_budget_loops_over_the_batch(g, batch):
     prep = plan.prepare(wm)
     dst = torch.zeros((n, 1080, 1920, 3), dtype=torch.uint8, device="cuda")
     ctr = torch.zeros(8, dtype=torch.int32, device="cuda")
+    unit = plan.preemptible_unit_rows(n)
+    assert unit == 4                                  # the same row of 4 consecutive frames
     plan.run_preemptible(src[:n], dst, prep, ctr, max_rows=2 * n * 1080 + 500)
     torch.cuda.synchronize()
-    assert rows_done(ctr) == 2 * n * 1080 + 500 and int(ctr[0]) == 500
+    assert rows_done(ctr) == 2 * n * 1080 + 500 and int(ctr[0]) == 500 // unit
     assert np.array_equal(dst.cpu().numpy(), want[:n])
 
 
