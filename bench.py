@@ -76,7 +76,7 @@ IMG_SMS = int(os.environ.get("FR_IMG_SMS", "8"))
 SGD_SMS = int(os.environ.get("FR_SGD_SMS", "20"))
 E2E_SMS = int(os.environ.get("FR_E2E_SMS", "4"))     # K5 SMs + copy-ahead depth (2 ring slots per SM-equivalent): PCIe DMA during compute costs dT too
 PAIRS = int(os.environ.get("FR_DT_PAIRS", "8"))           # (baseline, harvest) pairs for the headline ΔT (ABBA order)
-PAIRS_OTHER = int(os.environ.get("FR_DT_PAIRS_OTHER", "3"))   # ... for every other workload
+PAIRS_OTHER = int(os.environ.get("FR_DT_PAIRS_OTHER", "4"))   # ... for every other workload
 STEP_GROUP = int(os.environ.get("FR_STEP_GROUP", "3"))   # steps between one pair of timing events
 E2E_IMAGES_PER_STEP = 1
 E2E_RING = int(os.environ.get("FR_E2E_RING", "128"))   # device staging slots: the copy engines run ahead of the steps
@@ -386,10 +386,12 @@ def ours(args):
         for j in range(npairs - 1)]
     # per-pair pipeline ΔTs of the headline: their spread is the estimate's
     # standard error (the GPU's clock transients hit runs at random)
-    local_res["image"]["pair_dT"] = [
-        PD.critical_path_dt(A, STAGES, MICRO_BATCHES, K, {i: r_["ops_base_runs"][j] for i, r_ in enumerate(runs["image"])},
-                            {i: r_["ops_with_runs"][j] for i, r_ in enumerate(runs["image"])})["dT"]
-        for j in range(npairs)]
+    for n in names:   # every workload: its pairs' pipeline ΔTs (spread -> standard error)
+        npn = min(len(r_["ops_with_runs"]) for r_ in runs[n])
+        local_res[n]["pair_dT"] = [
+            PD.critical_path_dt(A, STAGES, MICRO_BATCHES, K, {i: r_["ops_base_runs"][j] for i, r_ in enumerate(runs[n])},
+                                {i: r_["ops_with_runs"][j] for i, r_ in enumerate(runs[n])})["dT"]
+            for j in range(npn)]
     local_res["clocks"] = clk.summary()
     local_res["l2_gbps"] = gpu.l2_read_gbps()   # PageRank's working set is L2-resident: its roofline
     local_res["gap_kernels"] = sum(r["train_ops"] // (2 * MICRO_BATCHES) * (2 * MICRO_BATCHES + 1)
@@ -438,6 +440,11 @@ def ours(args):
         mixed["dT_stage_max"] = max(x["dT"] for x in mixed["stages"])
         if len({r_["stage"] for r_ in mruns}) == STAGES:
             mixed["dT_pipeline"] = pipe_dt(mruns, STAGES, MICRO_BATCHES, K)["dT"]
+            mp = [PD.critical_path_dt(A, STAGES, MICRO_BATCHES, K, {r_["stage"]: r_["ops_base_runs"][j] for r_ in mruns},
+                                      {r_["stage"]: r_["ops_with_runs"][j] for r_ in mruns})["dT"]
+                  for j in range(min(len(r_["ops_with_runs"]) for r_ in mruns))]
+            mixed["dT_pairs"] = mp
+            mixed["dT_se"] = statistics.stdev(mp) / len(mp) ** 0.5 if len(mp) > 1 else None
         mixed["fill_mean"] = statistics.fmean(x["fill"] for x in mixed["stages"])
     local_res["mixed"] = mixed
     # configs[4] at N = 1: every stage of the 8-stage, m = 8 pipeline of
@@ -455,10 +462,14 @@ def ours(args):
             h.close()
             c5runs.append(dict(r, stage=s))
         pipe = pipe_dt(c5runs, 8, 8, K5)
+        c5_pairs = [PD.critical_path_dt(A, 8, 8, K5, {r_["stage"]: r_["ops_base_runs"][j] for r_ in c5runs},
+                                        {r_["stage"]: r_["ops_with_runs"][j] for r_ in c5runs})["dT"]
+                    for j in range(min(len(r_["ops_with_runs"]) for r_ in c5runs))]
         c5 = {"bubble_rate": prof["bubble_rate"], "fp_ms": prof["fp_ticks"] / 1e6, "bp_ms": prof["bp_ticks"] / 1e6,
               "epochs": K5, "side_sms_mean": statistics.fmean(r_["sms"] for r_ in c5runs),
               "units_per_bubble_s": sum(r_["with"]["work_units"] for r_ in c5runs) / sum(r_["base"]["bubble_s"] for r_ in c5runs),
-              "dT_pipeline": pipe["dT"],
+              "dT_pipeline": pipe["dT"], "dT_pairs": c5_pairs,
+              "dT_se": statistics.stdev(c5_pairs) / len(c5_pairs) ** 0.5 if len(c5_pairs) > 1 else None,
               "dT_stage_max": max((r_["with"]["makespan_s"] - r_["base"]["makespan_s"]) / r_["base"]["makespan_s"] for r_ in c5runs),
               "fill": sum(r_["with"]["used_s"] for r_ in c5runs) / sum(r_["with"]["bubble_s"] for r_ in c5runs)}
     local_res["c5"] = c5
@@ -516,11 +527,15 @@ def emit(args, results, ws, names, csr):
     def dT_stages(n):
         return max(x for r in results for x in r[n]["stage_dT"])
 
+    def se(xs):
+        return statistics.stdev(xs) / len(xs) ** 0.5 if len(xs) > 1 else None
+
     def dT_fields(n):
-        return {"dT": dT(n), "dT_stage_max": dT_stages(n),
+        pairs = results[0][n].get("pair_dT") or []
+        return {"dT": dT(n), "dT_se": se(pairs), "dT_pairs": pairs, "dT_stage_max": dT_stages(n),
                 "dT_stages": results[0][n]["stage_dT"], "side_sms_mean": results[0][n]["sms"],
                 "dt_budget": results[0][n]["budget"],
-                "dT_budget_met": dT(n) <= 0.01}
+                "dT_budget_met": (dT(n) <= 0.01) if results[0][n]["budget"] > 0 else None}
 
     def fill(n):
         return sum(r[n]["used"] for r in results) / sum(r[n]["bubble_with"] for r in results)
@@ -633,8 +648,7 @@ def emit(args, results, ws, names, csr):
         "dT_budget_met": dT("image") <= 0.01, "fill": fill("image"),
         "delta_t_pairs": PAIRS,
         "delta_t_pair_values": results[0]["image"]["pair_dT"],
-        "delta_t_se": (statistics.stdev(results[0]["image"]["pair_dT"]) / len(results[0]["image"]["pair_dT"]) ** 0.5
-                       if len(results[0]["image"]["pair_dT"]) > 1 else None),
+        "delta_t_se": se(results[0]["image"]["pair_dT"]),
         "delta_t_noise": {"null_dT": results[0]["image"]["null_dT"],
                           "how": "pipeline ΔT between the baseline runs (no side task in either) of successive ABBA pairs"},
         "overrun_frac": sum(r["image"]["overrun"] for r in results) / max(1e-12, sum(r["image"]["used"] for r in results)),
