@@ -341,7 +341,8 @@ def ours(args):
                     task = gpu.SgdTask(**SGD)
                 runs[n].append(harvest(h, n, task, K, W, sms=sms_of.get(n, 0), kinds=kinds,
                                        budget=0.0 if n.endswith("_full_gpu") else DT_BUDGET,
-                                       pairs=PAIRS if n in ("image", "image_e2e") else PAIRS_OTHER))
+                                       pairs=PAIRS if n in ("image", "image_e2e")
+                                       else 1 if n.endswith("_full_gpu") else PAIRS_OTHER))
             h.close()
     torch.cuda.synchronize()
     if dist:
