@@ -65,16 +65,6 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   return p;
 }
 
-// Global -> shared bulk copy without an L2 cache hint.
-__device__ __forceinline__ void bulk_g2s_nohint(void* smem_dst, const void* gmem_src, uint32_t bytes,
-                                                uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(smem_dst)),
-      "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
 // Global -> shared bulk copy; completion is counted in bytes on `bar`.
 // bytes and both addresses must be multiples of 16.
 __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gmem_src, uint32_t bytes,

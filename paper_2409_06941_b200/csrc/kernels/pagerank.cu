@@ -226,7 +226,6 @@ struct PrArgs {
   int32_t bstart[8];     // first row of bucket b (7 = split .. 1 = g 1), bstart[0] = tail
   int32_t istart[8];     // first item of bucket b = 6..1 (items of b-1 follow), istart[0] = total
   int32_t hot, V, do_tail;
-  int32_t hot_tma;       // stage the hot prefix by TMA bulk copies (FR_PR_HOT_TMA=0: LDG/STS)
   int32_t nlists;        // chunk lists (LPT at build, one per CTA of a full grid); a smaller
                          // grid (an SM budget) walks lists b, b + grid, ...
   double base, damp;
@@ -357,35 +356,16 @@ __global__ void __maxnreg__(kPrThreads >= 1024 ? 56 : 40) pr_pull_kernel(PrArgs 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // launched as a programmatic dependent of the previous iteration: the CTA
   // is resident early, but reads c_in only once that grid completed
-  __shared__ uint64_t hot_bar;
-  const bool tma_hot = a.hot_tma != 0;
-  if (tma_hot && tid == 0) {
-    frk::mbar_init(&hot_bar, 1);
-    frk::fence_mbar_init();
-  }
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (tma_hot) {
-    __syncthreads();
-    // the hot prefix by TMA bulk copies (16 KB pieces, no L2 hint), not 12
-    // LDG/STS pairs per thread: 51.6 -> 49.6 us per isolated iteration,
-    // 48.1 -> 47.5 us back to back (same box)
-    if (tid == 0 && a.hot > 0) {
-      const uint32_t bytes = static_cast<uint32_t>(a.hot) * 4u;
-      frk::mbar_arrive_expect_tx(&hot_bar, bytes);
-      for (uint32_t off = 0; off < bytes; off += 16384u)
-        frk::bulk_g2s_nohint(reinterpret_cast<char*>(hot4) + off, reinterpret_cast<const char*>(a.c_in) + off,
-                             min(16384u, bytes - off), &hot_bar);
-    }
-  } else {
+  {
     const float4* src = reinterpret_cast<const float4*>(a.c_in);
     for (int i = tid; i < (a.hot >> 2); i += kPrThreads) hot4[i] = __ldg(&src[i]);
-  }
-  if (tid < kMaxSlots) {
-    sacc[tid] = 0.0;
-    scnt[tid] = 0;
+    if (tid < kMaxSlots) {
+      sacc[tid] = 0.0;
+      scnt[tid] = 0;
+    }
   }
   __syncthreads();
-  if (tma_hot && a.hot > 0) frk::mbar_wait(&hot_bar, 0);
   // split-row chunks, software-pipelined: the next chunk's descriptor and
   // first 8 column ids per lane load while this chunk gathers
   for (int lb = blockIdx.x; lb < a.nlists; lb += gridDim.x) {
@@ -883,11 +863,6 @@ int fr_pr_step(fr_pr_state* st, int32_t iters, float damping, void* stream) {
   std::memcpy(a.bstart, g->bstart, sizeof(a.bstart));
   std::memcpy(a.istart, g->istart, sizeof(a.istart));
   a.hot = hot_vertices(g->V);
-  static const int hot_tma = [] {  // FR_PR_HOT_TMA=0: per-thread LDG/STS staging instead
-    const char* e = std::getenv("FR_PR_HOT_TMA");
-    return e ? std::atoi(e) : 1;
-  }();
-  a.hot_tma = hot_tma;
   a.V = g->V;
   a.damp = static_cast<double>(damping);
   a.base = (1.0 - static_cast<double>(damping)) / static_cast<double>(g->V);
