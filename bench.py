@@ -71,7 +71,7 @@ IMAGES_PER_STEP = int(os.environ.get("FR_IMAGES_PER_STEP", "16"))   # ~95 us ste
 # a bubble can take differs from box to box (image at a fixed 16 SMs: +0.3 %
 # on one, +1.6 % on another), so a fixed budget cannot hold the ΔT
 # everywhere.  FR_DT_BUDGET=0 runs the fixed budgets instead.
-DT_BUDGET = float(os.environ.get("FR_DT_BUDGET", "0.005"))
+DT_BUDGET = float(os.environ.get("FR_DT_BUDGET", "0.004"))
 IMG_SMS = int(os.environ.get("FR_IMG_SMS", "8"))
 SGD_SMS = int(os.environ.get("FR_SGD_SMS", "20"))
 E2E_SMS = int(os.environ.get("FR_E2E_SMS", "4"))     # K5 SMs + copy-ahead depth (2 ring slots per SM-equivalent): PCIe DMA during compute costs dT too
